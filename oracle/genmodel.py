@@ -1,0 +1,289 @@
+"""GenModel (oracle; test infrastructure only).
+
+T = A·α + B·β + C·γ + D·δ + max(w − w_t, 0)·B·ε
+
+  A  communication rounds (steps)
+  B  data through a link per step, here per rank max(sent, received)   (reading Q9)
+  C  reduce operations: a fan-in-f reduce of a block costs (f−1)·|block|
+  D  memory operations: a fan-in-f reduce of a block costs (f+1)·|block|
+  w  fan-in of the step: 1 + the most distinct senders into one receiver   (Q8)
+
+Units: bytes; α in seconds, β/γ/δ/ε in seconds per byte (Table 5's per-float values / 4,
+exact in binary; reading Q17).
+
+Two evaluations are provided and both are pinned by tests:
+  * exact rational (`fractions.Fraction`) — used for every identity the paper fixes
+    (Tables 1/2, Theorem 1/2, Eq. 6);
+  * fixed-order float64 — the contract the C-ABI library reproduces bit for bit
+    (DESIGN.md "cost evaluation order"):  per step  ((((α + B·β) + C·γ) + D·δ) + I·ε)  with
+    I = max(w − w_t, 0)·B formed in integers, steps summed in plan order; closed forms as
+    (((A·α + (Bn/den)·β) + (Cn/den)·γ) + (Dn/den)·δ) + (In/den)·ε with integer numerators.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from fractions import Fraction
+
+from .plans import Plan, block_size, is_pow2
+
+
+@dataclass(frozen=True)
+class Params:
+    """Per-byte GenModel parameters.  `combined` = fitted 2β+γ."""
+    alpha: float
+    beta: float
+    gamma: float
+    delta: float
+    epsilon: float
+    w_t: int
+    combined: float | None = None
+
+    def effective(self):
+        """(β, γ) actually used: with only 2β+γ known, β_eff = combined/2, γ_eff = 0
+        ("bandwidth=(B/2)·combined, compute=0"; exact in binary)."""
+        if self.combined is not None:
+            return self.combined * 0.5, 0.0
+        return self.beta, self.gamma
+
+
+def params_per_float(alpha, beta, gamma, delta, epsilon, w_t) -> Params:
+    """Table 5 units (per float) -> per byte."""
+    return Params(alpha, beta / 4, gamma / 4, delta / 4, epsilon / 4, w_t)
+
+
+@dataclass(frozen=True)
+class StepCoeffs:
+    A: int
+    B: int      # bytes
+    C: int      # bytes
+    D: int      # bytes
+    w: int
+
+
+@dataclass(frozen=True)
+class StepParams:
+    alpha: float
+    beta: float
+    epsilon: float
+    w_t: int
+    gamma: float
+    delta: float
+
+
+def step_coeffs(plan: Plan, esize: int) -> list:
+    """Per-step (A, B, C, D, w) of a plan.  Each quantity is the max over
+    ranks of that rank's per-step total (ranks run in parallel)."""
+    n, out = plan.n, []
+    for st in plan.steps:
+        sent, recv = [0] * n, [0] * n
+        senders = [set() for _ in range(n)]
+        for t in st.transfers:
+            sent[t.src] += t.size * esize
+            recv[t.dst] += t.size * esize
+            senders[t.dst].add(t.src)
+        cc, dd = [0] * n, [0] * n
+        for rd in st.reduces:
+            k = len(rd.inputs)
+            if k >= 2:
+                sz = block_size(plan.count, n, rd.block) * esize
+                cc[rd.server] += (k - 1) * sz
+                dd[rd.server] += (k + 1) * sz
+        B = max(max(sent), max(recv))
+        w = 1 + max(len(s) for s in senders)
+        out.append(StepCoeffs(1, B, max(cc), max(dd), w))
+    return out
+
+
+def uniform_step_params(p: Params, nsteps: int) -> list:
+    beta, gamma = p.effective()
+    return [StepParams(p.alpha, beta, p.epsilon, p.w_t, gamma, p.delta)] * nsteps
+
+
+def topo_step_params(topo, plan: Plan) -> list:
+    """Per-step parameters from the links the step's transfers traverse: max α, β, ε and
+    min w_t over traversed uplinks (reading Q16); γ, δ = max over servers.  Per byte."""
+    gamma = max(topo.nodes[s].compute["gamma"] for s in topo.servers) / 4
+    delta = max(topo.nodes[s].compute["delta"] for s in topo.servers) / 4
+    out = []
+    for st in plan.steps:
+        links = set()
+        for t in st.transfers:
+            links.update(topo.path_links(topo.servers[t.src], topo.servers[t.dst]))
+        if links:
+            ups = [topo.nodes[x].uplink for x in sorted(links)]
+            out.append(StepParams(max(u["alpha"] for u in ups), max(u["beta"] for u in ups) / 4,
+                                  max(u["epsilon"] for u in ups) / 4,
+                                  min(u["w_t"] for u in ups), gamma, delta))
+        else:
+            out.append(StepParams(0.0, 0.0, 0.0, 1 << 30, gamma, delta))
+    return out
+
+
+def _breakdown(lat, bw, comp, mem, inc, tot):
+    return {"latency": lat, "bandwidth": bw, "compute": comp, "memory": mem,
+            "incast": inc, "total": tot}
+
+
+def predict_exact(coeffs: list, sparams: list) -> dict:
+    """Exact rational GenModel of a plan, summed over steps."""
+    F = Fraction
+    lat = bw = comp = mem = inc = F(0)
+    for c, p in zip(coeffs, sparams):
+        lat += c.A * F(p.alpha)
+        bw += c.B * F(p.beta)
+        comp += c.C * F(p.gamma)
+        mem += c.D * F(p.delta)
+        inc += max(c.w - p.w_t, 0) * c.B * F(p.epsilon)
+    return _breakdown(lat, bw, comp, mem, inc, lat + bw + comp + mem + inc)
+
+
+def predict_f64(coeffs: list, sparams: list) -> dict:
+    """Fixed-order float64 GenModel (the library's contract, bit for bit)."""
+    lat = bw = comp = mem = inc = tot = 0.0
+    for c, p in zip(coeffs, sparams):
+        a = float(c.A) * p.alpha
+        b = float(c.B) * p.beta
+        g = float(c.C) * p.gamma
+        d = float(c.D) * p.delta
+        i = float(max(c.w - p.w_t, 0) * c.B) * p.epsilon
+        t = (((a + b) + g) + d) + i
+        lat += a
+        bw += b
+        comp += g
+        mem += d
+        inc += i
+        tot += t
+    return _breakdown(lat, bw, comp, mem, inc, tot)
+
+
+# ---------------------------------------------------------------- closed forms (Tables 1, 2)
+
+def _ceil_log2(c: int) -> int:
+    return (c - 1).bit_length()
+
+
+def closed_form_terms(kind: str, c: int, S: int, w_t: int, fanins: tuple = ()):
+    """Integer numerators over a common denominator for Table 2's row of `kind` at
+    N = c servers and S bytes: returns (A, Bn, Cn, Dn, In, den) with the ε coefficient
+    I = In/den already multiplied by the max(·, 0) factors.
+
+    RB   P:459 (γ = (N−1)S, reading Q7)      Ring P:460      RHD P:461 (+χ(N) fold)
+    CPS  P:462                               HCPS P:463 with readings Q5 (memory) and Q6
+    (incast): D = (2·Σ_{i=1}^{m−1} Π_{j=i}^{m−1} f_j + N + 1)·S/N,
+              I = Σ_i max(0, f_i − w_t)·2(f_i − 1)·Π_{j>i} f_j·S/N.
+    """
+    if c < 2:
+        raise ValueError("closed forms need N >= 2")
+    if kind == "rb":
+        return 2, 2 * (c - 1) * S, (c - 1) * S, (c + 1) * S, 2 * (c - 1) * S * max(c - w_t, 0), 1
+    if kind == "cps":
+        return 2, 2 * (c - 1) * S, (c - 1) * S, (c + 1) * S, 2 * (c - 1) * S * max(c - w_t, 0), c
+    if kind == "ring":
+        return 2 * (c - 1), 2 * (c - 1) * S, (c - 1) * S, 3 * (c - 1) * S, 0, c
+    if kind == "rhd":
+        chi = 0 if is_pow2(c) else 1
+        return (2 * _ceil_log2(c), 2 * (c - 1) * S + chi * 2 * S * c, (c - 1) * S + chi * S * c,
+                3 * (c - 1) * S + chi * 3 * S * c, 0, c)
+    if kind == "hcps":
+        f = tuple(fanins)
+        prod = 1
+        for x in f:
+            prod *= x
+        if prod != c or any(x < 2 for x in f) or not f:
+            raise ValueError(f"invalid factorization {f} of {c}")
+        m = len(f)
+        suffix_sum = 0
+        for i in range(1, m):
+            p = 1
+            for j in range(i, m):
+                p *= f[j]
+            suffix_sum += p
+        inc = 0
+        for i in range(m):
+            tail = 1
+            for j in range(i + 1, m):
+                tail *= f[j]
+            inc += max(0, f[i] - w_t) * 2 * (f[i] - 1) * tail
+        return (2 * m, 2 * (c - 1) * S, (c - 1) * S, (2 * suffix_sum + c + 1) * S, inc * S, c)
+    raise ValueError(f"no closed form for {kind!r}")
+
+
+def closed_form_exact(kind, c, S, p: Params, fanins=()) -> dict:
+    A, Bn, Cn, Dn, In, den = closed_form_terms(kind, c, S, p.w_t, fanins)
+    beta, gamma = p.effective()
+    F = Fraction
+    lat = A * F(p.alpha)
+    bw = F(Bn, den) * F(beta)
+    comp = F(Cn, den) * F(gamma)
+    mem = F(Dn, den) * F(p.delta)
+    inc = F(In, den) * F(p.epsilon)
+    return _breakdown(lat, bw, comp, mem, inc, lat + bw + comp + mem + inc)
+
+
+def closed_form_f64(kind, c, S, p: Params, fanins=()) -> dict:
+    A, Bn, Cn, Dn, In, den = closed_form_terms(kind, c, S, p.w_t, fanins)
+    beta, gamma = p.effective()
+    dd = float(den)
+    lat = float(A) * p.alpha
+    bw = (float(Bn) / dd) * beta
+    comp = (float(Cn) / dd) * gamma
+    mem = (float(Dn) / dd) * p.delta
+    inc = (float(In) / dd) * p.epsilon
+    return _breakdown(lat, bw, comp, mem, inc, (((lat + bw) + comp) + mem) + inc)
+
+
+def abc_table1_terms(kind: str, c: int, S: int):
+    """Table 1, the (α,β,γ) model, as exact (A, B, C) Fractions."""
+    F = Fraction
+    if kind == "rb":
+        return 2, F(2 * (c - 1) * S), F(2 * (c - 1) * S)
+    if kind == "cps":
+        return 2, F(2 * (c - 1) * S, c), F((c - 1) * S, c)
+    if kind == "ring":
+        return 2 * (c - 1), F(2 * (c - 1) * S, c), F((c - 1) * S, c)
+    if kind == "rhd":
+        chi = 0 if is_pow2(c) else 1
+        return (2 * _ceil_log2(c), F(2 * (c - 1) * S, c) + chi * 2 * S,
+                F((c - 1) * S, c) + chi * S)
+    raise ValueError(kind)
+
+
+def memory_lower_bound(c: int, S) -> Fraction:
+    """Theorem 1 / Eq. 11: (N+1)S/N (times δ)."""
+    return Fraction(c + 1, c) * S
+
+
+def bandwidth_optimal_traffic(c: int, S) -> Fraction:
+    """Eq. 2: 2(N−1)S/N."""
+    return Fraction(2 * (c - 1), c) * S
+
+
+def optimality_flags(kind: str, c: int, S: int, w_t: int, fanins=()) -> dict:
+    """§3.3.1-3.3.2: δ-optimal iff D = (N+1)S/N exactly; ε-optimal iff the
+    incast coefficient is 0."""
+    A, Bn, Cn, Dn, In, den = closed_form_terms(kind, c, S, w_t, fanins)
+    return {"delta_optimal": Fraction(Dn, den) == memory_lower_bound(c, S),
+            "epsilon_optimal": In == 0}
+
+
+def enumerate_hcps_factorizations(n: int, max_steps: int) -> list:
+    """ordered factorizations, each f_i >= 2, 1 <= m <= max_steps; shorter lists
+    first, then lexicographically descending."""
+    found = []
+
+    def rec(rem, pref):
+        if rem == 1:
+            if pref:
+                found.append(tuple(pref))
+            return
+        if len(pref) == max_steps:
+            return
+        for d in range(2, rem + 1):
+            if rem % d == 0:
+                rec(rem // d, pref + [d])
+
+    rec(n, [])
+    out = []
+    for m in range(1, max_steps + 1):
+        out.extend(sorted((f for f in found if len(f) == m), reverse=True))
+    return out

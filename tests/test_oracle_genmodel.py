@@ -1,0 +1,201 @@
+"""Pins for oracle.genmodel (CPU only).
+
+Fixed by the paper: Table 1 vs Table 2 coefficient identities;
+Theorem 1 as a bound over every built-in plan; Theorem 2 at plan
+level; Eq. 6's monotonicity; the printed GenModel and (α,β,γ)
+bars of fig:costmodel and its 2.6 % / 19.8 % error claims; SPEC's
+hand-substituted worked examples.
+"""
+from fractions import Fraction
+
+import pytest
+
+from oracle import genmodel as G
+from oracle import plans as P
+from oracle import topology as T
+
+Sf = 10 ** 8          # floats
+Sb = 4 * Sf           # bytes
+
+
+def table5_params():
+    m, s = T.TABLE5["middle_sw"], T.TABLE5["server"]
+    return G.params_per_float(m["alpha"], m["beta"], s["gamma"], s["delta"], m["epsilon"], m["w_t"])
+
+
+@pytest.mark.parametrize("kind", ["cps", "ring", "rhd", "rb"])
+@pytest.mark.parametrize("n", [2, 3, 5, 8, 12, 16, 24])
+def test_table2_minus_new_terms_is_table1(kind, n):
+    """dropping δ and ε from Table 2 reproduces Table 1 exactly (RB γ exempt, Q7)."""
+    S = 1000
+    A, Bn, Cn, Dn, In, den = G.closed_form_terms(kind, n, S, 9)
+    a1, b1, c1 = G.abc_table1_terms(kind, n, S)
+    assert A == a1
+    assert Fraction(Bn, den) == b1
+    if kind == "rb":
+        assert 2 * Fraction(Cn, den) == c1        # Table 1 prints 2(N-1)S γ (Q7)
+    else:
+        assert Fraction(Cn, den) == c1
+
+
+def test_hcps_reduces_to_cps():
+    """Reading Q6: HCPS[N] must equal the CPS row, including incast."""
+    for n in (4, 9, 12, 24):
+        for wt in (2, 9, 30):
+            assert G.closed_form_terms("hcps", n, 77, wt, (n,))[1:] == \
+                   G.closed_form_terms("cps", n, 77, wt)[1:]
+
+
+@pytest.mark.parametrize("n", range(2, 65))
+def test_theorem1_memory_bound_all_kinds(n):
+    """Theorem 1: every plan's memory term >= (N+1)S/N δ; equality for CPS; Ring = 3(N−1)S/N."""
+    S = 1
+    lb = G.memory_lower_bound(n, S)
+    kinds = [("cps", ()), ("ring", ()), ("rhd", ()), ("rb", ())]
+    kinds += [("hcps", f) for f in G.enumerate_hcps_factorizations(n, 3)]
+    for name, f in kinds:
+        A, Bn, Cn, Dn, In, den = G.closed_form_terms(name, n, S, 9, f)
+        assert Fraction(Dn, den) >= lb
+    assert Fraction(G.closed_form_terms("cps", n, S, 9)[3], n) == lb
+    assert Fraction(G.closed_form_terms("ring", n, S, 9)[3], n) == Fraction(3 * (n - 1), n)
+
+
+@pytest.mark.parametrize("n", range(2, 65))
+def test_theorem2_plan_level(n):
+    """with w_t = 9 no built-in plan is both δ- and ε-optimal when N > 9; CPS is
+    both when N <= 9."""
+    kinds = [("cps", ()), ("ring", ()), ("rb", ())]
+    if P.is_pow2(n):
+        kinds.append(("rhd", ()))
+    kinds += [("hcps", f) for f in G.enumerate_hcps_factorizations(n, 3)]
+    both = [k for k in kinds
+            if all(G.optimality_flags(k[0], n, 1000, 9, k[1]).values())]
+    if n > 9:
+        assert both == []
+    else:
+        assert ("cps", ()) in both
+
+
+def test_optimality_flags_examples():
+    assert G.optimality_flags("cps", 24, 100, 9) == {"delta_optimal": True, "epsilon_optimal": False}
+    assert G.optimality_flags("ring", 24, 100, 9) == {"delta_optimal": False, "epsilon_optimal": True}
+    assert G.optimality_flags("cps", 4, 100, 9) == {"delta_optimal": True, "epsilon_optimal": True}
+
+
+def test_eq6_per_op_cost_decreasing():
+    """T(x)/(x−1) = ((x+1)/(x−1))Sδ + Sγ strictly decreasing; the δ share
+    at x = 16 is <= 37.8 % of x = 2 ("saved by 66.7% at max")."""
+    vals = [Fraction(x + 1, x - 1) + Fraction(1, 3) for x in range(2, 17)]
+    assert all(a > b for a, b in zip(vals, vals[1:]))
+    assert Fraction(17, 15) / 3 <= Fraction(378, 1000)
+    assert 1 - Fraction(1, 3) == Fraction(2, 3)         # the 66.7 % limit
+
+
+def test_spec_worked_examples(spec_examples):
+    p = table5_params()
+    cps = G.closed_form_exact("cps", 24, 4 * 10 ** 7, p)
+    e = spec_examples["cps_24_1e7"]
+    assert float(cps["total"]) == pytest.approx(e["total"], rel=e["rel_tol"])
+    h = G.closed_form_exact("hcps", 24, 4 * 10 ** 7, p, (8, 3))
+    e = spec_examples["hcps_8_3_24_1e7"]
+    for key in ("total", "latency", "bandwidth", "compute", "memory"):
+        assert float(h[key]) == pytest.approx(e[key], rel=e["rel_tol"])
+    assert h["incast"] == 0
+
+
+def costmodel_params():
+    """SURVEY App. A back-solve of fig:costmodel: α = 4.0e-3 s, (2β+γ)S = 0.6638 s,
+    Sδ = 0.0391 s, Sε = 0.01066 s, w_t = 9 (S = 1e8 floats)."""
+    return G.Params(4.0e-3, 0.0, 0.0, 0.0391 / Sb, 0.01066 / Sb, 9, combined=0.6638 / Sb)
+
+
+def test_fig_costmodel_genmodel_bars(golden):
+    """All 10 printed GenModel predictions within 1.5 % (bars are printed to ~3 digits)."""
+    p = costmodel_params()
+    for n in ("12", "15"):
+        for kind, v in golden["fig_costmodel"][n]["genmodel"].items():
+            name, f = P.parse_kind(kind)
+            got = float(G.closed_form_exact(name, int(n), Sb, p, f)["total"])
+            assert got == pytest.approx(v, rel=0.015), (n, kind)
+
+
+def test_fig_costmodel_abc_bars(golden):
+    """The (α,β,γ) bars are reproduced exactly by Table 1 with α = 4e-3, (2β+γ)S = 0.66164
+    (HCPS rows use 2mα + 2(N−1)S/N β + (N−1)S/N γ, i.e. Table 2 with δ = ε = 0)."""
+    p = G.Params(4.0e-3, 0.0, 0.0, 0.0, 0.0, 9, combined=0.66164 / Sb)
+    for n in ("12", "15"):
+        for kind, v in golden["fig_costmodel"][n]["abc"].items():
+            name, f = P.parse_kind(kind)
+            got = float(G.closed_form_exact(name, int(n), Sb, p, f)["total"])
+            assert got == pytest.approx(v, abs=2e-8), (n, kind)
+
+
+def test_fig_costmodel_error_claims(golden):
+    """max GenModel error 2.6 %, max (α,β,γ) error 19.8 %, error = |pred−meas|/meas."""
+    eg, ea = [], []
+    for n in ("12", "15"):
+        d = golden["fig_costmodel"][n]
+        for k, meas in d["measured"].items():
+            eg.append(abs(d["genmodel"][k] - meas) / meas)
+            ea.append(abs(d["abc"][k] - meas) / meas)
+    assert round(max(eg), 3) == golden["fig_costmodel"]["max_error_genmodel"]
+    assert round(max(ea), 3) == golden["fig_costmodel"]["max_error_abc"]
+
+
+@pytest.mark.parametrize("kind", ["cps", "ring", "rhd", "hcps:4,2", "hcps:2,4", "hcps:2,2,2",
+                                  "hcps:2,3", "hcps:3,2", "hcps:6,2", "hcps:2,2,3"])
+@pytest.mark.parametrize("wt", [2, 3, 9])
+def test_per_step_evaluator_equals_closed_form(kind, wt):
+    """Per-step GenModel of a built plan ≡ Table 2 row on a uniform single switch, N | S,
+    exact rationals."""
+    name, f = P.parse_kind(kind)
+    n = 8
+    if name == "hcps":
+        n = 1
+        for x in f:
+            n *= x
+    S = n * 96
+    p = G.Params(1e-6, 1e-9, 3e-10, 2e-10, 5e-11, wt)
+    plan = P.build_plan(kind, n, S // 4)
+    got = G.predict_exact(G.step_coeffs(plan, 4), G.uniform_step_params(p, plan.nsteps))
+    ref = G.closed_form_exact(name, n, S, p, f)
+    for key in ref:
+        assert got[key] == ref[key], key
+
+
+def test_rb_per_step_incast_is_half_of_printed():
+    """Reading Q7: the broadcast step has w = 2, so the per-step evaluator charges incast on
+    the reduce phase only: exactly half of Table 2's printed RB incast."""
+    n, S = 12, 12 * 40
+    p = G.Params(0, 1e-9, 0, 0, 1e-10, 3)
+    plan = P.build_plan("rb", n, S // 4)
+    got = G.predict_exact(G.step_coeffs(plan, 4), G.uniform_step_params(p, 2))
+    ref = G.closed_form_exact("rb", n, S, p)
+    assert got["incast"] * 2 == ref["incast"]
+    assert got["bandwidth"] == ref["bandwidth"]
+
+
+def test_f64_close_to_exact():
+    p = table5_params()
+    for kind in ("cps", "ring", "rhd", "rb"):
+        for n in (4, 8, 24):
+            ex = G.closed_form_exact(kind, n, Sb, p)
+            fl = G.closed_form_f64(kind, n, Sb, p)
+            assert abs(fl["total"] - float(ex["total"])) <= 1e-14 * float(ex["total"])
+
+
+def test_factorizations(spec_examples):
+    assert [list(f) for f in G.enumerate_hcps_factorizations(24, 2)] == \
+           spec_examples["factorizations_24_2"]
+    assert G.enumerate_hcps_factorizations(7, 2) == [(7,)]
+    assert (3, 2, 2) in G.enumerate_hcps_factorizations(12, 3)
+
+
+def test_hcps_memory_nonincreasing_in_f0():
+    """§3.3: "the larger the prior steps' fan-in degrees, the less the memory
+    access overhead" — for m = 2 and fixed N, D decreases as f0 grows."""
+    for n in (12, 24, 36, 64):
+        fs = [f for f in G.enumerate_hcps_factorizations(n, 2) if len(f) == 2]
+        d = {f[0]: Fraction(G.closed_form_terms("hcps", n, 1, 99, f)[3], n) for f in fs}
+        keys = sorted(d)
+        assert all(d[a] >= d[b] for a, b in zip(keys, keys[1:]))
