@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the GenTree-plan AllReduce hot path (arXiv 2409.04202) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Metric (BASELINE.json): AllReduce busbw (GB/s) = S/t * 2(R-1)/R for S bytes per rank and R
+ranks (nccl-tests convention); plus the GenModel prediction error of the executed plan.
+
+Workload (config C4 of BASELINE.json, "bf16, 256 MB buffer, GenTree plan through one
+executor"):
+  * N = 1 (default): R = 8 ranks emulated on one B200 ("8 ranks/GPU", config C5's mode) —
+    one cooperative launch of the step-table kernel moves every rank's 256 MiB through HBM;
+  * N > 1 (torchrun, one process per GPU): R = N ranks, peer buffers mapped with CUDA IPC,
+    the kernel pulls/pushes over NVLink 5 (NVSwitch).  NCCL all_reduce on the same buffer is
+    timed alongside for comparison.
+A "step" is one full AllReduce (all SURVEY §8(a) rows) of the 256 MiB buffer.  Inputs are
+synthetic gradient-shaped data from the seeded generator (DESIGN.md input recipe), resident
+in HBM; the working set (>= 256 MiB per GPU) exceeds the 126 MB L2, so no flush is needed.
+
+Only the cpu_baseline leg and --impl reference execute the CPU oracle (oracle/).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1 << 20
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=["bf16", "f32"], default="bf16")
+    ap.add_argument("--mib", type=int, default=256, help="MiB per rank")
+    ap.add_argument("--ranks", type=int, default=8, help="emulated ranks when --gpus 1")
+    ap.add_argument("--force", default=None, help="plan kind instead of GenTree (cps, ring, rhd, rb, hcps:a,b)")
+    ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--cpu-sample-mib", type=float, default=8.0, help="oracle sample per rank (MiB)")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+NVLINK_PEAK_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
+
+
+def model_params():
+    """GenModel parameters (per byte) used to select the plan: the B200 fit committed under
+    profiles/ when present, else nominal B200 values."""
+    path = os.path.join(ROOT, "profiles", "genmodel_params.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return p, "fitted (profiles/genmodel_params.json)"
+    return {"alpha": 3e-6, "beta": 1 / 900e9, "gamma": 0.0, "delta": 1 / 6.54e12, "epsilon": 0.0,
+            "w_t": 9}, "nominal"
+
+
+def single_switch_doc(world, p):
+    from_float = 4.0
+    nodes = [{"id": "sw", "kind": "switch", "parent": None, "uplink": None}]
+    for i in range(world):
+        nodes.append({"id": f"s{i}", "kind": "server", "parent": "sw",
+                      "uplink": {"alpha": p["alpha"], "beta": p["beta"] * from_float,
+                                 "epsilon": p["epsilon"] * from_float, "w_t": int(p["w_t"])},
+                      "compute": {"gamma": p["gamma"] * from_float, "delta": p["delta"] * from_float}})
+    return json.dumps({"nodes": nodes})
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.out = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.out, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        rows = []
+        with open(self.out) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].isdigit():
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [int(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("[N/A]", ""))}
+
+
+def busbw(bytes_per_rank, ranks, seconds):
+    return bytes_per_rank / seconds * 2 * (ranks - 1) / ranks / 1e9
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+
+def oracle_sample_time(world, dtype, count, force, p):
+    """The oracle (as it stands) simulating the same plan kind on a bounded sample."""
+    from oracle import genmodel as OG
+    from oracle import gentree as GT
+    from oracle import simulate as SM
+    from oracle import topology as T
+    from synth import generator as GEN
+    t = T.parse_topology(single_switch_doc(world, p))
+    op = OG.Params(p["alpha"], p["beta"], p["gamma"], p["delta"], p["epsilon"], int(p["w_t"]))
+    plan, _ = GT.gentree(t, count, 2 if dtype == "bf16" else 4, params=op, force=force)
+    xs = GEN.generate_all(GEN.config_seed(4), world, count, dtype)
+    t0 = time.perf_counter()
+    SM.simulate(plan, xs, dtype)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(world, dtype, sample_mib, force, p):
+    es = 2 if dtype == "bf16" else 4
+    count = int(sample_mib * MIB) // es
+    secs = oracle_sample_time(world, dtype, count, force, p)
+    return {"value": round(busbw(count * es, world, secs), 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"{world} ranks x {count} {dtype} elements ({sample_mib:g} MiB/rank), same plan kind, "
+                      f"numpy single-threaded step-by-step simulation; {secs:.2f} s per AllReduce"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as the reference arm (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = args.gpus
+    world = args.ranks if n == 1 else n
+    p, _ = model_params()
+    es = 2 if args.dtype == "bf16" else 4
+    count = int(args.cpu_sample_mib * MIB) // es
+    for _ in range(min(args.warmup, 1)):
+        oracle_sample_time(world, args.dtype, count, args.force, p)
+    times = [oracle_sample_time(world, args.dtype, count, args.force, p) for _ in range(max(1, min(args.steps, 3)))]
+    t = sum(times) / len(times)
+    v = busbw(count * es, world, t)
+    line = {"impl": "reference", "metric": "allreduce_busbw", "value": round(v, 4), "unit": "GB/s",
+            "n_gpus": n, "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": round(t * 1e3, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic",
+            "config": {"workload": f"C4 {'emulated ' + str(world) + ' ranks/GPU' if n == 1 else str(n) + ' ranks'}"
+                                   f", {args.dtype}, bounded sample of the {args.mib} MiB/rank buffer",
+                       "ranks": world, "bytes_per_rank": count * es, "plan": args.force or "gentree"},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{world} ranks x {count} elements per step"},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import paper_2409_04202_b200 as G
+
+    n = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if n > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        assert dist.get_world_size() == n
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    es = 2 if args.dtype == "bf16" else 4
+    nbytes = args.mib * MIB
+    count = nbytes // es
+    world = args.ranks if n == 1 else n
+    p, p_src = model_params()
+    gp = G.params(p["alpha"], p["beta"], p["gamma"], p["delta"], p["epsilon"], int(p["w_t"]))
+    plan = G.Plan.from_topology(single_switch_doc(world, p), count, args.dtype, None, args.force)
+    chosen = plan.report()[-1]["chosen"]
+    pred = plan.predict(gp)["total"]
+    seed = 0x240904202 ^ 4
+    stream = torch.cuda.current_stream()
+
+    if n == 1:
+        comm = G.Comm.local(world, dev)
+        stride = G.rank_stride_bytes(count, args.dtype)
+        buf = torch.empty(world * stride, dtype=torch.uint8, device="cuda")
+        for r in range(world):
+            G.fill_synthetic(buf.data_ptr() + r * stride, count, args.dtype, seed, r, 0)
+        dbytes = world * stride
+    else:
+        comm = G.Comm.create(rank, n, dev)
+        buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        G.fill_synthetic(buf, count, args.dtype, seed, rank, 0)
+        comm.register(buf)
+        dbytes = nbytes
+    if args.ctas:
+        comm.set_ctas(args.ctas)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def refill():   # keep magnitudes bounded (in-place sums grow x world per call)
+        if n == 1:
+            for r in range(world):
+                G.fill_synthetic(buf.data_ptr() + r * stride, count, args.dtype, seed, r, 0)
+        else:
+            G.fill_synthetic(buf, count, args.dtype, seed, rank, 0)
+
+    for _ in range(args.warmup):
+        G.allreduce_exec(plan, comm, buf)
+    refill()
+    torch.cuda.synchronize()
+    comm.async_error()
+    barrier()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    torch.cuda.synchronize()
+    barrier()
+    ev[0].record(stream)
+    for i in range(args.steps):
+        G.allreduce_exec(plan, comm, buf)
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    comm.async_error()
+    launches = args.steps * comm.last_launch_count()
+    per_step = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(args.steps)]
+    total = ev[0].elapsed_time(ev[-1]) / 1e3
+    if dist is not None:
+        tt = torch.tensor([total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    t_step = total / args.steps
+    value = busbw(nbytes, world, t_step)
+
+    # roofline of the dominant (only) kernel: launch duration = the step's event interval
+    kern_t = statistics.mean(per_step)
+    if n == 1:
+        hbm_peak, hbm_src = load_peaks()
+        alg_bytes = 2 * world * nbytes          # every rank buffer read once + written once
+        achieved = alg_bytes / kern_t / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": alg_bytes, "peak_source": hbm_src}
+    else:
+        wire = 2 * (n - 1) * nbytes / n          # Eq. 2: bytes per direction per GPU
+        achieved = wire / kern_t / 1e9
+        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
+                "algorithmic_bytes_per_launch": int(wire),
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
+
+    # NCCL on the same buffer (N > 1)
+    nccl = None
+    if dist is not None and not args.no_nccl:
+        t = torch.empty(count, dtype=torch.bfloat16 if args.dtype == "bf16" else torch.float32, device="cuda")
+        t.normal_()
+        for _ in range(args.warmup):
+            dist.all_reduce(t)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            dist.all_reduce(t)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        nccl = {"busbw": round(busbw(nbytes, n, float(tt.item())), 2), "ms_per_step": round(float(tt.item()) * 1e3, 4),
+                "version": ".".join(map(str, torch.cuda.nccl.version())),
+                "algo_env": os.environ.get("NCCL_ALGO", "default")}
+        del t
+
+    # end to end through the C-ABI from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty(dbytes, dtype=torch.uint8, pin_memory=True)
+        host.copy_(buf)
+        k = max(1, min(args.steps, 5))
+        G.allreduce_exec_host(plan, comm, buf, host.data_ptr(), count, args.dtype)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            G.allreduce_exec_host(plan, comm, buf, host.data_ptr(), count, args.dtype)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = e0.elapsed_time(e1) / 1e3 / k
+        if dist is not None:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        e2e = {"value": round(busbw(nbytes, world, te), 4), "unit": "GB/s",
+               "h2d_bytes_per_step": dbytes * (n if n > 1 else 1), "d2h_bytes_per_step": dbytes * (n if n > 1 else 1),
+               "ms_per_step": round(te * 1e3, 3), "steps": k}
+        comm.async_error()
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline(world, args.dtype, args.cpu_sample_mib, args.force, p)
+    line = {
+        "metric": "allreduce_busbw", "value": round(value, 2), "unit": "GB/s", "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic",
+        "config": {"workload": (f"C4: GenTree-plan AllReduce, {args.dtype}, {args.mib} MiB per rank, "
+                                + (f"{world} ranks emulated on 1 GPU (8 ranks/GPU, C5 mode)" if n == 1
+                                   else f"{n} ranks = {n} GPUs over NVLink/NVSwitch")),
+                   "ranks": world, "bytes_per_rank": nbytes, "plan": chosen,
+                   "plan_source": args.force or f"GenTree with {p_src} GenModel params",
+                   "l2": f"working set {dbytes / MIB:.0f} MiB per GPU > 126 MB L2 (no flush needed)",
+                   "ctas_per_rank": args.ctas or "auto"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "gpu_launches_note": "one cooperative launch of ar_exec_kernel per step (per process)",
+        "clocks": clk,
+        "genmodel": {"predicted_ms": round(pred * 1e3, 4), "measured_ms": round(t_step * 1e3, 4),
+                     "pred_err": round(abs(pred - t_step) / t_step, 4), "params": p_src},
+        "busbw_per_step_min_median_max": [round(busbw(nbytes, world, max(per_step)), 2),
+                                          round(busbw(nbytes, world, statistics.median(per_step)), 2),
+                                          round(busbw(nbytes, world, min(per_step)), 2)],
+    }
+    if nccl:
+        line["nccl"] = nccl
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

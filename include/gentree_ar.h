@@ -1,0 +1,199 @@
+/* gentree_ar.h — C-ABI of the B200-native GenModel/GenTree AllReduce library.
+ *
+ * Implements the data-parallel hot path of arXiv 2409.04202 ("Revisiting the Time Cost
+ * Model of AllReduce"): fit GenModel (§3.4), generate a plan with GenTree (§4.2,
+ * Algorithms 1-2) and execute it on device buffers (the ReduceScatter step(s) with fan-in
+ * chosen by GenModel, then the AllGather = the RS reversed) with hand-written
+ * sm_100a kernels that pull peer chunks over NVLink from CUDA-IPC-mapped buffers and push
+ * results with P2P stores under flag synchronisation.
+ *
+ * Citations: "P:n" = PAPER.md line n, "S:n" = SPEC.md line n (the reference text),
+ * readings "Qn" = the register in DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *   - return value is a status: AR_OK (0), AR_EINVAL (1) for validation/domain errors
+ *     (SPEC exit code 1), AR_ESYS (2) for CUDA / system errors (SPEC exit code 2);
+ *     nothing is thrown or aborted across the ABI;
+ *   - ar_last_error() returns a thread-local message for the last failing call on this
+ *     thread, valid until the next call;
+ *   - all pointer arguments are borrowed for the duration of the call unless stated;
+ *   - GenModel quantities are in seconds and bytes (β, γ, δ, ε in seconds per byte; the
+ *     topology document keeps Table 5's per-float units and is converted by /4, exactly).
+ */
+#ifndef GENTREE_AR_H
+#define GENTREE_AR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AR_OK 0
+#define AR_EINVAL 1
+#define AR_ESYS 2
+
+#define AR_F32 0  /* IEEE binary32 data, fp32 accumulation */
+#define AR_BF16 1 /* bfloat16 data, fp32 accumulation, one RNE rounding per stored partial (Q2) */
+
+#define AR_MAX_RANKS 64     /* ranks of one communicator (2..64) */
+#define AR_BLOB_BYTES 256   /* size of one exported registration blob */
+
+const char *ar_last_error(void);
+const char *ar_version(void);
+
+/* ------------------------------------------------------------------ GenModel */
+
+/* GenModel parameters, per byte.  When has_combined != 0 only the fitted
+ * (2β+γ) = `combined` is known: evaluation then uses β = combined/2, γ = 0. */
+typedef struct {
+  double alpha, beta, gamma, delta, epsilon;
+  int32_t w_t;
+  int32_t has_combined;
+  double combined;
+} gm_params;
+
+/* Per-term time (seconds) of a plan or closed form. */
+typedef struct {
+  double latency, bandwidth, compute, memory, incast, total;
+} gm_breakdown;
+
+/* One Co-located-PS benchmark observation: n ranks, `bytes` per rank,
+ * mean AllReduce time in seconds. */
+typedef struct {
+  int32_t n;
+  int32_t reserved;
+  uint64_t bytes;
+  double seconds;
+} gm_measurement;
+
+/* §3.4 fit (procedure S:441-458): for each w_t in [wt_min, wt_max], NNLS for
+ * (α, k = 2β+γ, δ, ε) on the CPS row of Table 2; the lowest SSE wins (ties, within 1e-6
+ * relative, go to the smaller w_t).  If link_bytes_per_s > 0, β = 1/link_bytes_per_s and
+ * γ = k − 2β (AR_EINVAL if negative); otherwise out->has_combined = 1.
+ * rows: n_rows observations, repeated (n, bytes) pairs are averaged.  `sse` may be NULL.
+ * Errors: AR_EINVAL if fewer than 4 distinct (n, bytes) rows, fewer than 2 distinct n or
+ * bytes, or an empty w_t range. */
+int genmodel_fit(const gm_measurement *rows, size_t n_rows, int32_t wt_min, int32_t wt_max,
+                 double link_bytes_per_s, gm_params *out, double *sse);
+
+/* Table 2 closed form (readings Q5-Q7) of `kind` ("cps", "ring", "rhd", "rb",
+ * "hcps:f0,f1,...") for n ranks and `bytes` per rank, evaluated in the fixed float64
+ * order of DESIGN.md.  Errors: AR_EINVAL for n < 2, unknown kind, bad factorization. */
+int genmodel_closed_form(const char *kind, int32_t n, uint64_t bytes, const gm_params *params,
+                         gm_breakdown *out);
+
+/* ------------------------------------------------------------------ GenTree */
+
+typedef struct gt_plan gt_plan; /* opaque, immutable, library-owned, thread-shareable */
+
+/* Build an AllReduce plan for `count` elements of `dtype` per rank on the tree described by
+ * `topology_json` (SPEC's document format; NUL-terminated).  Ranks are the servers in
+ * depth-first pre-order.  params == NULL uses each link's own parameters from the
+ * document; otherwise `params` is used for every link and server.  force_kind == NULL (or
+ * "") runs GenTree's selection; otherwise every switch uses that kind ("cps", "ring",
+ * "rhd", "hcps:f0,f1,..", or "rb" on a single-switch topology).  The plan is verified
+ * (conservation invariant) before it is returned.  *out must be released with
+ * gt_plan_free.  Errors: AR_EINVAL on a malformed/invalid topology, count < 1, unknown
+ * dtype or kind, or a forced kind that does not fit a switch. */
+int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
+                 const char *force_kind, gt_plan **out);
+
+/* Convenience: single switch with `world` ranks and uniform `params` (required). */
+int gentree_plan_single_switch(int32_t world, uint64_t count, int32_t dtype, const gm_params *params,
+                               const char *force_kind, gt_plan **out);
+
+/* Canonical plan JSON (sorted keys, compact; byte-identical to the oracle's).  Writes at most
+ * cap bytes including the NUL; *needed (if non-NULL) receives the full size incl. NUL.
+ * AR_EINVAL if cap is too small (buf then holds nothing useful). */
+int gt_plan_to_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed);
+/* GenTree decision report (per switch: chosen kind, candidate totals, rearranged children,
+ * start/finish times), JSON, same buffer protocol. */
+int gt_plan_report_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed);
+/* Shape of a plan. */
+int gt_plan_info(const gt_plan *plan, int32_t *n_ranks, int32_t *n_steps, uint64_t *count, int32_t *dtype);
+/* Per-step GenModel of the plan as executed (a6): params == NULL uses
+ * the topology's links as traversed by each step (max α/β/ε, min w_t; reading Q16). */
+int genmodel_predict(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
+void gt_plan_free(gt_plan *plan);
+
+/* ------------------------------------------------------------------ communicator */
+
+typedef struct ar_comm ar_comm; /* opaque; one per process and device; single-threaded */
+
+/* Multi-process communicator: this process is `rank` of `world` (2..64) and drives CUDA
+ * device `cuda_device`.  Allocates this rank's flag page.  Errors: AR_EINVAL for bad
+ * rank/world, AR_ESYS on CUDA failure. */
+int ar_comm_create(int32_t rank, int32_t world, int32_t cuda_device, ar_comm **out);
+
+/* Emulated communicator: all `world` ranks live in this process on one device (each rank's
+ * buffer is a separate region of device memory; "8 ranks/GPU" of config C5).  The executor
+ * runs all ranks in one cooperative launch, with the same step tables and flag protocol. */
+int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out);
+
+/* Number of CTAs per rank used by allreduce_exec (0 = automatic).  Same value on all ranks. */
+int ar_comm_set_ctas(ar_comm *comm, int32_t ctas);
+
+/* Export `bytes` of device memory at `dptr` (16-byte aligned; may be an interior pointer of
+ * a cudaMalloc allocation, e.g. a torch tensor) for peer access.  Writes AR_BLOB_BYTES to
+ * blob_out (CUDA IPC handles of the allocation and of this rank's flag page + offsets).
+ * The caller gathers the blobs of all ranks (in rank order) and passes them to
+ * ar_comm_open_peers.  The memory stays caller-owned and must outlive the registration.
+ * Not used by emulated communicators. */
+int ar_comm_register(ar_comm *comm, void *dptr, size_t bytes, void *blob_out);
+/* Map every peer's registered buffer (and flag page, first time) into this process.
+ * blobs = world * AR_BLOB_BYTES, rank order, from ar_comm_register on every rank for the
+ * same logical buffer (same size).  Collective: call on all ranks before the first
+ * allreduce_exec on that buffer. */
+int ar_comm_open_peers(ar_comm *comm, const void *blobs);
+/* Asynchronous device error of earlier executions (flag wait timeout = AR_ESYS), cleared on
+ * read.  Synchronises the communicator's device. */
+int ar_comm_get_async_error(ar_comm *comm);
+int ar_comm_destroy(ar_comm *comm);
+
+/* Bytes between consecutive ranks' buffers of an emulated communicator:
+ * count * element size rounded up to 256. */
+uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
+
+/* ------------------------------------------------------------------ execution */
+
+/* In-place AllReduce (SUM) of `count` elements of `dtype` at `dptr` by executing `plan`
+ * (lowered once per (plan, comm) to a device step table).  Multi-process comm: dptr is this
+ * rank's registered buffer (ar_comm_register + ar_comm_open_peers).  Emulated comm: dptr
+ * is the base of world consecutive rank buffers, rank r's at dptr + r *
+ * ar_rank_stride_bytes(count, dtype).  Asynchronous and ordered on `stream` (a
+ * cudaStream_t; NULL = legacy default stream).  Every element of every rank's buffer ends
+ * equal to the plan's left-to-right fp32 sum of the ranks' inputs (bit-exact to the CPU
+ * oracle).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
+ * plan's, unregistered or misaligned buffer; AR_ESYS on launch failure. */
+int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
+                   void *stream);
+
+/* The same, end to end from host memory: copies `host` (pinned recommended; for an emulated
+ * comm world consecutive rank buffers at the same stride) into dptr, executes, copies the
+ * result back into `host`, all on `stream`. */
+int allreduce_exec_host(const gt_plan *plan, ar_comm *comm, void *dptr, void *host, uint64_t count,
+                        int32_t dtype, void *stream);
+
+/* Device kernels launched by the last allreduce_exec of this comm (per rank, per call). */
+int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
+
+/* ------------------------------------------------------------------ inputs and harness */
+
+/* Fill `count` elements at dptr with the seeded synthetic generator G(seed, rank, i),
+ * i = start..start+count-1 (mode 0 gradient, 1 integer,
+ * 2 specials).  Independent CUDA implementation of synth/generator.py. */
+int ar_fill_synthetic(void *dptr, uint64_t count, int32_t dtype, uint64_t seed, int32_t rank,
+                      int32_t mode, uint64_t start, void *stream);
+
+/* Eq. 6 micro-benchmark kernel: out = ((in[0] + in[1]) + ...) + in[k-1]
+ * elementwise, fp32 accumulation, k = 1..64 device pointers (array in host memory),
+ * one read of each input and one write of out per element. */
+int ar_local_reduce(void *const *inputs, int32_t k, void *out, uint64_t count, int32_t dtype, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GENTREE_AR_H */

@@ -148,6 +148,44 @@ def simulate_scalar(plan: Plan, inputs: list, dtype: str) -> list:
     return [np.array(b, dtype=np.uint16) for b in bufs]
 
 
+def simulate_at(plan: Plan, idx, values: list, dtype: str) -> list:
+    """The plan's outputs at selected element indices only (for full-size checks).
+
+    idx: sorted element indices; values[r][k] = rank r's input at idx[k] (float32 values or
+    bf16 bit patterns).  Replays every step on just those elements, with the same
+    arithmetic as `simulate`.  Returns per-rank arrays of len(idx)."""
+    n, count = plan.n, plan.count
+    idx = np.asarray(idx, dtype=np.int64)
+    bufs = [np.array(v, copy=True) for v in values]
+    starts = np.array([block_offset(count, n, b) for b in range(n)], dtype=np.int64)
+    blk = np.searchsorted(starts, idx, side="right") - 1
+    for st in plan.steps:
+        if st.phase == "rs":
+            for rd in st.reduces:
+                sel = np.nonzero(blk == rd.block)[0]
+                if sel.size == 0:
+                    continue
+                if len(rd.inputs) == 1:
+                    bufs[rd.server][sel] = bufs[rd.inputs[0]][sel]
+                    continue
+                if dtype == "f32":
+                    acc = bufs[rd.inputs[0]][sel].astype(np.float32, copy=True)
+                    for q in rd.inputs[1:]:
+                        acc = acc + bufs[q][sel]
+                    bufs[rd.server][sel] = acc
+                else:
+                    acc = bf16_bits_to_f32(bufs[rd.inputs[0]][sel]).copy()
+                    for q in rd.inputs[1:]:
+                        acc = acc + bf16_bits_to_f32(bufs[q][sel])
+                    bufs[rd.server][sel] = f32_to_bf16_rne(acc)
+        else:
+            for t in st.transfers:
+                sel = np.nonzero(blk == t.block)[0]
+                if sel.size:
+                    bufs[t.dst][sel] = bufs[t.src][sel]
+    return bufs
+
+
 def exact_sum_f64(inputs: list, dtype: str) -> np.ndarray:
     """The plain definition out[e] = sum_q x_q[e], accumulated in float64
     (exact for the generator's inputs up to N=64 ranks only in 'integer' mode; otherwise

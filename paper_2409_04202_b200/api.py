@@ -1,0 +1,240 @@
+"""Python API over the C-ABI (same names as include/gentree_ar.h; marshalling only).
+
+    plan = Plan.single_switch(world=8, count=n, dtype="bf16", params=p)      # GenTree
+    comm = Comm.local(world=8, device=0)                                     # 8 ranks, 1 GPU
+    allreduce_exec(plan, comm, buf)                                          # sm_100a kernels
+
+Multi-process (one process per GPU, torch.distributed for the handle exchange):
+
+    comm = Comm.from_process_group(device=local_rank)
+    comm.register(tensor)                     # collective
+    allreduce_exec(plan, comm, tensor)
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+
+from . import _lib as L
+from ._lib import AR_BF16, AR_F32, GmBreakdown, GmMeasurement, GmParams, check, lib
+
+__all__ = ["GmParams", "params", "genmodel_fit", "genmodel_closed_form", "Plan", "Comm",
+           "allreduce_exec", "allreduce_exec_host", "fill_synthetic", "local_reduce",
+           "rank_stride_bytes", "dtype_code"]
+
+
+def dtype_code(dtype) -> int:
+    if isinstance(dtype, int):
+        return dtype
+    if dtype in L.DTYPES:
+        return L.DTYPES[dtype]
+    s = str(dtype)
+    if s.endswith("float32"):
+        return AR_F32
+    if s.endswith("bfloat16"):
+        return AR_BF16
+    raise ValueError(f"unsupported dtype {dtype!r}")
+
+
+def params(alpha=0.0, beta=0.0, gamma=0.0, delta=0.0, epsilon=0.0, w_t=1, combined=None) -> GmParams:
+    """GenModel parameters per byte (seconds, seconds/byte)."""
+    p = GmParams(alpha, beta, gamma, delta, epsilon, int(w_t), 0, 0.0)
+    if combined is not None:
+        p.has_combined = 1
+        p.combined = combined
+    return p
+
+
+def genmodel_fit(rows, wt_min: int, wt_max: int, link_bytes_per_s: float = 0.0):
+    """rows: iterable of (n, bytes, seconds).  Returns (GmParams, sse)."""
+    rows = list(rows)
+    arr = (GmMeasurement * max(1, len(rows)))()
+    for i, (n, b, t) in enumerate(rows):
+        arr[i] = GmMeasurement(int(n), 0, int(b), float(t))
+    out = GmParams()
+    sse = ctypes.c_double()
+    check(lib.genmodel_fit(arr, len(rows), wt_min, wt_max, float(link_bytes_per_s), ctypes.byref(out),
+                           ctypes.byref(sse)))
+    return out, sse.value
+
+
+def genmodel_closed_form(kind: str, n: int, nbytes: int, p: GmParams) -> dict:
+    out = GmBreakdown()
+    check(lib.genmodel_closed_form(kind.encode(), n, nbytes, ctypes.byref(p), ctypes.byref(out)))
+    return out.as_dict()
+
+
+class Plan:
+    """Immutable AllReduce plan (opaque gt_plan*)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def from_topology(cls, topology_json: str, count: int, dtype="f32", params: GmParams | None = None,
+                      force: str | None = None) -> "Plan":
+        h = ctypes.c_void_p()
+        check(lib.gentree_plan(topology_json.encode(), count, dtype_code(dtype),
+                               ctypes.byref(params) if params is not None else None,
+                               force.encode() if force else None, ctypes.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def single_switch(cls, world: int, count: int, dtype="f32", params: GmParams | None = None,
+                      force: str | None = None) -> "Plan":
+        h = ctypes.c_void_p()
+        if params is None:
+            params = GmParams(1e-6, 1.0 / 900e9, 0.0, 1.0 / 6.5e12, 0.0, 64, 0, 0.0)
+        check(lib.gentree_plan_single_switch(world, count, dtype_code(dtype), ctypes.byref(params),
+                                             force.encode() if force else None, ctypes.byref(h)))
+        return cls(h)
+
+    def _str(self, fn) -> str:
+        need = ctypes.c_size_t()
+        fn(self._h, None, 0, ctypes.byref(need))
+        buf = ctypes.create_string_buffer(need.value)
+        check(fn(self._h, buf, need.value, None))
+        return buf.value.decode()
+
+    def to_json(self) -> str:
+        return self._str(lib.gt_plan_to_json)
+
+    def report(self) -> list:
+        return json.loads(self._str(lib.gt_plan_report_json))
+
+    def info(self) -> dict:
+        n, s, c, d = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_int32()
+        check(lib.gt_plan_info(self._h, ctypes.byref(n), ctypes.byref(s), ctypes.byref(c), ctypes.byref(d)))
+        return {"n": n.value, "steps": s.value, "count": c.value, "dtype": d.value}
+
+    def predict(self, params: GmParams | None = None) -> dict:
+        out = GmBreakdown()
+        check(lib.genmodel_predict(self._h, ctypes.byref(params) if params is not None else None,
+                                   ctypes.byref(out)))
+        return out.as_dict()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib.gt_plan_free(h)
+
+
+def rank_stride_bytes(count: int, dtype) -> int:
+    return int(lib.ar_rank_stride_bytes(count, dtype_code(dtype)))
+
+
+def _ptr(x) -> int:
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+class Comm:
+    """Communicator (opaque ar_comm*)."""
+
+    def __init__(self, handle, world: int, rank: int, local: bool, device: int):
+        self._h = handle
+        self.world, self.rank, self.local, self.device = world, rank, local, device
+
+    @classmethod
+    def create(cls, rank: int, world: int, device: int) -> "Comm":
+        h = ctypes.c_void_p()
+        check(lib.ar_comm_create(rank, world, device, ctypes.byref(h)))
+        return cls(h, world, rank, False, device)
+
+    @classmethod
+    def local(cls, world: int, device: int = 0) -> "Comm":
+        h = ctypes.c_void_p()
+        check(lib.ar_comm_create_local(world, device, ctypes.byref(h)))
+        return cls(h, world, 0, True, device)
+
+    @classmethod
+    def from_process_group(cls, device: int, group=None) -> "Comm":
+        import torch.distributed as dist
+        return cls.create(dist.get_rank(group), dist.get_world_size(group), device)
+
+    def set_ctas(self, ctas: int):
+        check(lib.ar_comm_set_ctas(self._h, ctas))
+
+    def export(self, buf, nbytes: int | None = None) -> bytes:
+        if nbytes is None:
+            nbytes = buf.numel() * buf.element_size()
+        blob = ctypes.create_string_buffer(L.AR_BLOB_BYTES)
+        check(lib.ar_comm_register(self._h, _ptr(buf), nbytes, blob))
+        return blob.raw
+
+    def open_peers(self, blobs: list):
+        assert len(blobs) == self.world
+        data = b"".join(blobs)
+        check(lib.ar_comm_open_peers(self._h, data))
+
+    def register(self, tensor, group=None):
+        """Collective over torch.distributed: export + all_gather_object + open_peers."""
+        import torch.distributed as dist
+        blob = self.export(tensor)
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, blob, group=group)
+        self.open_peers(blobs)
+
+    def async_error(self):
+        check(lib.ar_comm_get_async_error(self._h))
+
+    def last_launch_count(self) -> int:
+        k = ctypes.c_int32()
+        check(lib.ar_comm_last_launch_count(self._h, ctypes.byref(k)))
+        return k.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def destroy(self):
+        h, self._h = self._h, None
+        if h:
+            lib.ar_comm_destroy(h)
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        try:
+            import torch
+            return int(torch.cuda.current_stream().cuda_stream) or None
+        except Exception:
+            return None
+    if isinstance(stream, int):
+        return stream or None
+    return int(stream.cuda_stream) or None
+
+
+def allreduce_exec(plan: Plan, comm: Comm, buf, count: int | None = None, dtype=None, stream=None):
+    """In-place AllReduce of `buf` (torch tensor or device pointer) with `plan`."""
+    info = None
+    if count is None or dtype is None:
+        info = plan.info()
+    count = info["count"] if count is None else count
+    dt = info["dtype"] if dtype is None else dtype_code(dtype)
+    check(lib.allreduce_exec(plan.handle, comm.handle, _ptr(buf), count, dt, _stream(stream)))
+
+
+def allreduce_exec_host(plan: Plan, comm: Comm, dbuf, host_ptr: int, count: int, dtype, stream=None):
+    check(lib.allreduce_exec_host(plan.handle, comm.handle, _ptr(dbuf), host_ptr, count, dtype_code(dtype),
+                                  _stream(stream)))
+
+
+def fill_synthetic(buf, count: int, dtype, seed: int, rank: int, mode: int = 0, start: int = 0, stream=None):
+    check(lib.ar_fill_synthetic(_ptr(buf), count, dtype_code(dtype), seed, rank, mode, start, _stream(stream)))
+
+
+def local_reduce(inputs, out, count: int, dtype, stream=None):
+    arr = (ctypes.c_void_p * len(inputs))(*[_ptr(x) for x in inputs])
+    check(lib.ar_local_reduce(arr, len(inputs), _ptr(out), count, dtype_code(dtype), _stream(stream)))

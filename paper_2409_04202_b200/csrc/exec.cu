@@ -1,0 +1,1034 @@
+// Plan executor for sm_100a: communicator (CUDA IPC peer maps + flag pages), lowering of a
+// plan to per-rank device step tables, and the persistent step-table kernel.
+//
+// Hot path:
+//   a1  entry flags — each CTA posts the call's epoch into its slot of every consumer's
+//       flag page (st.release.sys over NVLink) and waits for its paired producers;
+//   a2  ReduceScatter step — k-way pull reduction: k 16-byte loads per vector from local
+//       HBM / peer HBM (NVLink, IPC-mapped), fp32 left-to-right sum in the plan's order
+//       (reading Q1), one RNE rounding for bf16 (Q2);
+//   a3  inter-step flags — full producer->consumer waits between dependent steps;
+//   a4  AllGather — P2P 16-byte stores of the reduced vector; the last RS level is fused
+//       with the first AG level so the owner writes its block straight from registers to
+//       every destination (one read and one write per element, the δ saving of P:402);
+//   a5  exit flags — paired waits on every rank that accessed this rank's buffer.
+// The same kernel runs an emulated communicator (all ranks on one GPU) as one cooperative
+// launch with blockIdx.y = rank.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/gentree_ar.h"
+#include "internal.hpp"
+
+using namespace gtar;
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kMaxSlots = 256;        // plan steps + entry (slot 0)
+constexpr int kCtaCapMulti = 256;     // flag page CTA dimension, multi-process comms
+constexpr uint32_t kBlobMagic = 0x47544152u;  // "GTAR"
+
+// ------------------------------------------------------------------ device tables
+struct DevOp {
+  long long off, len;        // elements
+  int nsrc, ndst;
+  int src_begin, dst_begin;  // into the rank list
+};
+struct DevStep {
+  int slot;                  // flag slot written after this step (0 = entry)
+  int op_begin, op_count;
+  int wait_begin, wait_count;
+  int notify_begin, notify_count;
+  int pad;
+};
+struct DevWait {
+  int rank, slot, paired, pad;
+};
+struct ExecArgs {
+  const DevStep *steps;
+  const DevOp *ops;
+  const DevWait *waits;
+  const int *ranks;          // op src/dst rank lists and notify lists
+  const int *prog_begin;     // per local rank
+  const int *prog_len;
+  char *bufs[AR_MAX_RANKS];            // rank -> data buffer base (as seen here)
+  unsigned long long *sigs[AR_MAX_RANKS];  // rank -> flag page base (as seen here)
+  unsigned long long *err;
+  unsigned long long epoch;
+  unsigned long long timeout_ns;
+  int rank0, world, cta_cap, esize;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ uint4 ld_cg(const uint4 *p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_v4(uint4 *p, const uint4 &v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// bf16 <-> fp32.  Widening is exact; narrowing is round-to-nearest-even with NaN mapped to
+// a quiet NaN that keeps the sign (reading Q2).
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+__device__ __forceinline__ uint32_t f2bf(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FC0u | ((u >> 16) & 0x8000u);
+  return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+}
+
+// ------------------------------------------------------------------ reduction core
+// Accumulate one 16-byte vector of source s into acc (fp32).  First source initialises.
+template <bool BF16>
+__device__ __forceinline__ void acc_first(float (&acc)[8], const uint4 &v) {
+  if (BF16) {
+    acc[0] = bf_lo(v.x); acc[1] = bf_hi(v.x); acc[2] = bf_lo(v.y); acc[3] = bf_hi(v.y);
+    acc[4] = bf_lo(v.z); acc[5] = bf_hi(v.z); acc[6] = bf_lo(v.w); acc[7] = bf_hi(v.w);
+  } else {
+    acc[0] = __uint_as_float(v.x); acc[1] = __uint_as_float(v.y);
+    acc[2] = __uint_as_float(v.z); acc[3] = __uint_as_float(v.w);
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ void acc_add(float (&acc)[8], const uint4 &v) {
+  if (BF16) {
+    acc[0] = __fadd_rn(acc[0], bf_lo(v.x)); acc[1] = __fadd_rn(acc[1], bf_hi(v.x));
+    acc[2] = __fadd_rn(acc[2], bf_lo(v.y)); acc[3] = __fadd_rn(acc[3], bf_hi(v.y));
+    acc[4] = __fadd_rn(acc[4], bf_lo(v.z)); acc[5] = __fadd_rn(acc[5], bf_hi(v.z));
+    acc[6] = __fadd_rn(acc[6], bf_lo(v.w)); acc[7] = __fadd_rn(acc[7], bf_hi(v.w));
+  } else {
+    acc[0] = __fadd_rn(acc[0], __uint_as_float(v.x)); acc[1] = __fadd_rn(acc[1], __uint_as_float(v.y));
+    acc[2] = __fadd_rn(acc[2], __uint_as_float(v.z)); acc[3] = __fadd_rn(acc[3], __uint_as_float(v.w));
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ uint4 acc_pack(const float (&acc)[8]) {
+  uint4 o;
+  if (BF16) {
+    o.x = f2bf(acc[0]) | (f2bf(acc[1]) << 16);
+    o.y = f2bf(acc[2]) | (f2bf(acc[3]) << 16);
+    o.z = f2bf(acc[4]) | (f2bf(acc[5]) << 16);
+    o.w = f2bf(acc[6]) | (f2bf(acc[7]) << 16);
+  } else {
+    o.x = __float_as_uint(acc[0]); o.y = __float_as_uint(acc[1]);
+    o.z = __float_as_uint(acc[2]); o.w = __float_as_uint(acc[3]);
+  }
+  return o;
+}
+
+struct OpShared {
+  const uint4 *src[AR_MAX_RANKS];
+  uint4 *dst[AR_MAX_RANKS];
+  int nsrc, ndst;
+};
+
+// Vector body, NSRC sources known at compile time (1 = copy).  UNROLL vectors per thread
+// per iteration, all loads issued before any add (memory-level parallelism).
+template <int NSRC, int UNROLL, bool BF16>
+__device__ __noinline__ void body_fixed(const OpShared &s, size_t v0, size_t v1) {
+  const size_t stride = (size_t)blockDim.x * UNROLL;
+  const int ndst = s.ndst;
+  for (size_t base = v0 + threadIdx.x; base < v1; base += stride) {
+    uint4 x[UNROLL][NSRC];
+#pragma unroll
+    for (int u = 0; u < UNROLL; u++) {
+      size_t v = base + (size_t)u * blockDim.x;
+      if (v < v1) {
+#pragma unroll
+        for (int k = 0; k < NSRC; k++) x[u][k] = ld_cg(s.src[k] + v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; u++) {
+      size_t v = base + (size_t)u * blockDim.x;
+      if (v < v1) {
+        uint4 o;
+        if (NSRC == 1) {
+          o = x[u][0];
+        } else {
+          float acc[8];
+          acc_first<BF16>(acc, x[u][0]);
+#pragma unroll
+          for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[u][k]);
+          o = acc_pack<BF16>(acc);
+        }
+        for (int d = 0; d < ndst; d++) st_v4(s.dst[d] + v, o);
+      }
+    }
+  }
+}
+
+// Any number of sources (> 8): groups of 8 loads, accumulation order unchanged.
+template <bool BF16>
+__device__ __noinline__ void body_generic(const OpShared &s, size_t v0, size_t v1) {
+  for (size_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+    float acc[8];
+    for (int k0 = 0; k0 < s.nsrc; k0 += 8) {
+      uint4 x[8];
+      const int kn = min(8, s.nsrc - k0);
+#pragma unroll
+      for (int k = 0; k < 8; k++)
+        if (k < kn) x[k] = ld_cg(s.src[k0 + k] + v);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        if (k >= kn) break;
+        if (k0 + k == 0) acc_first<BF16>(acc, x[k]);
+        else acc_add<BF16>(acc, x[k]);
+      }
+    }
+    uint4 o = acc_pack<BF16>(acc);
+    for (int d = 0; d < s.ndst; d++) st_v4(s.dst[d] + v, o);
+  }
+}
+
+template <bool BF16>
+__device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
+  switch (s.nsrc) {
+    case 1: body_fixed<1, 4, BF16>(s, v0, v1); break;
+    case 2: body_fixed<2, 2, BF16>(s, v0, v1); break;
+    case 3: body_fixed<3, 2, BF16>(s, v0, v1); break;
+    case 4: body_fixed<4, 1, BF16>(s, v0, v1); break;
+    case 5: body_fixed<5, 1, BF16>(s, v0, v1); break;
+    case 6: body_fixed<6, 1, BF16>(s, v0, v1); break;
+    case 7: body_fixed<7, 1, BF16>(s, v0, v1); break;
+    case 8: body_fixed<8, 1, BF16>(s, v0, v1); break;
+    default: body_generic<BF16>(s, v0, v1); break;
+  }
+}
+
+// Scalar elements [e0, e1) (unaligned head / tail), same summation order.
+__device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, const int *src_ranks, const int *dst_ranks,
+                             long long e0, long long e1, bool bf16) {
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    if (bf16) {
+      const unsigned short *p0 = (const unsigned short *)(a.bufs[src_ranks[0]]) + e;
+      unsigned short out;
+      if (s.nsrc == 1) {
+        out = *(volatile const unsigned short *)p0;
+      } else {
+        float acc = __uint_as_float((uint32_t)(*(volatile const unsigned short *)p0) << 16);
+        for (int k = 1; k < s.nsrc; k++) {
+          const unsigned short *pk = (const unsigned short *)(a.bufs[src_ranks[k]]) + e;
+          acc = __fadd_rn(acc, __uint_as_float((uint32_t)(*(volatile const unsigned short *)pk) << 16));
+        }
+        out = (unsigned short)f2bf(acc);
+      }
+      for (int d = 0; d < s.ndst; d++) ((unsigned short *)(a.bufs[dst_ranks[d]]))[e] = out;
+    } else {
+      const uint32_t *p0 = (const uint32_t *)(a.bufs[src_ranks[0]]) + e;
+      uint32_t out;
+      if (s.nsrc == 1) {
+        out = *(volatile const uint32_t *)p0;
+      } else {
+        float acc = __uint_as_float(*(volatile const uint32_t *)p0);
+        for (int k = 1; k < s.nsrc; k++) {
+          const uint32_t *pk = (const uint32_t *)(a.bufs[src_ranks[k]]) + e;
+          acc = __fadd_rn(acc, __uint_as_float(*(volatile const uint32_t *)pk));
+        }
+        out = __float_as_uint(acc);
+      }
+      for (int d = 0; d < s.ndst; d++) ((uint32_t *)(a.bufs[dst_ranks[d]]))[e] = out;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long *flag_ptr(const ExecArgs &a, int page_rank, int slot, int producer,
+                                                        int cta) {
+  return a.sigs[page_rank] + ((size_t)(slot * a.world + producer) * a.cta_cap + cta);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_constant__ ExecArgs a) {
+  __shared__ OpShared sh;
+  const int lr = blockIdx.y;
+  const int me = a.rank0 + lr;
+  const int cta = blockIdx.x;
+  const int nctas = gridDim.x;
+  const bool bf16 = a.esize == 2;
+  const int vec_elems = 16 / a.esize;
+  const DevStep *prog = a.steps + a.prog_begin[lr];
+  const int nst = a.prog_len[lr];
+  const unsigned long long t_start = globaltimer();
+
+  for (int si = 0; si < nst; si++) {
+    const DevStep st = prog[si];
+    // ---- waits (a1 / a3 / a5)
+    if (st.wait_count > 0) {
+      const int tot = st.wait_count * nctas;  // full waits use all CTAs; paired use one
+      for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+        const DevWait w = a.waits[st.wait_begin + i / nctas];
+        const int c = i % nctas;
+        if (w.paired && c != cta) continue;
+        const unsigned long long *f = flag_ptr(a, me, w.slot, w.rank, c);
+        unsigned int spins = 0;
+        while (ld_acquire_sys(f) < a.epoch) {
+          if ((++spins & 1023u) == 0 && globaltimer() - t_start > a.timeout_ns) {
+            atomicExch(a.err, 1ull);
+            break;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- ops (a2 / a4)
+    for (int oi = 0; oi < st.op_count; oi++) {
+      const DevOp op = a.ops[st.op_begin + oi];
+      const int *sr = a.ranks + op.src_begin;
+      const int *dr = a.ranks + op.dst_begin;
+      const long long b0 = op.off * a.esize, b1 = (op.off + op.len) * a.esize;
+      const long long vb = (b0 + 15) / 16, ve = b1 / 16;   // whole 16-byte vectors
+      __syncthreads();
+      if (threadIdx.x < op.nsrc) sh.src[threadIdx.x] = (const uint4 *)a.bufs[sr[threadIdx.x]];
+      if (threadIdx.x < op.ndst) sh.dst[threadIdx.x] = (uint4 *)a.bufs[dr[threadIdx.x]];
+      if (threadIdx.x == 0) { sh.nsrc = op.nsrc; sh.ndst = op.ndst; }
+      __syncthreads();
+      if (vb >= ve) {
+        if (cta == 0) scalar_elems(sh, a, sr, dr, op.off, op.off + op.len, bf16);
+        continue;
+      }
+      const long long nv = ve - vb;
+      const size_t v0 = (size_t)(vb + nv * cta / nctas), v1 = (size_t)(vb + nv * (cta + 1) / nctas);
+      if (bf16) body_dispatch<true>(sh, v0, v1);
+      else body_dispatch<false>(sh, v0, v1);
+      if (cta == 0 && vb * 16 > b0) scalar_elems(sh, a, sr, dr, op.off, vb * vec_elems, bf16);
+      if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(sh, a, sr, dr, ve * vec_elems, op.off + op.len, bf16);
+    }
+    // ---- notify (release our slot on every consumer's page)
+    if (st.notify_count > 0) {
+      __threadfence_system();
+      __syncthreads();
+      for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
+        const int consumer = a.ranks[st.notify_begin + i];
+        st_release_sys(flag_ptr(a, consumer, st.slot, me, cta), a.epoch);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ synthetic inputs
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  unsigned long long z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__constant__ uint32_t kSpecF32[12] = {0x00000000u, 0x80000000u, 0x00000001u, 0x807FFFFFu, 0x7F7FFFFFu, 0xFF7FFFFFu,
+                                       0x7F800000u, 0xFF800000u, 0x7FC00000u, 0x00800000u, 0x80000010u, 0x3F800000u};
+__constant__ uint16_t kSpecBF16[12] = {0x0000, 0x8000, 0x0001, 0x807F, 0x7F7F, 0xFF7F,
+                                        0x7F80, 0xFF80, 0x7FC0, 0x0080, 0x8010, 0x3F80};
+
+__global__ void fill_kernel(void *dptr, unsigned long long count, int bf16, unsigned long long seed, int rank,
+                            int mode, unsigned long long start) {
+  const unsigned long long key = (seed * 0x9E3779B97F4A7C15ull) ^ ((unsigned long long)rank << 48);
+  for (unsigned long long j = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; j < count;
+       j += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = start + j;
+    const unsigned long long z = splitmix64(key ^ i);
+    uint32_t bits;
+    if (mode == 1) {
+      long long m = bf16 ? (long long)(z % 65ull) - 32 : (long long)(z % 2049ull) - 1024;
+      bits = __float_as_uint((float)m);
+      if (bf16) bits >>= 16;
+    } else {
+      const int e = 7 + (int)(splitmix64((seed ^ 0xA5A5ull) ^ (i >> 16)) % 12ull);
+      if (!bf16) {
+        long long m = (long long)((z >> 40) & 0xFFFFFFull) - 0x800000ll;
+        bits = __float_as_uint(ldexpf((float)m, -(23 + e)));
+        if (mode == 2 && (i % 8ull) == 0) bits = kSpecF32[(i / 8ull) % 12ull];
+      } else {
+        long long m = (long long)((z >> 56) & 0xFFull) - 0x80ll;
+        bits = __float_as_uint(ldexpf((float)m, -(7 + e))) >> 16;
+        if (mode == 2 && (i % 8ull) == 0) bits = kSpecBF16[(i / 8ull) % 12ull];
+      }
+    }
+    if (bf16) ((uint16_t *)dptr)[j] = (uint16_t)bits;
+    else ((uint32_t *)dptr)[j] = bits;
+  }
+}
+
+// Eq. 6 local fan-in reduce: out = ((in0 + in1) + ...) + in_{k-1}.
+struct LocalReduceArgs {
+  const uint4 *in[AR_MAX_RANKS];
+  uint4 *out;
+  unsigned long long nvec;
+  int k;
+};
+template <bool BF16>
+__global__ void __launch_bounds__(kThreads, 2) local_reduce_kernel(const __grid_constant__ LocalReduceArgs a) {
+  __shared__ OpShared sh;
+  if (threadIdx.x < a.k) sh.src[threadIdx.x] = a.in[threadIdx.x];
+  if (threadIdx.x == 0) { sh.nsrc = a.k; sh.ndst = 1; sh.dst[0] = a.out; }
+  __syncthreads();
+  const size_t v0 = a.nvec * blockIdx.x / gridDim.x, v1 = a.nvec * (blockIdx.x + 1) / gridDim.x;
+  body_dispatch<BF16>(sh, v0, v1);
+}
+
+// ------------------------------------------------------------------ host side
+#define CUDA_OK(x)                                                                           \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) throw SysError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct SysError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct Registration {
+  char *local = nullptr;
+  size_t bytes = 0;
+  std::vector<char *> peer;   // rank -> mapped pointer (own = local)
+  bool opened = false;
+};
+
+struct Lowered {
+  DevStep *steps = nullptr;
+  DevOp *ops = nullptr;
+  DevWait *waits = nullptr;
+  int *ranks = nullptr;
+  int *prog_begin = nullptr;
+  int *prog_len = nullptr;
+  int nctas = 0;
+};
+
+}  // namespace
+
+struct ar_comm {
+  int rank = 0, world = 0, device = 0;
+  bool local = false;
+  int nctas = 0, cta_cap = 0, max_ctas = 0;
+  unsigned long long epoch = 0;
+  size_t page_elems = 0;                       // uint64 per flag page
+  unsigned long long *sig_local = nullptr;     // own page (multi) or all pages (local)
+  std::vector<unsigned long long *> sig;       // rank -> page as seen here
+  bool sig_opened = false;
+  std::map<std::string, char *> ipc_opened;    // handle bytes -> base (opened once)
+  std::vector<Registration> regs;
+  std::map<uint64_t, Lowered> lowered;
+  unsigned long long *err = nullptr;
+  unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
+  int last_launches = 0;
+};
+
+namespace {
+
+struct Blob {
+  uint32_t magic, version;
+  int32_t rank, world;
+  uint64_t bytes, offset;
+  cudaIpcMemHandle_t data, sig;
+};
+static_assert(sizeof(Blob) <= AR_BLOB_BYTES, "blob too large");
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+static void base_of(void *p, char **base, size_t *size) {
+  static PFN_getAddressRange fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    CUDA_OK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) throw SysError("cuMemGetAddressRange unavailable");
+    fn = (PFN_getAddressRange)f;
+  }
+  CUdeviceptr b;
+  size_t s;
+  if (fn(&b, &s, (CUdeviceptr)p) != CUDA_SUCCESS) throw InvalidArg("pointer is not device memory from cudaMalloc");
+  *base = (char *)b;
+  *size = s;
+}
+
+// ------------------------------------------------------------------ lowering
+struct HostOp {
+  long long off, len;
+  std::vector<int> src, dst;
+};
+struct Access {
+  int step, rank;              // executing rank
+  long long off, len;
+  bool write;
+};
+
+static bool overlap(long long a0, long long al, long long b0, long long bl) {
+  return a0 < b0 + bl && b0 < a0 + al;
+}
+
+// Plan -> per-rank programs.  Ops of one rank and step are contiguous ranges; the final RS
+// op of an owner is fused with the AG pushes of the same region in the next step when that
+// creates no conflict inside the step.  Dependencies come from a conflict analysis of the
+// buffer regions every op reads or writes (entry = every rank writes its own buffer before
+// slot 0; exit = every rank overwrites its own buffer after the kernel).
+static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, std::vector<DevOp> &ops,
+                       std::vector<DevWait> &waits, std::vector<int> &ranks, std::vector<int> &prog_begin,
+                       std::vector<int> &prog_len) {
+  const int n = p.n;
+  const int S = (int)p.steps.size();
+  if (S + 1 > kMaxSlots) throw InvalidArg("plan has too many steps");
+  // ops[step][rank]
+  std::vector<std::vector<std::vector<HostOp>>> H(S, std::vector<std::vector<HostOp>>(n));
+  for (int s = 0; s < S; s++) {
+    const Step &st = p.steps[s];
+    if (!st.ag) {
+      std::vector<std::vector<const Reduce *>> by(n);
+      for (auto &rd : st.reduces) by[rd.server].push_back(&rd);
+      for (int r = 0; r < n; r++) {
+        std::sort(by[r].begin(), by[r].end(), [](const Reduce *a, const Reduce *b) { return a->block < b->block; });
+        for (const Reduce *rd : by[r]) {
+          long long off = block_offset(p.count, n, rd->block), len = block_size(p.count, n, rd->block);
+          if (len == 0) continue;
+          auto &v = H[s][r];
+          if (!v.empty() && v.back().off + v.back().len == off && v.back().src == rd->inputs) v.back().len += len;
+          else v.push_back({off, len, rd->inputs, {r}});
+        }
+      }
+    } else {
+      std::vector<std::map<int, std::vector<int>>> by(n);   // src -> block -> dsts
+      for (auto &t : st.transfers) by[t.src][t.block].push_back(t.dst);
+      for (int r = 0; r < n; r++)
+        for (auto &kv : by[r]) {
+          std::vector<int> d = kv.second;
+          std::sort(d.begin(), d.end());
+          long long off = block_offset(p.count, n, kv.first), len = block_size(p.count, n, kv.first);
+          if (len == 0) continue;
+          auto &v = H[s][r];
+          if (!v.empty() && v.back().off + v.back().len == off && v.back().dst == d) v.back().len += len;
+          else v.push_back({off, len, {r}, d});
+        }
+    }
+  }
+  // conflict check inside one step (reads vs writes of different ops)
+  auto step_conflict_free = [&](int s) {
+    std::vector<std::pair<const HostOp *, int>> all;
+    for (int r = 0; r < n; r++)
+      for (auto &o : H[s][r]) all.push_back({&o, r});
+    for (size_t i = 0; i < all.size(); i++)
+      for (size_t j = 0; j < all.size(); j++) {
+        if (i == j) continue;
+        const HostOp &A = *all[i].first, &B = *all[j].first;
+        if (!overlap(A.off, A.len, B.off, B.len)) continue;
+        for (int w : A.dst) {
+          for (int x : B.src)
+            if (x == w) return false;
+          for (int x : B.dst)
+            if (x == w) return false;
+        }
+      }
+    return true;
+  };
+  // fusion: RS op (dst = {r}) at s-1 + AG copy of the same region by r at s
+  for (int s = 1; s < S; s++) {
+    if (!p.steps[s].ag || p.steps[s - 1].ag) continue;
+    auto saveA = H[s - 1];
+    auto saveB = H[s];
+    bool any = false;
+    for (int r = 0; r < n; r++) {
+      auto &ag = H[s][r];
+      for (size_t i = 0; i < ag.size();) {
+        bool fused = false;
+        for (auto &x : H[s - 1][r])
+          if (x.off == ag[i].off && x.len == ag[i].len && x.dst.size() == 1 && x.dst[0] == r && x.src.size() >= 2) {
+            for (int d : ag[i].dst) x.dst.push_back(d);
+            fused = true;
+            break;
+          }
+        if (fused) { ag.erase(ag.begin() + i); any = true; }
+        else i++;
+      }
+    }
+    if (any && !step_conflict_free(s - 1)) {
+      H[s - 1] = saveA;
+      H[s] = saveB;
+    }
+  }
+  // accesses per buffer rank
+  std::vector<std::vector<Access>> acc(n);
+  for (int s = 0; s < S; s++)
+    for (int r = 0; r < n; r++)
+      for (auto &o : H[s][r]) {
+        for (int q : o.src) acc[q].push_back({s, r, o.off, o.len, false});
+        for (int q : o.dst) acc[q].push_back({s, r, o.off, o.len, true});
+      }
+  // deps[r][s] : producer rank -> producer step (-1 = entry); exit deps separately
+  std::vector<std::vector<std::map<int, int>>> deps(n, std::vector<std::map<int, int>>(S));
+  std::vector<std::map<int, int>> exitdeps(n);
+  for (int s = 0; s < S; s++)
+    for (int r = 0; r < n; r++)
+      for (auto &o : H[s][r]) {
+        auto visit = [&](int q, bool write) {
+          auto &d = deps[r][s];
+          if (q != r && !d.count(q)) d[q] = -1;           // entry of q
+          for (const Access &x : acc[q]) {
+            if (x.step >= s) continue;
+            if (!write && !x.write) continue;
+            if (!overlap(o.off, o.len, x.off, x.len)) continue;
+            auto it = d.find(x.rank);
+            if (it == d.end() || it->second < x.step) d[x.rank] = x.step;
+          }
+        };
+        for (int q : o.src) visit(q, false);
+        for (int q : o.dst) visit(q, true);
+      }
+  for (int r = 0; r < n; r++)
+    for (const Access &x : acc[r]) {
+      if (x.rank == r) continue;
+      auto it = exitdeps[r].find(x.rank);
+      if (it == exitdeps[r].end() || it->second < x.step) exitdeps[r][x.rank] = x.step;
+    }
+  // notify lists: notify[t][s+1] = consumers of (t, s)
+  std::vector<std::vector<std::set<int>>> notify(n, std::vector<std::set<int>>(S + 1));
+  for (int r = 0; r < n; r++) {
+    for (int s = 0; s < S; s++)
+      for (auto &kv : deps[r][s])
+        if (!(kv.first == r && kv.second == -1)) notify[kv.first][kv.second + 1].insert(r);
+    for (auto &kv : exitdeps[r]) notify[kv.first][kv.second + 1].insert(r);
+  }
+  // programs
+  prog_begin.assign(world, 0);
+  prog_len.assign(world, 0);
+  for (int r = 0; r < n; r++) {
+    prog_begin[r] = (int)steps.size();
+    auto emit = [&](int slot, const std::vector<HostOp> *hops, const std::map<int, int> *dp, bool exit) {
+      DevStep d{};
+      d.slot = slot;
+      d.op_begin = (int)ops.size();
+      if (hops)
+        for (auto &o : *hops) {
+          DevOp x{};
+          x.off = o.off;
+          x.len = o.len;
+          x.nsrc = (int)o.src.size();
+          x.ndst = (int)o.dst.size();
+          x.src_begin = (int)ranks.size();
+          ranks.insert(ranks.end(), o.src.begin(), o.src.end());
+          x.dst_begin = (int)ranks.size();
+          ranks.insert(ranks.end(), o.dst.begin(), o.dst.end());
+          ops.push_back(x);
+        }
+      d.op_count = (int)ops.size() - d.op_begin;
+      d.wait_begin = (int)waits.size();
+      if (dp)
+        for (auto &kv : *dp) {
+          if (kv.first == r && kv.second == -1) continue;
+          DevWait w{};
+          w.rank = kv.first;
+          w.slot = kv.second + 1;
+          w.paired = (exit || kv.second == -1) ? 1 : 0;
+          waits.push_back(w);
+        }
+      d.wait_count = (int)waits.size() - d.wait_begin;
+      d.notify_begin = (int)ranks.size();
+      if (!exit)
+        for (int c : notify[r][slot]) ranks.push_back(c);
+      d.notify_count = (int)ranks.size() - d.notify_begin;
+      if (d.op_count || d.wait_count || d.notify_count) steps.push_back(d);
+    };
+    emit(0, nullptr, nullptr, false);
+    for (int s = 0; s < S; s++) {
+      if (H[s][r].empty() && notify[r][s + 1].empty() && deps[r][s].empty()) continue;
+      emit(s + 1, &H[s][r], &deps[r][s], false);
+    }
+    emit(0, nullptr, &exitdeps[r], true);
+    prog_len[r] = (int)steps.size() - prog_begin[r];
+  }
+}
+
+template <typename T>
+static T *upload(const std::vector<T> &v) {
+  T *d = nullptr;
+  size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  CUDA_OK(cudaMalloc(&d, bytes));
+  if (!v.empty()) CUDA_OK(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+static void free_lowered(Lowered &L) {
+  cudaFree(L.steps);
+  cudaFree(L.ops);
+  cudaFree(L.waits);
+  cudaFree(L.ranks);
+  cudaFree(L.prog_begin);
+  cudaFree(L.prog_len);
+}
+
+static int resident_ctas(int device) {
+  int nsm = 0, per = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, 0));
+  return nsm * std::max(per, 1);
+}
+
+#define SYS_TRY(...)                                          \
+  try {                                                        \
+    __VA_ARGS__                                                \
+  } catch (const InvalidArg &e) {                              \
+    set_error(e.what());                                       \
+    return AR_EINVAL;                                          \
+  } catch (const SysError &e) {                                \
+    set_error(e.what());                                       \
+    return AR_ESYS;                                            \
+  } catch (const std::exception &e) {                          \
+    set_error(std::string("internal error: ") + e.what());     \
+    return AR_ESYS;                                            \
+  }
+
+static void init_comm(ar_comm *c) {
+  CUDA_OK(cudaSetDevice(c->device));
+  int nsm = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+  c->max_ctas = resident_ctas(c->device);
+  if (c->local) {
+    c->cta_cap = std::max(1, c->max_ctas / c->world);
+    c->nctas = c->cta_cap;
+  } else {
+    c->cta_cap = kCtaCapMulti;
+    c->nctas = std::min(nsm, kCtaCapMulti);
+  }
+  c->page_elems = (size_t)kMaxSlots * c->world * c->cta_cap;
+  const size_t pages = c->local ? c->world : 1;
+  CUDA_OK(cudaMalloc(&c->sig_local, pages * c->page_elems * sizeof(unsigned long long)));
+  CUDA_OK(cudaMemset(c->sig_local, 0, pages * c->page_elems * sizeof(unsigned long long)));
+  CUDA_OK(cudaMalloc(&c->err, sizeof(unsigned long long)));
+  CUDA_OK(cudaMemset(c->err, 0, sizeof(unsigned long long)));
+  c->sig.assign(c->world, nullptr);
+  if (c->local) {
+    for (int r = 0; r < c->world; r++) c->sig[r] = c->sig_local + (size_t)r * c->page_elems;
+    c->sig_opened = true;
+  } else {
+    c->sig[c->rank] = c->sig_local;
+  }
+  if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) c->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype) {
+  uint64_t b = count * (uint64_t)(dtype == AR_BF16 ? 2 : 4);
+  return (b + 255) / 256 * 256;
+}
+
+int ar_comm_create(int32_t rank, int32_t world, int32_t cuda_device, ar_comm **out) {
+  SYS_TRY({
+    if (!out) throw InvalidArg("null out");
+    if (world < 2 || world > AR_MAX_RANKS || rank < 0 || rank >= world) throw InvalidArg("bad rank/world");
+    ar_comm *c = new ar_comm();
+    c->rank = rank;
+    c->world = world;
+    c->device = cuda_device;
+    try {
+      init_comm(c);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+    return AR_OK;
+  })
+}
+
+int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out) {
+  SYS_TRY({
+    if (!out) throw InvalidArg("null out");
+    if (world < 2 || world > AR_MAX_RANKS) throw InvalidArg("bad world");
+    ar_comm *c = new ar_comm();
+    c->rank = 0;
+    c->world = world;
+    c->device = cuda_device;
+    c->local = true;
+    try {
+      init_comm(c);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    if (c->cta_cap < 1 || c->max_ctas < world) {
+      delete c;
+      throw InvalidArg("too many emulated ranks for one device");
+    }
+    *out = c;
+    return AR_OK;
+  })
+}
+
+int ar_comm_set_ctas(ar_comm *c, int32_t ctas) {
+  SYS_TRY({
+    if (!c) throw InvalidArg("null comm");
+    int want = ctas > 0 ? ctas : (c->local ? c->cta_cap : std::min(c->max_ctas, kCtaCapMulti));
+    if (want > c->cta_cap) throw InvalidArg("ctas exceeds the flag page capacity");
+    if ((long long)want * (c->local ? c->world : 1) > c->max_ctas) throw InvalidArg("ctas exceeds resident capacity");
+    if (ctas <= 0 && !c->local) {
+      int nsm = 0;
+      CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
+      want = std::min(nsm, kCtaCapMulti);
+    }
+    c->nctas = want;
+    return AR_OK;
+  })
+}
+
+int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
+  SYS_TRY({
+    if (!c || !dptr || !blob_out) throw InvalidArg("null argument");
+    if (c->local) throw InvalidArg("emulated communicators need no registration");
+    if ((uintptr_t)dptr % 16) throw InvalidArg("buffer must be 16-byte aligned");
+    CUDA_OK(cudaSetDevice(c->device));
+    char *base;
+    size_t size;
+    base_of(dptr, &base, &size);
+    if ((char *)dptr + bytes > base + size) throw InvalidArg("buffer extends past its allocation");
+    Blob b{};
+    b.magic = kBlobMagic;
+    b.version = 1;
+    b.rank = c->rank;
+    b.world = c->world;
+    b.bytes = bytes;
+    b.offset = (uint64_t)((char *)dptr - base);
+    CUDA_OK(cudaIpcGetMemHandle(&b.data, base));
+    CUDA_OK(cudaIpcGetMemHandle(&b.sig, c->sig_local));
+    std::memset(blob_out, 0, AR_BLOB_BYTES);
+    std::memcpy(blob_out, &b, sizeof b);
+    Registration reg;
+    reg.local = (char *)dptr;
+    reg.bytes = bytes;
+    reg.peer.assign(c->world, nullptr);
+    reg.peer[c->rank] = (char *)dptr;
+    for (auto it = c->regs.begin(); it != c->regs.end(); ++it)
+      if (it->local == reg.local) { c->regs.erase(it); break; }
+    c->regs.push_back(reg);
+    return AR_OK;
+  })
+}
+
+int ar_comm_open_peers(ar_comm *c, const void *blobs) {
+  SYS_TRY({
+    if (!c || !blobs) throw InvalidArg("null argument");
+    if (c->local) throw InvalidArg("emulated communicators need no peers");
+    CUDA_OK(cudaSetDevice(c->device));
+    const char *bb = (const char *)blobs;
+    const Blob *mine = (const Blob *)(bb + (size_t)c->rank * AR_BLOB_BYTES);
+    Registration *reg = nullptr;
+    for (auto &r : c->regs)
+      if ((uint64_t)r.bytes == mine->bytes) reg = &r;
+    // the most recently registered buffer with this size is the one being opened
+    for (auto it = c->regs.rbegin(); it != c->regs.rend(); ++it)
+      if ((uint64_t)it->bytes == mine->bytes) { reg = &*it; break; }
+    if (!reg) throw InvalidArg("no local registration matches the blobs");
+    for (int t = 0; t < c->world; t++) {
+      const Blob *b = (const Blob *)(bb + (size_t)t * AR_BLOB_BYTES);
+      if (b->magic != kBlobMagic || b->world != c->world || b->rank != t) throw InvalidArg("corrupt or misordered blob");
+      if (b->bytes != mine->bytes) throw InvalidArg("ranks registered buffers of different sizes");
+      if (t == c->rank) continue;
+      auto open = [&](const cudaIpcMemHandle_t &h) -> char * {
+        std::string key((const char *)&h, sizeof h);
+        key += std::to_string(t);
+        auto it = c->ipc_opened.find(key);
+        if (it != c->ipc_opened.end()) return it->second;
+        void *p = nullptr;
+        CUDA_OK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened[key] = (char *)p;
+        return (char *)p;
+      };
+      reg->peer[t] = open(b->data) + b->offset;
+      if (!c->sig[t]) c->sig[t] = (unsigned long long *)open(b->sig);
+    }
+    reg->opened = true;
+    c->sig_opened = true;
+    return AR_OK;
+  })
+}
+
+int ar_comm_get_async_error(ar_comm *c) {
+  SYS_TRY({
+    if (!c) throw InvalidArg("null comm");
+    CUDA_OK(cudaSetDevice(c->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    unsigned long long e = 0;
+    CUDA_OK(cudaMemcpy(&e, c->err, sizeof e, cudaMemcpyDeviceToHost));
+    if (e) {
+      CUDA_OK(cudaMemset(c->err, 0, sizeof e));
+      throw SysError("flag wait timed out on the device (peer not progressing)");
+    }
+    return AR_OK;
+  })
+}
+
+int ar_comm_destroy(ar_comm *c) {
+  if (!c) return AR_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto &kv : c->lowered) free_lowered(kv.second);
+  for (auto &kv : c->ipc_opened) cudaIpcCloseMemHandle(kv.second);
+  cudaFree(c->sig_local);
+  cudaFree(c->err);
+  delete c;
+  return AR_OK;
+}
+
+int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
+  if (!c || !kernels) { set_error("null argument"); return AR_EINVAL; }
+  *kernels = c->last_launches;
+  return AR_OK;
+}
+
+static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream) {
+  if (!plan || !c || !dptr) throw InvalidArg("null argument");
+  if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");
+  if ((uint64_t)plan->plan.count != count || plan->dtype != dtype) throw InvalidArg("count/dtype differ from the plan's");
+  if ((uintptr_t)dptr % 16) throw InvalidArg("buffer must be 16-byte aligned");
+  CUDA_OK(cudaSetDevice(c->device));
+  const size_t bytes = count * (size_t)plan->esize;
+  ExecArgs a{};
+  if (c->local) {
+    const uint64_t stride = ar_rank_stride_bytes(count, dtype);
+    for (int r = 0; r < c->world; r++) {
+      a.bufs[r] = (char *)dptr + stride * r;
+      a.sigs[r] = c->sig[r];
+    }
+  } else {
+    Registration *reg = nullptr;
+    for (auto &r : c->regs)
+      if (r.local == (char *)dptr && r.opened && r.bytes >= bytes) reg = &r;
+    if (!reg) throw InvalidArg("buffer is not registered and opened on this communicator");
+    for (int r = 0; r < c->world; r++) {
+      a.bufs[r] = reg->peer[r];
+      a.sigs[r] = c->sig[r];
+      if (!a.bufs[r] || !a.sigs[r]) throw InvalidArg("peer buffer not opened");
+    }
+  }
+  auto it = c->lowered.find(plan->uid);
+  if (it == c->lowered.end()) {
+    std::vector<DevStep> st;
+    std::vector<DevOp> ops;
+    std::vector<DevWait> w;
+    std::vector<int> rk, pb, pl;
+    lower_plan(plan->plan, c->world, st, ops, w, rk, pb, pl);
+    Lowered L;
+    if (!c->local) {  // this process runs only its own rank's program
+      std::vector<int> pb1{pb[c->rank]}, pl1{pl[c->rank]};
+      pb = pb1;
+      pl = pl1;
+    }
+    L.steps = upload(st);
+    L.ops = upload(ops);
+    L.waits = upload(w);
+    L.ranks = upload(rk);
+    L.prog_begin = upload(pb);
+    L.prog_len = upload(pl);
+    it = c->lowered.emplace(plan->uid, L).first;
+  }
+  const Lowered &L = it->second;
+  a.steps = L.steps;
+  a.ops = L.ops;
+  a.waits = L.waits;
+  a.ranks = L.ranks;
+  a.prog_begin = L.prog_begin;
+  a.prog_len = L.prog_len;
+  a.err = c->err;
+  a.epoch = ++c->epoch;
+  a.timeout_ns = c->timeout_ns;
+  a.rank0 = c->local ? 0 : c->rank;
+  a.world = c->world;
+  a.cta_cap = c->cta_cap;
+  a.esize = plan->esize;
+  dim3 grid(c->nctas, c->local ? c->world : 1);
+  void *args[] = {&a};
+  CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args, 0,
+                                      (cudaStream_t)stream));
+  c->last_launches = 1;
+  return AR_OK;
+}
+
+int allreduce_exec(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream) {
+  SYS_TRY({ return exec_impl(plan, c, dptr, count, dtype, stream); })
+}
+
+int allreduce_exec_host(const gt_plan *plan, ar_comm *c, void *dptr, void *host, uint64_t count, int32_t dtype,
+                        void *stream) {
+  SYS_TRY({
+    if (!host) throw InvalidArg("null host buffer");
+    if (!c) throw InvalidArg("null comm");
+    CUDA_OK(cudaSetDevice(c->device));
+    const size_t bytes = c->local ? ar_rank_stride_bytes(count, dtype) * c->world
+                                  : count * (size_t)(dtype == AR_BF16 ? 2 : 4);
+    cudaStream_t s = (cudaStream_t)stream;
+    CUDA_OK(cudaMemcpyAsync(dptr, host, bytes, cudaMemcpyHostToDevice, s));
+    int rc = exec_impl(plan, c, dptr, count, dtype, stream);
+    if (rc != AR_OK) return rc;
+    CUDA_OK(cudaMemcpyAsync(host, dptr, bytes, cudaMemcpyDeviceToHost, s));
+    return AR_OK;
+  })
+}
+
+int ar_fill_synthetic(void *dptr, uint64_t count, int32_t dtype, uint64_t seed, int32_t rank, int32_t mode,
+                      uint64_t start, void *stream) {
+  SYS_TRY({
+    if (!dptr) throw InvalidArg("null pointer");
+    if (dtype != AR_F32 && dtype != AR_BF16) throw InvalidArg("unknown dtype");
+    if (mode < 0 || mode > 2) throw InvalidArg("unknown mode");
+    if (count == 0) return AR_OK;
+    unsigned long long blocks = std::min<unsigned long long>((count + 255) / 256, 148ull * 16);
+    fill_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dptr, count, dtype == AR_BF16, seed, rank, mode,
+                                                                    start);
+    CUDA_OK(cudaGetLastError());
+    return AR_OK;
+  })
+}
+
+int ar_local_reduce(void *const *inputs, int32_t k, void *out, uint64_t count, int32_t dtype, void *stream) {
+  SYS_TRY({
+    if (!inputs || !out) throw InvalidArg("null argument");
+    if (k < 1 || k > AR_MAX_RANKS) throw InvalidArg("k must be in 1..64");
+    const int es = dtype == AR_BF16 ? 2 : 4;
+    if ((count * es) % 16) throw InvalidArg("count * element size must be a multiple of 16 bytes");
+    LocalReduceArgs a{};
+    for (int i = 0; i < k; i++) {
+      if ((uintptr_t)inputs[i] % 16) throw InvalidArg("inputs must be 16-byte aligned");
+      a.in[i] = (const uint4 *)inputs[i];
+    }
+    if ((uintptr_t)out % 16) throw InvalidArg("output must be 16-byte aligned");
+    a.out = (uint4 *)out;
+    a.nvec = count * es / 16;
+    a.k = k;
+    int dev = 0, nsm = 148;
+    CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (dtype == AR_BF16) local_reduce_kernel<true><<<nsm * 2, kThreads, 0, (cudaStream_t)stream>>>(a);
+    else local_reduce_kernel<false><<<nsm * 2, kThreads, 0, (cudaStream_t)stream>>>(a);
+    CUDA_OK(cudaGetLastError());
+    return AR_OK;
+  })
+}
+
+}  // extern "C"

@@ -1,0 +1,27 @@
+// Shared internals of the C-ABI library (not part of the public header).
+#pragma once
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "planner.hpp"
+
+struct gt_plan {
+  gtar::Plan plan;
+  std::vector<gtar::SwitchReport> reports;
+  gtar::Topology topo;
+  bool topo_params = true;     // built with per-link parameters from the document
+  int dtype = 0;
+  int esize = 4;
+  std::string json;            // canonical plan JSON
+  std::string report;          // GenTree report JSON
+  uint64_t uid = 0;            // unique id (lowering cache key)
+};
+
+namespace gtar {
+void set_error(const std::string &msg);
+uint64_t next_plan_uid();
+inline int esize_of(int dtype) { return dtype == 0 ? 4 : 2; }
+inline const char *dtype_name(int dtype) { return dtype == 0 ? "f32" : "bf16"; }
+}  // namespace gtar

@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element.
+
+Single GPU: the emulated communicator runs all ranks of a plan in one cooperative launch on
+one B200 (same step tables, same flag protocol as the multi-process path), so every plan kind
+is exercised at 2..64 ranks.  Inputs come from the device generator (ar_fill_synthetic),
+which is itself checked bit-for-bit against synth/generator.py first.  Bar: bit-exact
+(BASELINE.json north star), NaNs by isnan.
+"""
+import numpy as np
+import pytest
+
+from tests.gpu_util import assert_bits_equal, cuda_ok, emulated_buffer, rank_views
+
+pytestmark = pytest.mark.gpu
+
+if cuda_ok():
+    import torch
+
+    import paper_2409_04202_b200 as G
+    from oracle import gentree as GT
+    from oracle import plans as OP
+    from oracle import simulate as SM
+    from oracle import topology as T
+    from synth import generator as GEN
+else:  # collected but skipped on CPU-only hosts
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+MODES = {"gradient": 0, "integer": 1, "specials": 2}
+SEED = GEN.config_seed(1)
+
+
+def nominal():
+    """Nominal B200 GenModel parameters per byte: α = 3 µs, β = 1/900 GB/s,
+    δ = 1/6.54 TB/s, no incast below 9."""
+    return G.params(3e-6, 1 / 900e9, 0.0, 1 / 6.54e12, 0.0, 9)
+
+
+def oracle_params():
+    from oracle import genmodel as OG
+    return OG.Params(3e-6, 1 / 900e9, 0.0, 1 / 6.54e12, 0.0, 9)
+
+
+def single_switch(world):
+    return T.single_switch_doc(world, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
+                               {"gamma": 0.0, "delta": 4 / 6.54e12})
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("mode", ["gradient", "integer", "specials"])
+def test_device_generator_matches_numpy(dtype, mode):
+    count, start = 70001, 123457
+    buf = torch.zeros(count * 4, dtype=torch.uint8, device="cuda")
+    for rank in (0, 5):
+        G.fill_synthetic(buf.data_ptr(), count, dtype, SEED, rank, MODES[mode], start)
+        torch.cuda.synchronize()
+        raw = buf.cpu().numpy()[: count * (4 if dtype == "f32" else 2)]
+        got = raw.view(np.uint32 if dtype == "f32" else np.uint16)
+        want = GEN.generate(SEED, rank, count, dtype, mode, start=start)
+        want = want.view(np.uint32) if dtype == "f32" else want
+        assert np.array_equal(got, want)
+
+
+def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1):
+    plan = G.Plan.from_topology(doc, count, dtype, params, force)
+    comm = G.Comm.local(world, 0)
+    if ctas:
+        comm.set_ctas(ctas)
+    buf, stride = emulated_buffer(world, count, dtype, SEED, MODES[mode])
+    inputs = rank_views(buf, world, count, dtype, stride)
+    t = T.parse_topology(doc)
+    from oracle import genmodel as OG
+    op = None
+    if params is not None:
+        op = OG.Params(params.alpha, params.beta, params.gamma, params.delta, params.epsilon, params.w_t,
+                       params.combined if params.has_combined else None)
+    oplan, _ = GT.gentree(t, count, 4 if dtype == "f32" else 2, params=op, force=force)
+    assert plan.to_json() == OP.plan_to_json(oplan, dtype)
+    want = inputs
+    for _ in range(calls):
+        G.allreduce_exec(plan, comm, buf)
+        want = SM.simulate(oplan, want, dtype)
+    torch.cuda.synchronize()
+    comm.async_error()
+    got = rank_views(buf, world, count, dtype, stride)
+    for r in range(world):
+        assert_bits_equal(got[r], want[r], dtype, f"rank {r}")
+    assert comm.last_launch_count() == 1
+    return got
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 5, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_gentree_single_switch(world, dtype):
+    for count in (1, world - 1, 4096 * world + 3, 100003):
+        run_emulated(single_switch(world), world, count, dtype)
+
+
+@pytest.mark.parametrize("force", ["cps", "ring", "rhd", "rb", "hcps:4,2", "hcps:2,4", "hcps:2,2,2"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_forced_kinds_8_ranks(force, dtype):
+    for count in (8 * 1024, 262147):
+        run_emulated(single_switch(8), 8, count, dtype, force=force)
+
+
+@pytest.mark.parametrize("force", ["cps", "ring", "hcps:3,2", "hcps:2,3"])
+def test_forced_kinds_6_ranks(force):
+    run_emulated(single_switch(6), 6, 60001, "f32", force=force)
+
+
+@pytest.mark.parametrize("mode", ["integer", "specials"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_modes(mode, dtype):
+    got = run_emulated(single_switch(8), 8, 40000, dtype, force="ring", mode=mode)
+    if mode == "integer":
+        xs = GEN.generate_all(SEED, 8, 40000, dtype, "integer")
+        ref = sum(GEN.as_f64(x, dtype).astype(np.int64) for x in xs)
+        assert np.array_equal(GEN.as_f64(got[3], dtype).astype(np.int64), ref)
+
+
+def test_c1_two_level_tree():
+    doc = T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    run_emulated(doc, 4, 262144, "f32")
+
+
+def test_c5_64_ranks_8_per_gpu():
+    """C5: the 64-rank two-level tree (8 nodes x 8 GPUs), all 64 ranks on one GPU."""
+    nic = {"alpha": 6.58e-3, "beta": 4e-11, "epsilon": 6e-12, "w_t": 9}
+    nvl = {"alpha": 1e-5, "beta": 4.0 / 900e9, "epsilon": 1e-13, "w_t": 9}
+    doc = T.two_level_doc([8] * 8, nic, nvl, T.TABLE5["server"])
+    run_emulated(doc, 64, 64 * 1000 + 17, "f32")
+
+
+def test_asymmetric_tree_acps():
+    doc = T.two_level_doc([3, 4], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    run_emulated(doc, 7, 70001, "bf16")
+
+
+def test_repeated_calls_and_plan_interleave():
+    """Epoch progression: 3 back-to-back calls, then a different plan on the same comm."""
+    run_emulated(single_switch(4), 4, 50000, "f32", force="ring", calls=3)
+    doc = single_switch(4)
+    comm = G.Comm.local(4, 0)
+    count = 30000
+    p1 = G.Plan.from_topology(doc, count, "f32", None, "cps")
+    p2 = G.Plan.from_topology(doc, count, "f32", None, "hcps:2,2")
+    buf, stride = emulated_buffer(4, count, "f32", SEED)
+    x = rank_views(buf, 4, count, "f32", stride)
+    t = T.parse_topology(doc)
+    o1, _ = GT.gentree(t, count, 4, force="cps")
+    o2, _ = GT.gentree(t, count, 4, force="hcps:2,2")
+    for plan, oplan in ((p1, o1), (p2, o2), (p1, o1), (p2, o2)):
+        G.allreduce_exec(plan, comm, buf)
+        x = SM.simulate(oplan, x, "f32")
+    torch.cuda.synchronize()
+    got = rank_views(buf, 4, count, "f32", stride)
+    for r in range(4):
+        assert_bits_equal(got[r], x[r], "f32", f"rank {r}")
+
+
+@pytest.mark.parametrize("ctas", [1, 3, 17])
+def test_cta_counts(ctas):
+    run_emulated(single_switch(8), 8, 123457, "bf16", force="hcps:4,2", ctas=ctas)
+
+
+def test_full_size_bench_config_sampled():
+    """bench.py's N=1 workload (8 emulated ranks, bf16, 256 MiB per rank, GenTree plan) in the
+    launch configuration bench.py times; outputs checked at sampled indices one by one."""
+    world, count, dtype = 8, 128 * 1024 * 1024, "bf16"
+    doc = single_switch(world)
+    plan = G.Plan.from_topology(doc, count, dtype)
+    comm = G.Comm.local(world, 0)
+    buf, stride = emulated_buffer(world, count, dtype, SEED)
+    G.allreduce_exec(plan, comm, buf)
+    torch.cuda.synchronize()
+    comm.async_error()
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([rng.integers(0, count, 4000), np.arange(0, 64),
+                                    np.arange(count - 64, count),
+                                    [OP.block_offset(count, world, b) + d for b in range(1, world) for d in (-1, 0)]]))
+    vals = [GEN.generate(SEED, r, 1, dtype)[:0] for r in range(world)]
+    vals = [np.concatenate([GEN.generate(SEED, r, 1, dtype, start=int(i)) for i in idx]) for r in range(world)]
+    t = T.parse_topology(doc)
+    oplan, _ = GT.gentree(t, count, 2)
+    want = SM.simulate_at(oplan, idx, vals, dtype)
+    host = buf.view(torch.uint16)
+    for r in (0, 3, world - 1):
+        got = host[r * stride // 2 + torch.from_numpy(idx).cuda()].cpu().numpy().astype(np.uint16)
+        assert_bits_equal(got, want[r], dtype, f"rank {r}")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("k", [1, 2, 3, 8, 13])
+def test_local_reduce(dtype, k):
+    count = 1 << 16
+    es = 4 if dtype == "f32" else 2
+    ins = []
+    for i in range(k):
+        b = torch.empty(count * es, dtype=torch.uint8, device="cuda")
+        G.fill_synthetic(b, count, dtype, SEED, i, 0)
+        ins.append(b)
+    out = torch.empty(count * es, dtype=torch.uint8, device="cuda")
+    G.local_reduce(ins, out, count, dtype)
+    torch.cuda.synchronize()
+    xs = [GEN.generate(SEED, i, count, dtype) for i in range(k)]
+    plan = OP.Plan(1, count, [])
+    if dtype == "f32":
+        acc = xs[0].copy()
+        for x in xs[1:]:
+            acc = acc + x
+        want = acc
+    else:
+        acc = SM.bf16_bits_to_f32(xs[0]).copy()
+        for x in xs[1:]:
+            acc = acc + SM.bf16_bits_to_f32(x)
+        want = SM.f32_to_bf16_rne(acc) if k > 1 else xs[0]
+    got = out.cpu().numpy().view(np.float32 if dtype == "f32" else np.uint16)
+    assert_bits_equal(got, want, dtype)
+    del plan
+
+
+def test_errors_are_loud():
+    comm = G.Comm.local(4, 0)
+    plan = G.Plan.from_topology(single_switch(8), 1000, "f32")
+    buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    with pytest.raises(G.ArInvalid):
+        G.allreduce_exec(plan, comm, buf)          # world mismatch
+    plan4 = G.Plan.from_topology(single_switch(4), 1000, "f32")
+    with pytest.raises(G.ArInvalid):
+        G.allreduce_exec(plan4, comm, buf, count=999)
+    with pytest.raises(G.ArInvalid):
+        G.allreduce_exec(plan4, comm, buf.data_ptr() + 4)   # misaligned
+    mc = G.Comm.create(0, 2, 0)
+    with pytest.raises(G.ArInvalid):
+        G.allreduce_exec(G.Plan.from_topology(single_switch(2), 1000, "f32"), mc, buf)  # unregistered

@@ -1,0 +1,154 @@
+"""Library (C-ABI, host planning core) vs oracle: plan structure and costs (CPU only).
+
+The bar (BASELINE.json north star): plan generation and cost predictions are bit-exact —
+canonical plan JSON byte-identical, GenModel doubles bit-identical (fixed evaluation order,
+DESIGN.md).  Fits are compared within 1e-9 relative on noiseless data.
+"""
+import json
+import random
+import struct
+
+import pytest
+
+import paper_2409_04202_b200 as G
+from oracle import fit as OF
+from oracle import genmodel as OG
+from oracle import gentree as GT
+from oracle import plans as OP
+from oracle import topology as T
+from tests.test_oracle_gentree import _gtplan_topos, _random_tree, row
+
+ES = {"f32": 4, "bf16": 2}
+
+
+def bits(x: float) -> int:
+    return struct.unpack("<Q", struct.pack("<d", x))[0]
+
+
+def same_breakdown(a: dict, b: dict):
+    for k in ("latency", "bandwidth", "compute", "memory", "incast", "total"):
+        assert bits(a[k]) == bits(b[k]), (k, a[k], b[k])
+
+
+def lib_params(p: OG.Params) -> G.GmParams:
+    return G.params(p.alpha, p.beta, p.gamma, p.delta, p.epsilon, p.w_t, p.combined)
+
+
+def check_topology(doc, count, dtype="f32", params=None, force=None):
+    t = T.parse_topology(doc)
+    oplan, oreps = GT.gentree(t, count, ES[dtype], params=params, force=force)
+    lplan = G.Plan.from_topology(doc, count, dtype, lib_params(params) if params else None, force)
+    assert lplan.to_json() == OP.plan_to_json(oplan, dtype)
+    lrep = lplan.report()
+    assert [r["chosen"] for r in lrep] == [r.chosen for r in oreps]
+    for lr, orp in zip(lrep, oreps):
+        assert lr["switch"] == orp.switch
+        assert lr["rearranged_children"] == orp.rearranged_children
+        assert [c["kind"] for c in lr["candidates"]] == [k for k, _ in orp.candidates]
+        for c, (_, v) in zip(lr["candidates"], orp.candidates):
+            assert bits(c["total"]) == bits(v)
+    same_breakdown(lplan.predict(lib_params(params) if params else None),
+                   GT.predict_plan(t, oplan, ES[dtype], params))
+    return lplan, oplan
+
+
+def test_c1():
+    doc = T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    lp, _ = check_topology(doc, 262144)
+    assert lp.predict()["total"] == pytest.approx(0.029064844, rel=1e-8)
+
+
+@pytest.mark.parametrize("S", [10 ** 7, 32 * 10 ** 6, 10 ** 8, 32 * 10 ** 7])
+def test_c5_64_ranks(S):
+    nic = {"alpha": 6.58e-3, "beta": 4e-11, "epsilon": 6e-12, "w_t": 9}
+    nvl = {"alpha": 1e-5, "beta": 4.0 / 900e9, "epsilon": 1e-13, "w_t": 9}
+    check_topology(T.two_level_doc([8] * 8, nic, nvl, T.TABLE5["server"]), S)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 8, 12, 16])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_single_switch_gentree(n, dtype):
+    doc = T.single_switch_doc(n, row("middle_sw"), T.TABLE5["server"])
+    for count in (1, n - 1, 1000 * n + 3, 10 ** 7):
+        if count >= 1:
+            check_topology(doc, count, dtype)
+
+
+@pytest.mark.parametrize("force", ["cps", "ring", "rhd", "hcps:4,2", "hcps:2,4", "hcps:2,2,2", "rb"])
+def test_forced_kinds_8(force):
+    doc = T.single_switch_doc(8, row("middle_sw"), T.TABLE5["server"])
+    p = OG.Params(2e-6, 1.0 / 770e9, 1e-14, 1.0 / 6.5e12, 1e-14, 6)
+    for count in (8, 1001, 1 << 20):
+        check_topology(doc, count, "bf16", params=p, force=force)
+
+
+def test_explicit_and_combined_params():
+    doc = T.single_switch_doc(12, row("middle_sw"), T.TABLE5["server"])
+    Sb = 4 * 10 ** 8
+    p = OG.Params(4.0e-3, 0.0, 0.0, 0.0391 / Sb, 0.01066 / Sb, 9, combined=0.6638 / Sb)
+    lp, _ = check_topology(doc, 10 ** 8, params=p)
+    assert lp.report()[-1]["chosen"] == "hcps[6,2]"
+
+
+@pytest.mark.slow
+def test_gtplan_topologies():
+    for name, doc in _gtplan_topos().items():
+        for S in (10 ** 7, 10 ** 8):
+            check_topology(doc, S)
+
+
+def test_random_trees():
+    rnd = random.Random(4202)
+    done = 0
+    while done < 80:
+        doc = _random_tree(rnd, max_servers=40)
+        try:
+            t = T.parse_topology(doc)
+        except T.TopologyError:
+            continue
+        N = len(t.servers)
+        check_topology(doc, rnd.randint(1, 40 * N), rnd.choice(["f32", "bf16"]))
+        done += 1
+
+
+@pytest.mark.parametrize("kind", ["cps", "ring", "rhd", "rb", "hcps:4,2", "hcps:2,3,4", "hcps:8,3"])
+def test_closed_form_bits(kind):
+    name, f = OP.parse_kind(kind)
+    n = 8 if name != "hcps" else 1
+    for x in f:
+        n *= x
+    p = OG.Params(6.58e-3, 6.4e-9 / 4, 6e-10 / 4, 1.87e-10 / 4, 1.22e-10 / 4, 9)
+    for S in (4, 4 * 10 ** 7 + 12, 123456789):
+        same_breakdown(G.genmodel_closed_form(kind, n, S, lib_params(p)),
+                       OG.closed_form_f64(name, n, S, p, f))
+
+
+def test_invalid_inputs_rejected():
+    bad = [T.single_switch_doc(1, row("middle_sw"), T.TABLE5["server"]), "{nope", '{"nodes": []}']
+    for doc in bad:
+        with pytest.raises(G.ArInvalid):
+            G.Plan.from_topology(doc, 10)
+        with pytest.raises(T.TopologyError):
+            T.parse_topology(doc)
+    doc = T.single_switch_doc(8, row("middle_sw"), T.TABLE5["server"])
+    for force in ("hcps:3,3", "bogus", "hcps:x"):
+        with pytest.raises(G.ArInvalid):
+            G.Plan.from_topology(doc, 100, force=force)
+    with pytest.raises(G.ArInvalid):
+        G.Plan.from_topology(doc, 0)
+
+
+def test_fit_parity_noiseless():
+    truth = (6.58e-3, 1.34e-9 / 4, 1.87e-10 / 4, 1.22e-10 / 4, 6)
+    rows = []
+    for n in range(2, 9):
+        for s in (1 << 20, 1 << 24, 1 << 28):
+            rows.append((n, s, OF.cps_forward(n, s, *truth)))
+    o = OF.fit_params(rows, 2, 8)
+    lp, sse = G.genmodel_fit(rows, 2, 8)
+    assert lp.w_t == o["w_t"] == 6 and lp.has_combined == 1
+    for a, b in ((lp.alpha, o["alpha"]), (lp.combined, o["combined"]), (lp.delta, o["delta"]),
+                 (lp.epsilon, o["epsilon"])):
+        assert a == pytest.approx(b, rel=1e-9)
+    lp2, _ = G.genmodel_fit(rows, 2, 8, link_bytes_per_s=900e9)
+    assert lp2.beta == 1.0 / 900e9 and lp2.gamma == pytest.approx(truth[1] - 2 / 900e9, rel=1e-9)
