@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
-    ap.add_argument("--cpu-sample-mib", type=float, default=8.0, help="oracle sample per rank (MiB)")
+    ap.add_argument("--cpu-sample-mib", type=float, default=64.0, help="oracle sample per rank (MiB)")
     return ap.parse_args()
 
 

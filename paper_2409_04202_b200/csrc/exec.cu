@@ -69,6 +69,7 @@ struct ExecArgs {
   unsigned long long epoch;
   unsigned long long timeout_ns;
   int rank0, world, cta_cap, esize;
+  int bulk;                  // 1 = cp.async.bulk-staged body, 0 = register body
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -226,6 +227,117 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
   }
 }
 
+// ------------------------------------------------------------------ bulk-staged body
+// Warp-specialised pipeline: warp 0 (one lane) streams tiles of every source into shared
+// memory with cp.async.bulk (the TMA bulk-copy engine; works on local and NVLink-peer
+// addresses alike) completing on a per-stage mbarrier; warps 1.. wait, sum the NSRC tiles
+// in plan order from shared memory and store the result to every destination, then release
+// the stage.  kStages x kStageBytes of loads stay in flight per CTA without tying up
+// registers — the memory-level parallelism the NVLink round trip (~2 us) needs.
+constexpr int kStages = 4;
+constexpr int kStageBytes = 48 * 1024;
+constexpr int kDynSmem = kStages * kStageBytes;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+struct Pipe {
+  unsigned long long full[kStages];
+  unsigned long long empty[kStages];
+};
+
+template <int NSRC, bool BF16>
+__device__ __noinline__ void body_bulk(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
+                                       Pipe &pp) {
+  constexpr int T = (kStageBytes / NSRC) / 16 * 16;   // bytes per source per tile
+  constexpr int TV = T / 16;                           // 16-byte vectors per source per tile
+  const size_t nv = v1 - v0;
+  const uint32_t ntiles = (uint32_t)((nv + TV - 1) / TV);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (uint32_t i = 0; i < ntiles; i++) {
+        const uint32_t gi = g + i, st = gi % kStages, use = gi / kStages;
+        if (use > 0) mbar_wait(&pp.empty[st], (use - 1) & 1);
+        const size_t t0 = v0 + (size_t)i * TV;
+        const uint32_t bytes = (uint32_t)min((size_t)TV, v1 - t0) * 16;
+        mbar_expect_tx(&pp.full[st], bytes * NSRC);
+        uint8_t *base = smem + st * kStageBytes;
+#pragma unroll
+        for (int k = 0; k < NSRC; k++) bulk_g2s(base + k * T, s.src[k] + t0, bytes, &pp.full[st]);
+      }
+    }
+  } else {
+    const int ndst = s.ndst;
+    const int nthr = blockDim.x - 32;
+    for (uint32_t i = 0; i < ntiles; i++) {
+      const uint32_t gi = g + i, st = gi % kStages, use = gi / kStages;
+      mbar_wait(&pp.full[st], use & 1);
+      const size_t t0 = v0 + (size_t)i * TV;
+      const int nvt = (int)min((size_t)TV, v1 - t0);
+      const uint4 *base = (const uint4 *)(smem + st * kStageBytes);
+      for (int v = threadIdx.x - 32; v < nvt; v += nthr) {
+        uint4 x[NSRC];
+#pragma unroll
+        for (int k = 0; k < NSRC; k++) x[k] = base[k * TV + v];
+        uint4 o;
+        if (NSRC == 1) {
+          o = x[0];
+        } else {
+          float acc[8];
+          acc_first<BF16>(acc, x[0]);
+#pragma unroll
+          for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[k]);
+          o = acc_pack<BF16>(acc);
+        }
+        for (int d = 0; d < ndst; d++) st_v4(s.dst[d] + t0 + v, o);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pp.empty[st]);
+    }
+  }
+  g += ntiles;
+}
+
+template <bool BF16>
+__device__ void body_dispatch_bulk(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem, Pipe &pp) {
+  switch (s.nsrc) {
+    case 1: body_bulk<1, BF16>(s, v0, v1, g, smem, pp); break;
+    case 2: body_bulk<2, BF16>(s, v0, v1, g, smem, pp); break;
+    case 3: body_bulk<3, BF16>(s, v0, v1, g, smem, pp); break;
+    case 4: body_bulk<4, BF16>(s, v0, v1, g, smem, pp); break;
+    case 5: body_bulk<5, BF16>(s, v0, v1, g, smem, pp); break;
+    case 6: body_bulk<6, BF16>(s, v0, v1, g, smem, pp); break;
+    case 7: body_bulk<7, BF16>(s, v0, v1, g, smem, pp); break;
+    case 8: body_bulk<8, BF16>(s, v0, v1, g, smem, pp); break;
+    default: body_generic<BF16>(s, v0, v1); break;
+  }
+}
+
 // Scalar elements [e0, e1) (unaligned head / tail), same summation order.
 __device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, const int *src_ranks, const int *dst_ranks,
                              long long e0, long long e1, bool bf16) {
@@ -269,6 +381,8 @@ __device__ __forceinline__ unsigned long long *flag_ptr(const ExecArgs &a, int p
 
 __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_constant__ ExecArgs a) {
   __shared__ OpShared sh;
+  __shared__ Pipe pp;
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
   const int lr = blockIdx.y;
   const int me = a.rank0 + lr;
   const int cta = blockIdx.x;
@@ -278,6 +392,15 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   const DevStep *prog = a.steps + a.prog_begin[lr];
   const int nst = a.prog_len[lr];
   const unsigned long long t_start = globaltimer();
+  uint32_t g = 0;   // bulk-pipeline tile counter (identical in every thread)
+  if (a.bulk && threadIdx.x == 0) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&pp.full[s], 1);
+      mbar_init(&pp.empty[s], blockDim.x / 32 - 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
   for (int si = 0; si < nst; si++) {
     const DevStep st = prog[si];
@@ -298,6 +421,9 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
         }
       }
       __syncthreads();
+      // the bulk loads below run in the async proxy: order them after the generic-proxy
+      // writes this acquire made visible
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     // ---- ops (a2 / a4)
     for (int oi = 0; oi < st.op_count; oi++) {
@@ -317,8 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       }
       const long long nv = ve - vb;
       const size_t v0 = (size_t)(vb + nv * cta / nctas), v1 = (size_t)(vb + nv * (cta + 1) / nctas);
-      if (bf16) body_dispatch<true>(sh, v0, v1);
-      else body_dispatch<false>(sh, v0, v1);
+      if (a.bulk) {
+        if (bf16) body_dispatch_bulk<true>(sh, v0, v1, g, dyn_smem, pp);
+        else body_dispatch_bulk<false>(sh, v0, v1, g, dyn_smem, pp);
+      } else {
+        if (bf16) body_dispatch<true>(sh, v0, v1);
+        else body_dispatch<false>(sh, v0, v1);
+      }
       if (cta == 0 && vb * 16 > b0) scalar_elems(sh, a, sr, dr, op.off, vb * vec_elems, bf16);
       if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(sh, a, sr, dr, ve * vec_elems, op.off + op.len, bf16);
     }
@@ -439,6 +570,7 @@ struct ar_comm {
   unsigned long long *err = nullptr;
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
   int last_launches = 0;
+  bool bulk = true;                            // cp.async.bulk-staged body (AR_EXEC_BODY=regs: register body)
 };
 
 namespace {
@@ -684,7 +816,8 @@ static void free_lowered(Lowered &L) {
 static int resident_ctas(int device) {
   int nsm = 0, per = 0;
   CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, 0));
+  CUDA_OK(cudaFuncSetAttribute(ar_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, kDynSmem));
   return nsm * std::max(per, 1);
 }
 
@@ -728,6 +861,7 @@ static void init_comm(ar_comm *c) {
     c->sig[c->rank] = c->sig_local;
   }
   if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) c->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
+  if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
 }
 
 }  // namespace
@@ -736,7 +870,11 @@ extern "C" {
 
 uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype) {
   uint64_t b = count * (uint64_t)(dtype == AR_BF16 ? 2 : 4);
-  return (b + 255) / 256 * 256;
+  static const uint64_t pad = [] {   // experiment knob: extra bytes between emulated ranks
+    const char *e = std::getenv("AR_EMU_STRIDE_PAD");
+    return e ? (std::strtoull(e, nullptr, 10) + 255) / 256 * 256 : 0ull;
+  }();
+  return (b + 255) / 256 * 256 + pad;
 }
 
 int ar_comm_create(int32_t rank, int32_t world, int32_t cuda_device, ar_comm **out) {
@@ -962,10 +1100,11 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.world = c->world;
   a.cta_cap = c->cta_cap;
   a.esize = plan->esize;
+  a.bulk = c->bulk ? 1 : 0;
   dim3 grid(c->nctas, c->local ? c->world : 1);
   void *args[] = {&a};
-  CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args, 0,
-                                      (cudaStream_t)stream));
+  CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
+                                      c->bulk ? kDynSmem : 0, (cudaStream_t)stream));
   c->last_launches = 1;
   return AR_OK;
 }

@@ -1,0 +1,76 @@
+"""Worker for tests/test_gpu_multi.py: one process per GPU (torchrun), real IPC peer maps
+over NVLink.  Every rank checks its own output bit-for-bit against the CPU oracle run on
+all ranks' (deterministic) inputs.  Exit code 0 = all cases bit-exact."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2409_04202_b200 as G  # noqa: E402
+from oracle import gentree as GT  # noqa: E402
+from oracle import plans as OP  # noqa: E402
+from oracle import simulate as SM  # noqa: E402
+from oracle import topology as T  # noqa: E402
+from synth import generator as GEN  # noqa: E402
+from tests.gpu_util import assert_bits_equal  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    comm = G.Comm.create(rank, world, local)
+    doc = T.single_switch_doc(world, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
+                              {"gamma": 0.0, "delta": 4 / 6.54e12})
+    topo = T.parse_topology(doc)
+    kinds = [None, "cps", "ring", "rb"]
+    if world & (world - 1) == 0:
+        kinds.append("rhd")
+    if world == 4:
+        kinds.append("hcps:2,2")
+    if world == 8:
+        kinds += ["hcps:4,2", "hcps:2,4", "hcps:2,2,2"]
+    seed = GEN.config_seed(2)
+    keep = []
+    failures = 0
+    for dtype in ("f32", "bf16"):
+        es = 4 if dtype == "f32" else 2
+        for count in (1, world * 4096 + 5, 1 << 20, 3_000_001):
+            buf = torch.zeros(max(16, count * es), dtype=torch.uint8, device="cuda")
+            keep.append(buf)
+            comm.register(buf)
+            for force in kinds:
+                G.fill_synthetic(buf, count, dtype, seed, rank, 0)
+                plan = G.Plan.from_topology(doc, count, dtype, None, force)
+                oplan, _ = GT.gentree(topo, count, es, force=force)
+                assert plan.to_json() == OP.plan_to_json(oplan, dtype)
+                for _ in range(2):
+                    G.allreduce_exec(plan, comm, buf)
+                torch.cuda.synchronize()
+                comm.async_error()
+                xs = GEN.generate_all(seed, world, count, dtype)
+                want = SM.simulate(oplan, SM.simulate(oplan, xs, dtype), dtype)[rank]
+                got = buf.cpu().numpy()[: count * es].view(np.float32 if dtype == "f32" else np.uint16)
+                try:
+                    assert_bits_equal(got, want, dtype, f"rank {rank} {dtype} count={count} plan={force}")
+                except AssertionError as e:
+                    print(e, flush=True)
+                    failures += 1
+                dist.barrier()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"mp_worker world={world}: {'OK' if failures == 0 else f'{failures} FAILURES'}", flush=True)
+    sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,36 @@
+"""Multi-GPU parity (one process per GPU, IPC peer maps over NVLink/NVSwitch).
+
+Runs tests/mp_worker.py under torchrun on 2, 4 and 8 GPUs when the box has them; every
+rank's buffer must be bit-exact against the CPU oracle for GenTree, CPS, Ring, RB, RHD and
+HCPS plans, fp32 and bf16, ragged sizes, two back-to-back calls per buffer."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from tests.gpu_util import cuda_ok
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def ngpus():
+    if not cuda_ok():
+        return 0
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_multi_process_bit_exact(world):
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29617", os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"mp_worker world={world}: OK" in r.stdout
