@@ -179,6 +179,14 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *comm, void *dptr, void *ho
 /* Device kernels launched by the last allreduce_exec of this comm (per rank, per call). */
 int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
 
+/* Inspection (host only, no GPU needed): the per-rank device step tables allreduce_exec
+ * runs for `plan` — after op merging, RS/AG fusion and the dependency analysis — as JSON
+ * {"ranks":[{"steps":[{"slot":s,"ops":[{"off","len","src":[..],"dst":[..]}],
+ * "waits":[[rank,slot,paired],..],"notify":[..]}]}]}.  Slot 0 = entry; slot s+1 = after
+ * plan step s; the last step of each rank (exit) has only paired waits.  Same buffer
+ * protocol as gt_plan_to_json (the size query itself returns AR_EINVAL with *needed set). */
+int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed);
+
 /* ------------------------------------------------------------------ inputs and harness */
 
 /* Fill `count` elements at dptr with the seeded synthetic generator G(seed, rank, i),

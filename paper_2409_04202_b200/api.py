@@ -102,6 +102,10 @@ class Plan:
     def report(self) -> list:
         return json.loads(self._str(lib.gt_plan_report_json))
 
+    def lowering(self) -> dict:
+        """Device step tables allreduce_exec runs for this plan (host-only inspection)."""
+        return json.loads(self._str(lib.ar_plan_lowering_json))
+
     def info(self) -> dict:
         n, s, c, d = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64(), ctypes.c_int32()
         check(lib.gt_plan_info(self._h, ctypes.byref(n), ctypes.byref(s), ctypes.byref(c), ctypes.byref(d)))

@@ -1040,6 +1040,50 @@ int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
   return AR_OK;
 }
 
+int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed) {
+  SYS_TRY({
+    if (!plan) throw InvalidArg("null plan");
+    std::vector<DevStep> st;
+    std::vector<DevOp> ops;
+    std::vector<DevWait> w;
+    std::vector<int> rk, pb, pl;
+    lower_plan(plan->plan, plan->plan.n, st, ops, w, rk, pb, pl);
+    std::string o = "{\"ranks\":[";
+    for (int r = 0; r < plan->plan.n; r++) {
+      o += r ? ",{\"steps\":[" : "{\"steps\":[";
+      for (int i = 0; i < pl[r]; i++) {
+        const DevStep &d = st[pb[r] + i];
+        o += i ? "," : "";
+        o += "{\"slot\":" + std::to_string(d.slot) + ",\"ops\":[";
+        for (int k = 0; k < d.op_count; k++) {
+          const DevOp &x = ops[d.op_begin + k];
+          o += k ? "," : "";
+          o += "{\"off\":" + std::to_string(x.off) + ",\"len\":" + std::to_string(x.len) + ",\"src\":[";
+          for (int j = 0; j < x.nsrc; j++) o += (j ? "," : "") + std::to_string(rk[x.src_begin + j]);
+          o += "],\"dst\":[";
+          for (int j = 0; j < x.ndst; j++) o += (j ? "," : "") + std::to_string(rk[x.dst_begin + j]);
+          o += "]}";
+        }
+        o += "],\"waits\":[";
+        for (int k = 0; k < d.wait_count; k++) {
+          const DevWait &x = w[d.wait_begin + k];
+          o += (k ? ",[" : "[") + std::to_string(x.rank) + "," + std::to_string(x.slot) + "," +
+               std::to_string(x.paired) + "]";
+        }
+        o += "],\"notify\":[";
+        for (int k = 0; k < d.notify_count; k++) o += (k ? "," : "") + std::to_string(rk[d.notify_begin + k]);
+        o += "]}";
+      }
+      o += "]}";
+    }
+    o += "]}";
+    if (needed) *needed = o.size() + 1;
+    if (!buf || cap < o.size() + 1) throw InvalidArg("buffer too small");
+    std::memcpy(buf, o.c_str(), o.size() + 1);
+    return AR_OK;
+  })
+}
+
 static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream) {
   if (!plan || !c || !dptr) throw InvalidArg("null argument");
   if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");

@@ -1,0 +1,123 @@
+"""Host-side executor logic on CPU: the step tables `allreduce_exec` launches
+(ar_plan_lowering_json) are run by a CTA-level interpreter of the kernel's flag protocol
+under random schedules, and must produce the oracle's result with no deadlock.
+
+The interpreter models what the kernel does: every rank runs its step list on C CTAs; a CTA
+may start a step only when its waits are satisfied (paired: the producer's same-index CTA
+has posted the slot for this call; full: all producer CTAs have); it then executes its slice
+of every op (sources read, summed left to right in fp32, written to every destination) and
+posts the step's slot to every consumer.  A rank's call k+1 starts only after all its CTAs
+finished call k (stream order).  Random interleavings expose any missing dependency (RAW,
+WAR, WAW, across steps or across calls) as a wrong result."""
+import random
+
+import numpy as np
+import pytest
+
+import paper_2409_04202_b200 as G
+from oracle import gentree as GT
+from oracle import simulate as SM
+from oracle import topology as T
+from synth import generator as GEN
+
+
+def single_switch(world):
+    return T.single_switch_doc(world, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
+                               {"gamma": 0.0, "delta": 4 / 6.54e12})
+
+
+def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random) -> list:
+    n = len(low["ranks"])
+    bufs = [x.astype(np.float32).copy() for x in inputs]
+    flags = {}                                  # (consumer, slot, producer, cta) -> epoch
+    pc = [[0] * ctas for _ in range(n)]         # step index per CTA
+    epoch = [[1] * ctas for _ in range(n)]      # call number per CTA
+    done = [[False] * ctas for _ in range(n)]
+
+    def runnable(r, c):
+        if done[r][c]:
+            return False
+        prog = low["ranks"][r]["steps"]
+        if pc[r][c] == 0 and epoch[r][c] > 1:
+            # stream order: call k+1 starts after every CTA of this rank finished call k
+            if any(epoch[r][cc] < epoch[r][c] for cc in range(ctas)):
+                return False
+        st = prog[pc[r][c]]
+        e = epoch[r][c]
+        for (t, slot, paired) in st["waits"]:
+            cs = [c] if paired else range(ctas)
+            if any(flags.get((r, slot, t, cc), 0) < e for cc in cs):
+                return False
+        return True
+
+    def step(r, c):
+        st = low["ranks"][r]["steps"][pc[r][c]]
+        for op in st["ops"]:
+            lo = op["off"] + op["len"] * c // ctas
+            hi = op["off"] + op["len"] * (c + 1) // ctas
+            if hi <= lo:
+                continue
+            acc = bufs[op["src"][0]][lo:hi].copy()
+            for q in op["src"][1:]:
+                acc = acc + bufs[q][lo:hi]
+            for d in op["dst"]:
+                bufs[d][lo:hi] = acc
+        for consumer in st["notify"]:
+            flags[(consumer, st["slot"], r, c)] = epoch[r][c]
+        pc[r][c] += 1
+        if pc[r][c] == len(low["ranks"][r]["steps"]):
+            if epoch[r][c] == calls:
+                done[r][c] = True
+            else:
+                epoch[r][c] += 1
+                pc[r][c] = 0
+
+    agents = [(r, c) for r in range(n) for c in range(ctas)]
+    while True:
+        ready = [a for a in agents if runnable(*a)]
+        if not ready:
+            assert all(done[r][c] for r, c in agents), "deadlock in the lowered flag protocol"
+            return bufs
+        step(*rnd.choice(ready))
+
+
+CASES = [(single_switch(w), w, k) for w in (2, 3, 4, 8) for k in (None, "cps", "ring", "rb")]
+CASES += [(single_switch(8), 8, k) for k in ("rhd", "hcps:4,2", "hcps:2,4", "hcps:2,2,2")]
+CASES += [(single_switch(6), 6, k) for k in ("hcps:3,2", "hcps:2,3")]
+CASES += [(T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]), 4, None),
+          (T.two_level_doc([3, 4], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]), 7, None),
+          (T.two_level_doc([2, 2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]), 6, None)]
+
+
+@pytest.mark.parametrize("doc,world,force", CASES)
+def test_lowered_protocol_random_schedules(doc, world, force):
+    count = 37 * world + 5
+    plan = G.Plan.from_topology(doc, count, "f32", None, force)
+    low = plan.lowering()
+    oplan, _ = GT.gentree(T.parse_topology(doc), count, 4, force=force)
+    xs = [(GEN.generate(3, r, count, "f32", "integer")) for r in range(world)]
+    want = SM.simulate(oplan, SM.simulate(oplan, xs, "f32"), "f32")
+    rnd = random.Random(world * 100 + len(force or ""))
+    for trial in range(6):
+        got = interpret(low, xs, ctas=rnd.choice([1, 2, 3]), calls=2, rnd=rnd)
+        for r in range(world):
+            assert np.array_equal(got[r], want[r]), (force, trial, r)
+
+
+def test_cps_is_one_fused_step_with_two_flag_rounds():
+    """CPS lowers to entry -> one fused pull-reduce-push op -> exit: the AG step disappears
+    (P:402's one read/one write per element; A = 2 flag round trips)."""
+    low = G.Plan.from_topology(single_switch(8), 8000, "bf16", None, "cps").lowering()
+    for r, rk in enumerate(low["ranks"]):
+        slots = [s["slot"] for s in rk["steps"]]
+        assert slots == [0, 1, 0]
+        entry, work, exit_ = rk["steps"]
+        assert sorted(entry["notify"]) == [q for q in range(8) if q != r]
+        (op,) = work["ops"]
+        assert op["src"] == list(range(8)) and sorted(op["dst"]) == list(range(8)) and op["dst"][0] == r
+        assert all(p == 1 for _, _, p in exit_["waits"]) and len(exit_["waits"]) == 7
+
+
+def test_lowering_rejects_bad_buffer_query():
+    plan = G.Plan.from_topology(single_switch(2), 10, "f32")
+    assert plan.lowering()["ranks"][1]["steps"]
