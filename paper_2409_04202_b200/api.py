@@ -220,6 +220,24 @@ def _stream(stream) -> int | None:
     return int(stream.cuda_stream) or None
 
 
+class Executor:
+    """allreduce_exec(plan, comm, buf) with the arguments marshalled once, for repeated calls
+    (e.g. every training step, or inside torch.cuda.graph capture: the kernel launch carries no
+    per-call host state, the call epoch lives on the device)."""
+
+    def __init__(self, plan: Plan, comm: Comm, buf, stream=None):
+        info = plan.info()
+        self._keep = (plan, comm, buf)
+        self._args = (plan.handle, comm.handle, ctypes.c_void_p(_ptr(buf)), info["count"], info["dtype"],
+                      ctypes.c_void_p(_stream(stream)))
+        self._f = lib.allreduce_exec
+
+    def __call__(self):
+        rc = self._f(*self._args)
+        if rc:
+            check(rc)
+
+
 def allreduce_exec(plan: Plan, comm: Comm, buf, count: int | None = None, dtype=None, stream=None):
     """In-place AllReduce of `buf` (torch tensor or device pointer) with `plan`."""
     info = None

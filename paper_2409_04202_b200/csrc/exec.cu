@@ -66,7 +66,8 @@ struct ExecArgs {
   char *bufs[AR_MAX_RANKS];            // rank -> data buffer base (as seen here)
   unsigned long long *sigs[AR_MAX_RANKS];  // rank -> flag page base (as seen here)
   unsigned long long *err;
-  unsigned long long epoch;
+  unsigned long long *epoch_dev;   // last completed call's epoch (device-resident: graph-capturable)
+  unsigned int *done_ctr;          // CTAs finished in the current call
   unsigned long long timeout_ns;
   int rank0, world, cta_cap, esize;
   int bulk;                  // 1 = cp.async.bulk-staged body, 0 = register body
@@ -393,6 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   const int nst = a.prog_len[lr];
   const unsigned long long t_start = globaltimer();
   uint32_t g = 0;   // bulk-pipeline tile counter (identical in every thread)
+  // this call's epoch = last completed + 1; the last CTA to finish publishes it (below), so
+  // every CTA reads the same value and the launch carries no per-call host argument
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
   if (a.bulk && threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&pp.full[s], 1);
@@ -401,6 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const unsigned long long epoch = s_epoch;
 
   for (int si = 0; si < nst; si++) {
     const DevStep st = prog[si];
@@ -413,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
         if (w.paired && c != cta) continue;
         const unsigned long long *f = flag_ptr(a, me, w.slot, w.rank, c);
         unsigned int spins = 0;
-        while (ld_acquire_sys(f) < a.epoch) {
+        while (ld_acquire_sys(f) < epoch) {
           if ((++spins & 1023u) == 0 && globaltimer() - t_start > a.timeout_ns) {
             atomicExch(a.err, 1ull);
             break;
@@ -459,8 +465,18 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       __syncthreads();
       for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
         const int consumer = a.ranks[st.notify_begin + i];
-        st_release_sys(flag_ptr(a, consumer, st.slot, me, cta), a.epoch);
+        st_release_sys(flag_ptr(a, consumer, st.slot, me, cta), epoch);
       }
+    }
+  }
+  // publish the epoch once every CTA of this launch is done (they have all read it)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (atomicAdd(a.done_ctr, 1u) == total - 1) {
+      *(volatile unsigned int *)a.done_ctr = 0;
+      *(volatile unsigned long long *)a.epoch_dev = epoch;
+      __threadfence();
     }
   }
 }
@@ -571,6 +587,12 @@ struct ar_comm {
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
   int last_launches = 0;
   bool bulk = true;                            // cp.async.bulk-staged body (AR_EXEC_BODY=regs: register body)
+  // launch-argument cache for back-to-back calls with the same plan and buffer
+  bool fast_valid = false;
+  uint64_t fast_uid = 0;
+  void *fast_dptr = nullptr;
+  int fast_nctas = -1;
+  ExecArgs fast_args{};
 };
 
 namespace {
@@ -851,8 +873,9 @@ static void init_comm(ar_comm *c) {
   const size_t pages = c->local ? c->world : 1;
   CUDA_OK(cudaMalloc(&c->sig_local, pages * c->page_elems * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->sig_local, 0, pages * c->page_elems * sizeof(unsigned long long)));
-  CUDA_OK(cudaMalloc(&c->err, sizeof(unsigned long long)));
-  CUDA_OK(cudaMemset(c->err, 0, sizeof(unsigned long long)));
+  // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter
+  CUDA_OK(cudaMalloc(&c->err, 4 * sizeof(unsigned long long)));
+  CUDA_OK(cudaMemset(c->err, 0, 4 * sizeof(unsigned long long)));
   c->sig.assign(c->world, nullptr);
   if (c->local) {
     for (int r = 0; r < c->world; r++) c->sig[r] = c->sig_local + (size_t)r * c->page_elems;
@@ -965,6 +988,7 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     for (auto it = c->regs.begin(); it != c->regs.end(); ++it)
       if (it->local == reg.local) { c->regs.erase(it); break; }
     c->regs.push_back(reg);
+    c->fast_valid = false;
     return AR_OK;
   })
 }
@@ -1002,6 +1026,7 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
       if (!c->sig[t]) c->sig[t] = (unsigned long long *)open(b->sig);
     }
     reg->opened = true;
+    c->fast_valid = false;
     c->sig_opened = true;
     return AR_OK;
   })
@@ -1089,7 +1114,19 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");
   if ((uint64_t)plan->plan.count != count || plan->dtype != dtype) throw InvalidArg("count/dtype differ from the plan's");
   if ((uintptr_t)dptr % 16) throw InvalidArg("buffer must be 16-byte aligned");
-  CUDA_OK(cudaSetDevice(c->device));
+  int cur = -1;
+  CUDA_OK(cudaGetDevice(&cur));
+  if (cur != c->device) CUDA_OK(cudaSetDevice(c->device));
+  dim3 grid(c->nctas, c->local ? c->world : 1);
+  if (c->fast_valid && c->fast_uid == plan->uid && c->fast_dptr == dptr && c->fast_nctas == c->nctas) {
+    // steady state: same plan and buffer as the previous call — launch the cached arguments
+    ++c->epoch;
+    void *args[] = {&c->fast_args};
+    CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
+                                        c->bulk ? kDynSmem : 0, (cudaStream_t)stream));
+    c->last_launches = 1;
+    return AR_OK;
+  }
   const size_t bytes = count * (size_t)plan->esize;
   ExecArgs a{};
   if (c->local) {
@@ -1138,14 +1175,20 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.prog_begin = L.prog_begin;
   a.prog_len = L.prog_len;
   a.err = c->err;
-  a.epoch = ++c->epoch;
+  ++c->epoch;
+  a.epoch_dev = c->err + 1;
+  a.done_ctr = (unsigned int *)(c->err + 2);
   a.timeout_ns = c->timeout_ns;
   a.rank0 = c->local ? 0 : c->rank;
   a.world = c->world;
   a.cta_cap = c->cta_cap;
   a.esize = plan->esize;
   a.bulk = c->bulk ? 1 : 0;
-  dim3 grid(c->nctas, c->local ? c->world : 1);
+  c->fast_args = a;
+  c->fast_uid = plan->uid;
+  c->fast_dptr = dptr;
+  c->fast_nctas = c->nctas;
+  c->fast_valid = true;
   void *args[] = {&a};
   CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
                                       c->bulk ? kDynSmem : 0, (cudaStream_t)stream));

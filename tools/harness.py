@@ -1,0 +1,264 @@
+#!/usr/bin/env python
+"""GenModel measurement harness (configs C2, C3, C4) — JSONL on stdout.
+
+Multi-GPU (torchrun, one process per GPU; rank 0 prints):
+    torchrun --nproc-per-node N tools/harness.py sweep  [--dtype f32] [--plans "gentree;cps;ring"]
+        C2: busbw vs size 64 KiB..1 GiB for our plans and NCCL all_reduce on the same box
+    torchrun --nproc-per-node N tools/harness.py cps
+        C3-iii: CPS AllReduce times at this N for the §3.4 fit (run for N = 2..max)
+Single GPU, emulated ranks (all ranks of a plan in one launch, "8 ranks/GPU"):
+    python tools/harness.py emu-sweep --ranks 8
+    python tools/harness.py emu-cps   --max-ranks 8
+    python tools/harness.py fanin                           (C3-i, Eq. 6 local fan-in)
+
+Timing modes (--timing, comma list):
+  eager — CUDA events around every call, 5 warm-up calls, inputs refilled from the seeded
+          generator every 8 calls outside the events; includes host launch overhead
+  graph — `reps` calls captured in one CUDA graph (ours: the kernel has no per-call host
+          argument; NCCL: graph-captured all_reduce), replayed once, time / reps: device time
+Multi-GPU times are the max over ranks.  Mean and median are reported (the paper uses the
+mean; reading Q20).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2409_04202_b200 as G  # noqa: E402
+
+NOMINAL = {"alpha": 3e-6, "beta": 1 / 900e9, "gamma": 0.0, "delta": 1 / 6.54e12, "epsilon": 0.0, "w_t": 9}
+SIZES = [1 << k for k in range(16, 31)]       # 64 KiB .. 1 GiB
+
+
+def doc(world, p=NOMINAL):
+    nodes = [{"id": "sw", "kind": "switch", "parent": None, "uplink": None}]
+    for i in range(world):
+        nodes.append({"id": f"s{i}", "kind": "server", "parent": "sw",
+                      "uplink": {"alpha": p["alpha"], "beta": p["beta"] * 4, "epsilon": p["epsilon"] * 4,
+                                 "w_t": int(p["w_t"])},
+                      "compute": {"gamma": p["gamma"] * 4, "delta": p["delta"] * 4}})
+    return json.dumps({"nodes": nodes})
+
+
+def kinds_for(world, plans):
+    out = []
+    for k in plans.split(";"):
+        if k == "rhd" and world & (world - 1):
+            continue
+        if k.startswith("hcps:"):
+            prod = 1
+            for x in k[5:].split(","):
+                prod *= int(x)
+            if prod != world:
+                continue
+        out.append(k)
+    return out
+
+
+def reps_for(nbytes):
+    return 50 if nbytes <= 64 << 20 else 20
+
+
+class Timer:
+    def __init__(self, dist):
+        self.dist = dist
+
+    def _sync(self):
+        torch.cuda.synchronize()
+        if self.dist:
+            self.dist.barrier()
+
+    def _max(self, ts):
+        t = torch.tensor(ts, dtype=torch.float64, device="cuda")
+        if self.dist:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.cpu().tolist()
+
+    def run(self, make, reps, refill, mode):
+        """make() -> callable issuing one AllReduce on the current stream."""
+        if mode == "eager":
+            fn = make()
+            for _ in range(5):
+                fn()
+            refill()
+            self._sync()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+            for i in range(reps):
+                if i and i % 8 == 0:
+                    refill()
+                evs[i][0].record()
+                fn()
+                evs[i][1].record()
+            torch.cuda.synchronize()
+            ts = self._max([a.elapsed_time(b) / 1e3 for a, b in evs])
+            return {"t_mean": statistics.mean(ts), "t_med": statistics.median(ts), "t_min": min(ts),
+                    "reps": reps, "timing": "eager"}
+        # graph
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn = make()
+            for _ in range(3):
+                fn()
+        torch.cuda.current_stream().wait_stream(s)
+        self._sync()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn = make()
+            for _ in range(reps):
+                fn()
+        self._sync()
+        g.replay()
+        refill()
+        self._sync()
+        ts = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3 / reps)
+            refill()
+            self._sync()
+        ts = self._max(ts)
+        del g
+        return {"t_mean": statistics.mean(ts), "t_med": statistics.median(ts), "t_min": min(ts), "reps": reps,
+                "timing": "graph"}
+
+
+def busbw(nbytes, n, t):
+    return nbytes / t * 2 * (n - 1) / n / 1e9
+
+
+def emit(rank, row):
+    if rank == 0:
+        print(json.dumps(row), flush=True)
+
+
+def multi(args):
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = G.Comm.create(rank, world, local)
+    es = 4 if args.dtype == "f32" else 2
+    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    sizes = args.sizes or SIZES
+    if args.mode == "cps":
+        sizes = [1 << 20, 1 << 22, 1 << 24, 1 << 26, 1 << 28]
+    buf = torch.empty(max(sizes), dtype=torch.uint8, device="cuda")
+    timer = Timer(dist)
+    modes = args.timing.split(",")
+    for nbytes in sizes:
+        count = nbytes // es
+        view = buf[:nbytes]
+        comm.register(view)
+
+        def refill():
+            G.fill_synthetic(view, count, args.dtype, 11, rank, 0)
+
+        plans = ["cps"] if args.mode == "cps" else kinds_for(world, args.plans)
+        for k in plans:
+            plan = G.Plan.from_topology(doc(world), count, args.dtype, None, None if k == "gentree" else k)
+            for mode in modes:
+                r = timer.run(lambda: G.Executor(plan, comm, view), reps_for(nbytes), refill, mode)
+                emit(rank, {"mode": args.mode, "impl": "ours", "plan": k, "chosen": plan.report()[-1]["chosen"],
+                            "n": world, "bytes": nbytes, "dtype": args.dtype, **r,
+                            "busbw_med": busbw(nbytes, world, r["t_med"]),
+                            "busbw_mean": busbw(nbytes, world, r["t_mean"])})
+        if args.mode == "sweep" and not args.no_nccl:
+            t = view.view(tdt)
+            for mode in modes:
+                r = timer.run(lambda: (lambda: dist.all_reduce(t)), reps_for(nbytes), refill, mode)
+                emit(rank, {"mode": "sweep", "impl": "nccl", "plan": os.environ.get("NCCL_ALGO", "default"),
+                            "n": world, "bytes": nbytes, "dtype": args.dtype, **r,
+                            "busbw_med": busbw(nbytes, world, r["t_med"]),
+                            "busbw_mean": busbw(nbytes, world, r["t_mean"]),
+                            "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))})
+    comm.async_error()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
+def emu(args):
+    torch.cuda.set_device(0)
+    es = 4 if args.dtype == "f32" else 2
+    timer = Timer(None)
+    modes = args.timing.split(",")
+    worlds = list(range(2, args.max_ranks + 1)) if args.mode == "emu-cps" else [args.ranks]
+    sizes = args.sizes or ([1 << 20, 1 << 22, 1 << 24, 1 << 26, 1 << 28] if args.mode == "emu-cps"
+                           else [s for s in SIZES if s * args.ranks <= (8 << 30)])
+    for world in worlds:
+        comm = G.Comm.local(world, 0)
+        plans = ["cps"] if args.mode == "emu-cps" else kinds_for(world, args.plans)
+        for nbytes in sizes:
+            count = nbytes // es
+            stride = G.rank_stride_bytes(count, args.dtype)
+            buf = torch.empty(world * stride, dtype=torch.uint8, device="cuda")
+
+            def refill():
+                for r in range(world):
+                    G.fill_synthetic(buf.data_ptr() + r * stride, count, args.dtype, 11, r, 0)
+
+            for k in plans:
+                plan = G.Plan.from_topology(doc(world), count, args.dtype, None, None if k == "gentree" else k)
+                for mode in modes:
+                    r = timer.run(lambda: G.Executor(plan, comm, buf), reps_for(nbytes), refill, mode)
+                    emit(0, {"mode": args.mode, "impl": "ours", "plan": k, "chosen": plan.report()[-1]["chosen"],
+                             "n": world, "bytes": nbytes, "dtype": args.dtype, "emulated": True, **r,
+                             "busbw_med": busbw(nbytes, world, r["t_med"]),
+                             "hbm_gbs_med": 2 * world * nbytes / r["t_med"] / 1e9})
+            del buf
+        comm.async_error()
+        comm.destroy()
+
+
+def fanin(args):
+    """C3-i: k-way local reduce of 150M-float vectors, Eq. 6."""
+    torch.cuda.set_device(0)
+    count = args.count
+    es = 4 if args.dtype == "f32" else 2
+    bufs = [torch.empty(count * es, dtype=torch.uint8, device="cuda") for _ in range(args.kmax + 1)]
+    for i, b in enumerate(bufs):
+        G.fill_synthetic(b, count, args.dtype, 7, i, 0)
+    timer = Timer(None)
+    for k in range(2, args.kmax + 1):
+        r = timer.run(lambda: (lambda: G.local_reduce(bufs[:k], bufs[-1], count, args.dtype)), 20,
+                      lambda: None, "eager")
+        emit(0, {"mode": "fanin", "k": k, "count": count, "dtype": args.dtype, **r,
+                 "t_per_add_med": r["t_med"] / (k - 1),
+                 "hbm_gbs_med": (k + 1) * count * es / r["t_med"] / 1e9})
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin"])
+    ap.add_argument("--dtype", default="f32")
+    ap.add_argument("--plans", default="gentree;cps;ring;rhd;rb;hcps:2,2;hcps:4,2;hcps:2,4;hcps:2,2,2",
+                    help="';'-separated plan kinds")
+    ap.add_argument("--timing", default="eager,graph")
+    ap.add_argument("--ranks", type=int, default=8)
+    ap.add_argument("--max-ranks", type=int, default=8)
+    ap.add_argument("--sizes", type=int, nargs="*", default=None)
+    ap.add_argument("--count", type=int, default=150_000_000)
+    ap.add_argument("--kmax", type=int, default=8)
+    ap.add_argument("--no-nccl", action="store_true")
+    a = ap.parse_args()
+    if a.mode in ("sweep", "cps"):
+        multi(a)
+    elif a.mode == "fanin":
+        fanin(a)
+    else:
+        emu(a)
