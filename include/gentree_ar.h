@@ -179,6 +179,16 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *comm, void *dptr, void *ho
 /* Device kernels launched by the last allreduce_exec of this comm (per rank, per call). */
 int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
 
+/* Tracing: when enabled, thread 0 of every CTA writes %globaltimer (ns) at kernel
+ * start, after each step's waits, after its ops, after its notifies, and at exit, into
+ * slots_per_cta stamps per CTA ([local rank][cta][slot]; slot 0 = start, 1+3i / 2+3i / 3+3i =
+ * step i after waits / ops / notify, last = end; unused slots hold stale values).  Costs a few
+ * global stores per step; off by default.  read: synchronises the device, copies the stamps
+ * of the last call into `out` (cap elements); AR_EINVAL if tracing is off or cap is short. */
+int ar_comm_set_trace(ar_comm *comm, int32_t enable);
+int ar_comm_read_trace(ar_comm *comm, uint64_t *out, size_t cap, size_t *n, int32_t *slots_per_cta,
+                       int32_t *ctas_per_rank);
+
 /* Inspection (host only, no GPU needed): the per-rank device step tables allreduce_exec
  * runs for `plan` — after op merging, RS/AG fusion and the dependency analysis — as JSON
  * {"ranks":[{"steps":[{"slot":s,"ops":[{"off","len","src":[..],"dst":[..]}],

@@ -87,6 +87,9 @@ _SIGS = {
     "ar_comm_destroy": (I32, [P]),
     "ar_comm_last_launch_count": (I32, [P, ctypes.POINTER(I32)]),
     "ar_plan_lowering_json": (I32, [P, ctypes.c_char_p, SZ, ctypes.POINTER(SZ)]),
+    "ar_comm_set_trace": (I32, [P, I32]),
+    "ar_comm_read_trace": (I32, [P, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ), ctypes.POINTER(I32),
+                                 ctypes.POINTER(I32)]),
     "ar_rank_stride_bytes": (U64, [U64, I32]),
     "allreduce_exec": (I32, [P, P, P, U64, I32, P]),
     "allreduce_exec_host": (I32, [P, P, P, P, U64, I32, P]),

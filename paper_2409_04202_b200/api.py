@@ -184,6 +184,19 @@ class Comm:
         dist.all_gather_object(blobs, blob, group=group)
         self.open_peers(blobs)
 
+    def set_trace(self, enable: bool = True):
+        check(lib.ar_comm_set_trace(self._h, 1 if enable else 0))
+
+    def read_trace(self):
+        """globaltimer stamps (ns) of the last call: array [local ranks, ctas, slots]."""
+        import numpy as np
+        n, slots, ctas = ctypes.c_size_t(), ctypes.c_int32(), ctypes.c_int32()
+        lib.ar_comm_read_trace(self._h, None, 0, ctypes.byref(n), ctypes.byref(slots), ctypes.byref(ctas))
+        out = np.zeros(n.value, dtype=np.uint64)
+        check(lib.ar_comm_read_trace(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), n.value,
+                                     None, None, None))
+        return out.reshape(-1, ctas.value, slots.value)
+
     def async_error(self):
         check(lib.ar_comm_get_async_error(self._h))
 

@@ -39,6 +39,8 @@ constexpr int kThreads = 512;
 constexpr int kMaxSlots = 256;        // plan steps + entry (slot 0)
 constexpr int kCtaCapMulti = 256;     // flag page CTA dimension, multi-process comms
 constexpr uint32_t kBlobMagic = 0x47544152u;  // "GTAR"
+constexpr int kTraceSteps = 64;       // steps traced per CTA
+constexpr int kTraceSlots = 2 + 3 * kTraceSteps;
 
 // ------------------------------------------------------------------ device tables
 struct DevOp {
@@ -71,6 +73,7 @@ struct ExecArgs {
   unsigned long long timeout_ns;
   int rank0, world, cta_cap, esize;
   int bulk;                  // 1 = cp.async.bulk-staged body, 0 = register body
+  unsigned long long *trace; // optional globaltimer stamps (kTraceSlots per CTA), nullptr = off
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -393,6 +396,10 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   const DevStep *prog = a.steps + a.prog_begin[lr];
   const int nst = a.prog_len[lr];
   const unsigned long long t_start = globaltimer();
+  unsigned long long *tr = a.trace ? a.trace + (size_t)(lr * gridDim.x + cta) * kTraceSlots : nullptr;
+#define AR_TRACE(i) \
+  if (tr && threadIdx.x == 0 && (i) < kTraceSlots) tr[i] = globaltimer()
+  AR_TRACE(0);
   uint32_t g = 0;   // bulk-pipeline tile counter (identical in every thread)
   // this call's epoch = last completed + 1; the last CTA to finish publishes it (below), so
   // every CTA reads the same value and the launch carries no per-call host argument
@@ -431,6 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       // writes this acquire made visible
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
+    AR_TRACE(1 + 3 * si);
     // ---- ops (a2 / a4)
     for (int oi = 0; oi < st.op_count; oi++) {
       const DevOp op = a.ops[st.op_begin + oi];
@@ -459,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       if (cta == 0 && vb * 16 > b0) scalar_elems(sh, a, sr, dr, op.off, vb * vec_elems, bf16);
       if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(sh, a, sr, dr, ve * vec_elems, op.off + op.len, bf16);
     }
+    AR_TRACE(2 + 3 * si);
     // ---- notify (release our slot on every consumer's page)
     if (st.notify_count > 0) {
       __threadfence_system();
@@ -468,7 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
         st_release_sys(flag_ptr(a, consumer, st.slot, me, cta), epoch);
       }
     }
+    AR_TRACE(3 + 3 * si);
   }
+  AR_TRACE(kTraceSlots - 1);
+#undef AR_TRACE
   // publish the epoch once every CTA of this launch is done (they have all read it)
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -593,6 +605,8 @@ struct ar_comm {
   void *fast_dptr = nullptr;
   int fast_nctas = -1;
   ExecArgs fast_args{};
+  unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
+  size_t trace_elems = 0;
 };
 
 namespace {
@@ -1055,6 +1069,7 @@ int ar_comm_destroy(ar_comm *c) {
   for (auto &kv : c->ipc_opened) cudaIpcCloseMemHandle(kv.second);
   cudaFree(c->sig_local);
   cudaFree(c->err);
+  cudaFree(c->trace);
   delete c;
   return AR_OK;
 }
@@ -1063,6 +1078,43 @@ int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
   if (!c || !kernels) { set_error("null argument"); return AR_EINVAL; }
   *kernels = c->last_launches;
   return AR_OK;
+}
+
+int ar_comm_set_trace(ar_comm *c, int32_t enable) {
+  SYS_TRY({
+    if (!c) throw InvalidArg("null comm");
+    CUDA_OK(cudaSetDevice(c->device));
+    if (c->trace) {
+      CUDA_OK(cudaDeviceSynchronize());
+      cudaFree(c->trace);
+      c->trace = nullptr;
+      c->trace_elems = 0;
+    }
+    if (enable) {
+      c->trace_elems = (size_t)(c->local ? c->world : 1) * c->cta_cap * kTraceSlots;
+      CUDA_OK(cudaMalloc(&c->trace, c->trace_elems * sizeof(unsigned long long)));
+      CUDA_OK(cudaMemset(c->trace, 0, c->trace_elems * sizeof(unsigned long long)));
+    }
+    c->fast_valid = false;
+    return AR_OK;
+  })
+}
+
+int ar_comm_read_trace(ar_comm *c, uint64_t *out, size_t cap, size_t *n, int32_t *slots_per_cta,
+                       int32_t *ctas_per_rank) {
+  SYS_TRY({
+    if (!c || !out) throw InvalidArg("null argument");
+    if (!c->trace) throw InvalidArg("tracing is off (ar_comm_set_trace)");
+    const size_t used = (size_t)(c->local ? c->world : 1) * c->cta_cap * kTraceSlots;
+    if (n) *n = used;
+    if (slots_per_cta) *slots_per_cta = kTraceSlots;
+    if (ctas_per_rank) *ctas_per_rank = c->cta_cap;
+    if (cap < used) throw InvalidArg("buffer too small");
+    CUDA_OK(cudaSetDevice(c->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaMemcpy(out, c->trace, used * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return AR_OK;
+  })
 }
 
 int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed) {
@@ -1184,6 +1236,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.cta_cap = c->cta_cap;
   a.esize = plan->esize;
   a.bulk = c->bulk ? 1 : 0;
+  a.trace = c->trace;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;

@@ -68,6 +68,54 @@ def emu(args):
         del buf
 
 
+def trace(args):
+    """Per-phase in-kernel timing (globaltimer) of one call, emulated ranks."""
+    import numpy as np
+    world, count, dtype = args.ranks, args.count, args.dtype
+    plan = G.Plan.single_switch(world, count, dtype, G.params(3e-6, 1 / 900e9, 0.0, 1 / 6.54e12, 0.0, 9),
+                                args.force)
+    comm = G.Comm.local(world, 0)
+    if args.ctas[0]:
+        comm.set_ctas(args.ctas[0])
+    stride = G.rank_stride_bytes(count, dtype)
+    buf = torch.empty(world * stride, dtype=torch.uint8, device="cuda")
+    ex = G.Executor(plan, comm, buf)
+    for _ in range(5):
+        ex()
+    comm.set_trace(True)
+    ex = G.Executor(plan, comm, buf)
+    ex()
+    tr = comm.read_trace().astype(np.int64)
+    low = plan.lowering()
+    nst = len(low["ranks"][0]["steps"])
+    t0 = tr[:, :, 0].min()
+    rows = []
+    ctas = args.ctas[0] or tr.shape[1]
+    for si in range(nst):
+        w, o, n = (tr[:, :ctas, 1 + 3 * si] - t0, tr[:, :ctas, 2 + 3 * si] - t0, tr[:, :ctas, 3 + 3 * si] - t0)
+        rows.append({"step": si, "slot": low["ranks"][0]["steps"][si]["slot"],
+                     "wait_done_us": [float(np.median(w)) / 1e3, float(w.max()) / 1e3],
+                     "ops_done_us": [float(np.median(o)) / 1e3, float(o.max()) / 1e3],
+                     "notify_done_us": [float(np.median(n)) / 1e3, float(n.max()) / 1e3]})
+    end = tr[:, :ctas, -1] - t0
+    start = tr[:, :ctas, 0] - t0
+    print(json.dumps({"probe": "trace", "plan": plan.report()[-1]["chosen"], "ranks": world, "count": count,
+                      "start_spread_us": float(start.max()) / 1e3, "end_us": [float(np.median(end)) / 1e3,
+                                                                             float(end.max()) / 1e3],
+                      "steps": rows}), flush=True)
+    # host cost of one call (no sync)
+    import time
+    comm.set_trace(False)
+    ex = G.Executor(plan, comm, buf)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(200):
+        ex()
+    host = (time.perf_counter() - t) / 200
+    torch.cuda.synchronize()
+    print(json.dumps({"probe": "host_call_us", "us": host * 1e6}), flush=True)
+
+
 def copy(args):
     n = 1 << 30
     a = torch.empty(n, dtype=torch.bfloat16, device="cuda")
@@ -88,4 +136,4 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     torch.cuda.set_device(0)
-    {"fanin": fanin, "emu": emu, "copy": copy}[a.what](a)
+    {"fanin": fanin, "emu": emu, "copy": copy, "trace": trace}[a.what](a)
