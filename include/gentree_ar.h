@@ -118,6 +118,13 @@ int gt_plan_info(const gt_plan *plan, int32_t *n_ranks, int32_t *n_steps, uint64
 int genmodel_predict(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
 void gt_plan_free(gt_plan *plan);
 
+/* GenModel of the plan as the B200 executor runs it (reading A6x): the same
+ * per-step formula applied to the lowered steps — after the last RS level is fused
+ * with the first AG level — with one α per flag round (entry + one per executed step) and
+ * B = max over ranks of max(bytes in, bytes out) per step, since NVLink is full duplex and a
+ * fused step moves RS and AG traffic at the same time.  `params` is required (uniform). */
+int genmodel_predict_executed(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
+
 /* ------------------------------------------------------------------ communicator */
 
 typedef struct ar_comm ar_comm; /* opaque; one per process and device; single-threaded */

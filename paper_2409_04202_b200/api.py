@@ -117,6 +117,12 @@ class Plan:
                                    ctypes.byref(out)))
         return out.as_dict()
 
+    def predict_executed(self, params: GmParams) -> dict:
+        """GenModel of the lowered (fused, full-duplex) step structure the executor runs."""
+        out = GmBreakdown()
+        check(lib.genmodel_predict_executed(self._h, ctypes.byref(params), ctypes.byref(out)))
+        return out.as_dict()
+
     @property
     def handle(self):
         return self._h

@@ -1105,6 +1105,75 @@ int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
   return AR_OK;
 }
 
+int genmodel_predict_executed(const gt_plan *plan, const gm_params *params, gm_breakdown *out) {
+  SYS_TRY({
+    if (!plan || !params || !out) throw InvalidArg("null argument");
+    std::vector<DevStep> st;
+    std::vector<DevOp> ops;
+    std::vector<DevWait> w;
+    std::vector<int> rk, pb, pl;
+    const int n = plan->plan.n;
+    lower_plan(plan->plan, n, st, ops, w, rk, pb, pl);
+    const int64_t es = plan->esize;
+    // per executed slot: in/out bytes per rank (full duplex), reduce work, distinct peers
+    std::map<int, std::vector<int64_t>> in, outb, cc, dd;
+    std::map<int, std::vector<std::set<int>>> peers;
+    for (int r = 0; r < n; r++)
+      for (int i = 0; i < pl[r]; i++) {
+        const DevStep &d = st[pb[r] + i];
+        if (d.op_count == 0) continue;
+        const int s = d.slot;
+        if (!in.count(s)) {
+          in[s].assign(n, 0); outb[s].assign(n, 0); cc[s].assign(n, 0); dd[s].assign(n, 0);
+          peers[s].assign(n, std::set<int>());
+        }
+        for (int k = 0; k < d.op_count; k++) {
+          const DevOp &x = ops[d.op_begin + k];
+          const int64_t L = x.len * es;
+          for (int j = 0; j < x.nsrc; j++) {
+            const int q = rk[x.src_begin + j];
+            if (q == r) continue;
+            in[s][r] += L;
+            outb[s][q] += L;
+            peers[s][r].insert(q);
+          }
+          for (int j = 0; j < x.ndst; j++) {
+            const int q = rk[x.dst_begin + j];
+            if (q == r) continue;
+            outb[s][r] += L;
+            in[s][q] += L;
+            peers[s][q].insert(r);
+          }
+          if (x.nsrc >= 2) {
+            cc[s][r] += (x.nsrc - 1) * L;
+            dd[s][r] += (x.nsrc + 1) * L;
+          }
+        }
+      }
+    std::vector<StepCoeffs> co;
+    co.push_back(StepCoeffs{1, 0, 0, 0, 1});   // the entry flag round (one alpha)
+    for (auto &kv : in) {
+      const int s = kv.first;
+      StepCoeffs c{1, 0, 0, 0, 1};
+      for (int r = 0; r < n; r++) {
+        c.B = std::max(c.B, std::max(in[s][r], outb[s][r]));
+        c.C = std::max(c.C, cc[s][r]);
+        c.D = std::max(c.D, dd[s][r]);
+        c.w = std::max(c.w, 1 + (int)peers[s][r].size());
+      }
+      co.push_back(c);
+    }
+    Params p;
+    p.alpha = params->alpha; p.beta = params->beta; p.gamma = params->gamma; p.delta = params->delta;
+    p.epsilon = params->epsilon; p.w_t = params->w_t; p.has_combined = params->has_combined != 0;
+    p.combined = params->combined;
+    Breakdown b = predict_f64(co, uniform_step_params(p, co.size()));
+    out->latency = b.latency; out->bandwidth = b.bandwidth; out->compute = b.compute;
+    out->memory = b.memory; out->incast = b.incast; out->total = b.total;
+    return AR_OK;
+  })
+}
+
 int ar_comm_set_trace(ar_comm *c, int32_t enable) {
   SYS_TRY({
     if (!c) throw InvalidArg("null comm");
