@@ -65,16 +65,32 @@ def load_peaks():
 NVLINK_PEAK_GBS = 770.0   # measured peer copy per direction (B200_PROFILING.md)
 
 
-def model_params():
-    """GenModel parameters (per byte) used to select the plan: the B200 fit committed under
-    profiles/ when present, else nominal B200 values."""
-    path = os.path.join(ROOT, "profiles", "genmodel_params.json")
+NOMINAL = {"alpha": 3e-6, "beta": 1 / 900e9, "gamma": 0.0, "delta": 1 / 6.54e12, "epsilon": 0.0, "w_t": 9}
+
+
+def fitted_params(emulated=False):
+    """B200 GenModel fit committed under profiles/ (tools/fit_report.py --install): NVLink
+    ranks (genmodel_params.json) or emulated ranks sharing one GPU's HBM."""
+    path = os.path.join(ROOT, "profiles", "genmodel_params_emulated.json" if emulated else "genmodel_params.json")
     if os.path.exists(path):
         with open(path) as f:
-            p = json.load(f)
-        return p, "fitted (profiles/genmodel_params.json)"
-    return {"alpha": 3e-6, "beta": 1 / 900e9, "gamma": 0.0, "delta": 1 / 6.54e12, "epsilon": 0.0,
-            "w_t": 9}, "nominal"
+            return json.load(f)
+    return None
+
+
+def model_params(world=None, emulated=False):
+    """GenModel parameters (per byte) used to select the plan.  The B200 fit is used only for
+    worlds it was fitted on (its incast threshold w_t and slope ε are not identifiable beyond
+    the largest measured n); otherwise nominal B200 values (α 3 µs,
+    β 1/900 GB/s, δ 1/6.54 TB/s, no incast below 9)."""
+    if emulated:
+        # emulated ranks share one GPU's HBM: the fitted per-rank model attributes that shared
+        # bandwidth to incast (genmodel_fit_emulated8_graph.json), so selection uses nominal
+        return dict(NOMINAL), "nominal (emulated ranks)"
+    p = fitted_params(emulated)
+    if p is not None and (world is None or world <= p.get("n_max_fit", 0)):
+        return p, "fitted (%s)" % p.get("source", "profiles")
+    return dict(NOMINAL), "nominal (fit covers n <= %s)" % (p.get("n_max_fit") if p else "-")
 
 
 def single_switch_doc(world, p):
@@ -171,7 +187,7 @@ def run_reference(args):
         return
     n = args.gpus
     world = args.ranks if n == 1 else n
-    p, _ = model_params()
+    p, _ = model_params(world, emulated=n == 1)
     es = 2 if args.dtype == "bf16" else 4
     count = int(args.cpu_sample_mib * MIB) // es
     for _ in range(min(args.warmup, 1)):
@@ -218,11 +234,14 @@ def main():
     nbytes = args.mib * MIB
     count = nbytes // es
     world = args.ranks if n == 1 else n
-    p, p_src = model_params()
-    gp = G.params(p["alpha"], p["beta"], p["gamma"], p["delta"], p["epsilon"], int(p["w_t"]))
+    p, p_src = model_params(world, emulated=n == 1)
     plan = G.Plan.from_topology(single_switch_doc(world, p), count, args.dtype, None, args.force)
     chosen = plan.report()[-1]["chosen"]
-    pred = plan.predict(gp)["total"]
+    # a6: GenModel prediction of the executed plan with the B200 fit of this machine kind
+    fp = fitted_params(emulated=n == 1) or NOMINAL
+    pred_src = ("fitted " + fp["source"]) if "source" in fp else "nominal"
+    gp = G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"], fp["epsilon"], int(fp["w_t"]))
+    pred = plan.predict_executed(gp)["total"]
     seed = 0x240904202 ^ 4
     stream = torch.cuda.current_stream()
 
@@ -374,7 +393,8 @@ def main():
         "gpu_launches_note": "one cooperative launch of ar_exec_kernel per step (per process)",
         "clocks": clk,
         "genmodel": {"predicted_ms": round(pred * 1e3, 4), "measured_ms": round(t_step * 1e3, 4),
-                     "pred_err": round(abs(pred - t_step) / t_step, 4), "params": p_src},
+                     "pred_err": round(abs(pred - t_step) / t_step, 4), "params": pred_src,
+                     "model": "per-step GenModel of the executed (fused, full-duplex) steps"},
         "busbw_per_step_min_median_max": [round(busbw(nbytes, world, max(per_step)), 2),
                                           round(busbw(nbytes, world, statistics.median(per_step)), 2),
                                           round(busbw(nbytes, world, min(per_step)), 2)],

@@ -54,6 +54,7 @@ def main():
     ap.add_argument("--min-bytes", type=int, default=1 << 20)
     ap.add_argument("--install", action="store_true", help="write profiles/genmodel_params.json")
     ap.add_argument("--fanin", default=None, help="harness fanin JSONL (C3-i, Eq. 6)")
+    ap.add_argument("--emulated", action="store_true", help="install as the emulated-ranks fit")
     a = ap.parse_args()
     eq6 = None
     if a.fanin:
@@ -112,9 +113,11 @@ def main():
         p = fit.as_dict()
         beta = p["combined"] / 2 if p["has_combined"] else p["beta"]
         gamma = 0.0 if p["has_combined"] else p["gamma"]
-        with open(os.path.join(ROOT, "profiles", "genmodel_params.json"), "w") as f:
+        name = "genmodel_params_emulated.json" if a.emulated else "genmodel_params.json"
+        with open(os.path.join(ROOT, "profiles", name), "w") as f:
             json.dump({"alpha": p["alpha"], "beta": beta, "gamma": gamma, "delta": p["delta"],
-                       "epsilon": p["epsilon"], "w_t": p["w_t"], "source": f"genmodel_fit_{a.tag}.json",
+                       "epsilon": p["epsilon"], "w_t": p["w_t"], "n_max_fit": nmax,
+                       "source": f"genmodel_fit_{a.tag}.json",
                        "note": "per byte; beta = (2beta+gamma)/2 and gamma = 0 when only the combined "
                                "term is identifiable (P:532)"}, f, indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "rows"}, indent=1))
