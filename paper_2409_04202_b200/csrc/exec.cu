@@ -75,6 +75,7 @@ struct ExecArgs {
   int bulk;                  // 1 = cp.async.bulk-staged body, 0 = register body
   unsigned long long *trace; // optional globaltimer stamps (kTraceSlots per CTA), nullptr = off
   int fence_mode;            // notify ordering: 0 membar.sys/thread, 1 release.sys, 2 fence+relaxed, 3 gpu scope
+  int store_tma;             // 1 = results leave through cp.async.bulk stores (body_bulk_st)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -240,8 +241,9 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
 // the stage.  kStages x kStageBytes of loads stay in flight per CTA without tying up
 // registers — the memory-level parallelism the NVLink round trip (~2 us) needs.
 constexpr int kStages = 4;
-constexpr int kStageBytes = 48 * 1024;
-constexpr int kDynSmem = kStages * kStageBytes;
+constexpr int kStageBytes = 40 * 1024;
+constexpr int kOutTile = kStageBytes / 2;                 // >= one source tile when NSRC >= 2
+constexpr int kDynSmem = kStages * kStageBytes + 2 * kOutTile;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
@@ -328,6 +330,107 @@ __device__ __noinline__ void body_bulk(const OpShared &s, size_t v0, size_t v1, 
   g += ntiles;
 }
 
+// Same pipeline, but the results go out through the bulk-copy engine as well: consumer warps
+// sum into a shared-memory output tile and one thread issues cp.async.bulk stores of it to
+// every destination (local and NVLink peers), so the SM issues 16-byte smem stores instead of
+// ndst global stores per vector.  Two output tiles alternate; a copy op (NSRC = 1) stores
+// straight from the input stage.  The stage's empty barrier has a single arrival (the storer).
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void consumer_bar(int nthr) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");
+}
+
+template <int NSRC, bool BF16>
+__device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
+                                          Pipe &pp) {
+  constexpr int T = (kStageBytes / NSRC) / 16 * 16;
+  constexpr int TV = T / 16;
+  const size_t nv = v1 - v0;
+  const uint32_t ntiles = (uint32_t)((nv + TV - 1) / TV);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (uint32_t i = 0; i < ntiles; i++) {
+        const uint32_t gi = g + i, st = gi % kStages, use = gi / kStages;
+        if (use > 0) mbar_wait(&pp.empty[st], (use - 1) & 1);
+        const size_t t0 = v0 + (size_t)i * TV;
+        const uint32_t bytes = (uint32_t)min((size_t)TV, v1 - t0) * 16;
+        mbar_expect_tx(&pp.full[st], bytes * NSRC);
+        uint8_t *base = smem + st * kStageBytes;
+#pragma unroll
+        for (int k = 0; k < NSRC; k++) bulk_g2s(base + k * T, s.src[k] + t0, bytes, &pp.full[st]);
+      }
+    }
+  } else {
+    const int ndst = s.ndst;
+    const int nthr = blockDim.x - 32;
+    const bool storer = threadIdx.x == 32;
+    uint4 *outb = (uint4 *)(smem + kStages * kStageBytes);   // 2 x kOutTile bytes
+    for (uint32_t i = 0; i < ntiles; i++) {
+      const uint32_t gi = g + i, st = gi % kStages, use = gi / kStages;
+      mbar_wait(&pp.full[st], use & 1);
+      const size_t t0 = v0 + (size_t)i * TV;
+      const int nvt = (int)min((size_t)TV, v1 - t0);
+      const uint4 *base = (const uint4 *)(smem + st * kStageBytes);
+      const void *src_tile = base;
+      if (NSRC > 1) {
+        uint4 *o = outb + (gi & 1) * (kOutTile / 16);
+        consumer_bar(nthr);     // the storer has drained reads of this output tile (tile i-2)
+        for (int v = threadIdx.x - 32; v < nvt; v += nthr) {
+          uint4 x[NSRC];
+#pragma unroll
+          for (int k = 0; k < NSRC; k++) x[k] = base[k * TV + v];
+          float acc[8];
+          acc_first<BF16>(acc, x[0]);
+#pragma unroll
+          for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[k]);
+          o[v] = acc_pack<BF16>(acc);
+        }
+        consumer_bar(nthr);     // output tile complete, input stage fully read
+        src_tile = o;
+        if (storer) mbar_arrive(&pp.empty[st]);
+      }
+      if (storer) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int d = 0; d < ndst; d++) bulk_s2g(s.dst[d] + t0, src_tile, (uint32_t)nvt * 16);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (NSRC == 1) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&pp.empty[st]);
+        } else {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        }
+      }
+    }
+    if (storer) {
+      // the writes must be complete before this CTA releases its flags
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+  }
+  g += ntiles;
+}
+
+template <bool BF16>
+__device__ void body_dispatch_bulk_st(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
+                                      Pipe &pp) {
+  switch (s.nsrc) {
+    case 1: body_bulk_st<1, BF16>(s, v0, v1, g, smem, pp); break;
+    case 2: body_bulk_st<2, BF16>(s, v0, v1, g, smem, pp); break;
+    case 3: body_bulk_st<3, BF16>(s, v0, v1, g, smem, pp); break;
+    case 4: body_bulk_st<4, BF16>(s, v0, v1, g, smem, pp); break;
+    case 5: body_bulk_st<5, BF16>(s, v0, v1, g, smem, pp); break;
+    case 6: body_bulk_st<6, BF16>(s, v0, v1, g, smem, pp); break;
+    case 7: body_bulk_st<7, BF16>(s, v0, v1, g, smem, pp); break;
+    case 8: body_bulk_st<8, BF16>(s, v0, v1, g, smem, pp); break;
+    default: body_generic<BF16>(s, v0, v1); break;
+  }
+}
+
 template <bool BF16>
 __device__ void body_dispatch_bulk(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem, Pipe &pp) {
   switch (s.nsrc) {
@@ -409,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   if (a.bulk && threadIdx.x == 0) {
     for (int s = 0; s < kStages; s++) {
       mbar_init(&pp.full[s], 1);
-      mbar_init(&pp.empty[s], blockDim.x / 32 - 1);
+      mbar_init(&pp.empty[s], a.store_tma ? 1 : blockDim.x / 32 - 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -459,8 +562,13 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       const long long nv = ve - vb;
       const size_t v0 = (size_t)(vb + nv * cta / nctas), v1 = (size_t)(vb + nv * (cta + 1) / nctas);
       if (a.bulk) {
-        if (bf16) body_dispatch_bulk<true>(sh, v0, v1, g, dyn_smem, pp);
-        else body_dispatch_bulk<false>(sh, v0, v1, g, dyn_smem, pp);
+        if (a.store_tma) {
+          if (bf16) body_dispatch_bulk_st<true>(sh, v0, v1, g, dyn_smem, pp);
+          else body_dispatch_bulk_st<false>(sh, v0, v1, g, dyn_smem, pp);
+        } else {
+          if (bf16) body_dispatch_bulk<true>(sh, v0, v1, g, dyn_smem, pp);
+          else body_dispatch_bulk<false>(sh, v0, v1, g, dyn_smem, pp);
+        }
       } else {
         if (bf16) body_dispatch<true>(sh, v0, v1);
         else body_dispatch<false>(sh, v0, v1);
@@ -629,6 +737,7 @@ struct ar_comm {
   int fast_nctas = -1;
   ExecArgs fast_args{};
   int fence_mode = -1;                         // -1 = default (see ExecArgs::fence_mode); AR_FENCE_MODE
+  bool store_tma = false;                      // AR_EXEC_STORE=tma: bulk-copy stores of results
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
 };
@@ -924,6 +1033,7 @@ static void init_comm(ar_comm *c) {
   if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) c->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
   if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
   if (const char *f = std::getenv("AR_FENCE_MODE")) c->fence_mode = std::atoi(f);
+  if (const char *st = std::getenv("AR_EXEC_STORE")) c->store_tma = std::string(st) == "tma";
 }
 
 }  // namespace
@@ -1332,6 +1442,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.bulk = c->bulk ? 1 : 0;
   a.trace = c->trace;
   a.fence_mode = c->fence_mode >= 0 ? c->fence_mode : (c->local ? 3 : 1);
+  a.store_tma = c->store_tma ? 1 : 0;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;
