@@ -199,9 +199,13 @@ int ar_comm_read_trace(ar_comm *comm, uint64_t *out, size_t cap, size_t *n, int3
 /* Inspection (host only, no GPU needed): the per-rank device step tables allreduce_exec
  * runs for `plan` — after op merging, RS/AG fusion and the dependency analysis — as JSON
  * {"ranks":[{"steps":[{"slot":s,"ops":[{"off","len","src":[..],"dst":[..]}],
- * "waits":[[rank,slot,paired],..],"notify":[..]}]}]}.  Slot 0 = entry; slot s+1 = after
- * plan step s; the last step of each rank (exit) has only paired waits.  Same buffer
- * protocol as gt_plan_to_json (the size query itself returns AR_EINVAL with *needed set). */
+ * "waits":[[rank,slot,kind,p_off,p_len,c_off,c_len],..],"notify":[..]}]}]}.  Slot 0 = entry;
+ * slot s+1 = after plan step s; the last step of each rank (exit) has only paired waits.
+ * kind 0 = paired (the producer's CTA with my index), 1 = every producer CTA, 2 = range: the
+ * producer CTAs whose slice of op [p_off, p_off+p_len) intersects my slice of the consumer op
+ * [c_off, c_off+c_len) (elements; slices: whole 16-byte vectors split evenly over the CTAs, CTA
+ * 0 adds the unaligned head, the last CTA the tail).  Same buffer protocol as gt_plan_to_json
+ * (the size query itself returns AR_EINVAL with *needed set). */
 int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed);
 
 /* ------------------------------------------------------------------ inputs and harness */

@@ -55,8 +55,13 @@ struct DevStep {
   int notify_begin, notify_count;
   int pad;
 };
+constexpr int kWaitPaired = 0;   // wait for the producer's same-index CTA
+constexpr int kWaitFull = 1;     // wait for every producer CTA
+constexpr int kWaitRange = 2;    // wait for the producer CTAs whose slice of [p_off, p_len) meets ours of [c_off, c_len)
 struct DevWait {
-  int rank, slot, paired, pad;
+  int rank, slot, kind, pad;
+  long long p_off, p_len;    // producer op range (elements)
+  long long c_off, c_len;    // consumer op range (elements)
 };
 struct ExecArgs {
   const DevStep *steps;
@@ -482,6 +487,25 @@ __device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, 
   }
 }
 
+// Elements [e0, e1) of op [off, off+len) handled by CTA k of C: whole 16-byte vectors are split
+// evenly and contiguously; CTA 0 also takes the unaligned head and CTA C-1 the tail (if the
+// op has no whole vector, CTA 0 takes everything).  The ops loop below uses the same rule.
+__device__ __forceinline__ void cta_elems(long long off, long long len, int esize, int k, int C, long long &e0,
+                                          long long &e1) {
+  const long long E = 16 / esize;
+  const long long vb = (off * esize + 15) / 16, ve = (off + len) * esize / 16;
+  if (vb >= ve) {
+    e0 = k == 0 ? off : 0;
+    e1 = k == 0 ? off + len : 0;
+    return;
+  }
+  const long long nv = ve - vb;
+  e0 = (vb + nv * k / C) * E;
+  e1 = (vb + nv * (k + 1) / C) * E;
+  if (k == 0) e0 = off;
+  if (k == C - 1) e1 = off + len;
+}
+
 __device__ __forceinline__ unsigned long long *flag_ptr(const ExecArgs &a, int page_rank, int slot, int producer,
                                                         int cta) {
   return a.sigs[page_rank] + ((size_t)(slot * a.world + producer) * a.cta_cap + cta);
@@ -523,11 +547,17 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
     const DevStep st = prog[si];
     // ---- waits (a1 / a3 / a5)
     if (st.wait_count > 0) {
-      const int tot = st.wait_count * nctas;  // full waits use all CTAs; paired use one
+      const int tot = st.wait_count * nctas;  // (wait, producer CTA) pairs over the threads
       for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        const DevWait w = a.waits[st.wait_begin + i / nctas];
+        const DevWait &w = a.waits[st.wait_begin + i / nctas];
         const int c = i % nctas;
-        if (w.paired && c != cta) continue;
+        if (w.kind == kWaitPaired && c != cta) continue;
+        if (w.kind == kWaitRange) {
+          long long m0, m1, p0, p1;
+          cta_elems(w.c_off, w.c_len, a.esize, cta, nctas, m0, m1);
+          cta_elems(w.p_off, w.p_len, a.esize, c, nctas, p0, p1);
+          if (!(m0 < m1 && p0 < p1 && m0 < p1 && p0 < m1)) continue;
+        }
         const unsigned long long *f = flag_ptr(a, me, w.slot, w.rank, c);
         unsigned int spins = 0;
         while (ld_acquire_sys(f) < epoch) {
@@ -737,7 +767,7 @@ struct ar_comm {
   int fast_nctas = -1;
   ExecArgs fast_args{};
   int fence_mode = -1;                         // -1 = default (see ExecArgs::fence_mode); AR_FENCE_MODE
-  bool store_tma = false;                      // AR_EXEC_STORE=tma: bulk-copy stores of results
+  bool store_tma = true;                       // bulk-copy stores of results (AR_EXEC_STORE=regs: st.global)
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
 };
@@ -880,21 +910,24 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
         for (int q : o.src) acc[q].push_back({s, r, o.off, o.len, false});
         for (int q : o.dst) acc[q].push_back({s, r, o.off, o.len, true});
       }
-  // deps[r][s] : producer rank -> producer step (-1 = entry); exit deps separately
-  std::vector<std::vector<std::map<int, int>>> deps(n, std::vector<std::map<int, int>>(S));
+  // Waits of consumer (r, s): one entry per conflicting earlier producer op (rank t, step s',
+  // range) — a *range* wait: the consumer CTA polls only the producer CTAs whose slice of
+  // the producer op intersects its own slice of the consumer op (both sliced by the kernel's
+  // rule), so dependent steps pipeline CTA by CTA.  Entry waits (t's input ready) are paired.
+  using WaitKey = std::tuple<int, int, int, long long, long long, long long, long long>;
+  std::vector<std::vector<std::set<WaitKey>>> wl(n, std::vector<std::set<WaitKey>>(S));
   std::vector<std::map<int, int>> exitdeps(n);
   for (int s = 0; s < S; s++)
     for (int r = 0; r < n; r++)
       for (auto &o : H[s][r]) {
         auto visit = [&](int q, bool write) {
-          auto &d = deps[r][s];
-          if (q != r && !d.count(q)) d[q] = -1;           // entry of q
+          auto &d = wl[r][s];
+          if (q != r) d.insert(WaitKey{q, 0, kWaitPaired, 0, 0, 0, 0});   // entry of q
           for (const Access &x : acc[q]) {
             if (x.step >= s) continue;
             if (!write && !x.write) continue;
             if (!overlap(o.off, o.len, x.off, x.len)) continue;
-            auto it = d.find(x.rank);
-            if (it == d.end() || it->second < x.step) d[x.rank] = x.step;
+            d.insert(WaitKey{x.rank, x.step + 1, kWaitRange, x.off, x.len, o.off, o.len});
           }
         };
         for (int q : o.src) visit(q, false);
@@ -906,12 +939,11 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
       auto it = exitdeps[r].find(x.rank);
       if (it == exitdeps[r].end() || it->second < x.step) exitdeps[r][x.rank] = x.step;
     }
-  // notify lists: notify[t][s+1] = consumers of (t, s)
+  // notify lists: notify[t][slot] = consumers of t's step slot
   std::vector<std::vector<std::set<int>>> notify(n, std::vector<std::set<int>>(S + 1));
   for (int r = 0; r < n; r++) {
     for (int s = 0; s < S; s++)
-      for (auto &kv : deps[r][s])
-        if (!(kv.first == r && kv.second == -1)) notify[kv.first][kv.second + 1].insert(r);
+      for (auto &w : wl[r][s]) notify[std::get<0>(w)][std::get<1>(w)].insert(r);
     for (auto &kv : exitdeps[r]) notify[kv.first][kv.second + 1].insert(r);
   }
   // programs
@@ -919,7 +951,8 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
   prog_len.assign(world, 0);
   for (int r = 0; r < n; r++) {
     prog_begin[r] = (int)steps.size();
-    auto emit = [&](int slot, const std::vector<HostOp> *hops, const std::map<int, int> *dp, bool exit) {
+    auto emit = [&](int slot, const std::vector<HostOp> *hops, const std::set<WaitKey> *wk, const std::map<int, int> *dp,
+                    bool exit) {
       DevStep d{};
       d.slot = slot;
       d.op_begin = (int)ops.size();
@@ -938,13 +971,24 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
         }
       d.op_count = (int)ops.size() - d.op_begin;
       d.wait_begin = (int)waits.size();
+      if (wk)
+        for (auto &k : *wk) {
+          DevWait w{};
+          w.rank = std::get<0>(k);
+          w.slot = std::get<1>(k);
+          w.kind = std::get<2>(k);
+          w.p_off = std::get<3>(k);
+          w.p_len = std::get<4>(k);
+          w.c_off = std::get<5>(k);
+          w.c_len = std::get<6>(k);
+          waits.push_back(w);
+        }
       if (dp)
-        for (auto &kv : *dp) {
-          if (kv.first == r && kv.second == -1) continue;
+        for (auto &kv : *dp) {   // exit: paired waits on every remote accessor's last step
           DevWait w{};
           w.rank = kv.first;
           w.slot = kv.second + 1;
-          w.paired = (exit || kv.second == -1) ? 1 : 0;
+          w.kind = kWaitPaired;
           waits.push_back(w);
         }
       d.wait_count = (int)waits.size() - d.wait_begin;
@@ -954,12 +998,12 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
       d.notify_count = (int)ranks.size() - d.notify_begin;
       if (d.op_count || d.wait_count || d.notify_count) steps.push_back(d);
     };
-    emit(0, nullptr, nullptr, false);
+    emit(0, nullptr, nullptr, nullptr, false);
     for (int s = 0; s < S; s++) {
-      if (H[s][r].empty() && notify[r][s + 1].empty() && deps[r][s].empty()) continue;
-      emit(s + 1, &H[s][r], &deps[r][s], false);
+      if (H[s][r].empty() && notify[r][s + 1].empty() && wl[r][s].empty()) continue;
+      emit(s + 1, &H[s][r], &wl[r][s], nullptr, false);
     }
-    emit(0, nullptr, &exitdeps[r], true);
+    emit(0, nullptr, nullptr, &exitdeps[r], true);
     prog_len[r] = (int)steps.size() - prog_begin[r];
   }
 }
@@ -1033,7 +1077,7 @@ static void init_comm(ar_comm *c) {
   if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) c->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
   if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
   if (const char *f = std::getenv("AR_FENCE_MODE")) c->fence_mode = std::atoi(f);
-  if (const char *st = std::getenv("AR_EXEC_STORE")) c->store_tma = std::string(st) == "tma";
+  if (const char *st = std::getenv("AR_EXEC_STORE")) c->store_tma = std::string(st) != "regs";
 }
 
 }  // namespace
@@ -1349,7 +1393,8 @@ int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *ne
         for (int k = 0; k < d.wait_count; k++) {
           const DevWait &x = w[d.wait_begin + k];
           o += (k ? ",[" : "[") + std::to_string(x.rank) + "," + std::to_string(x.slot) + "," +
-               std::to_string(x.paired) + "]";
+               std::to_string(x.kind) + "," + std::to_string(x.p_off) + "," + std::to_string(x.p_len) + "," +
+               std::to_string(x.c_off) + "," + std::to_string(x.c_len) + "]";
         }
         o += "],\"notify\":[";
         for (int k = 0; k < d.notify_count; k++) o += (k ? "," : "") + std::to_string(rk[d.notify_begin + k]);

@@ -41,6 +41,6 @@ def test_two_process_plan_and_protocol_agreement(world_of_plan, tmp_path):
         assert allv[0]["low"] == allv[1]["low"]
         ranks = allv[0]["low"]["ranks"]
         notifies = {(r, s["slot"], c) for r, rk in enumerate(ranks) for s in rk["steps"] for c in s["notify"]}
-        waits = {(t, slot, r) for r, rk in enumerate(ranks) for s in rk["steps"] for (t, slot, _) in s["waits"]}
+        waits = {(t, slot, r) for r, rk in enumerate(ranks) for s in rk["steps"] for (t, slot, *_) in s["waits"]}
         assert waits <= notifies, waits - notifies
         assert notifies <= waits, notifies - waits

@@ -26,7 +26,23 @@ def single_switch(world):
                                {"gamma": 0.0, "delta": 4 / 6.54e12})
 
 
-def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random) -> list:
+def cta_elems(off, len_, esize, k, C):
+    """The kernel's slicing rule (exec.cu cta_elems): whole 16-byte vectors split evenly and
+    contiguously over C CTAs, CTA 0 adds the unaligned head, CTA C-1 the tail."""
+    E = 16 // esize
+    vb, ve = (off * esize + 15) // 16, (off + len_) * esize // 16
+    if vb >= ve:
+        return (off, off + len_) if k == 0 else (0, 0)
+    nv = ve - vb
+    e0, e1 = (vb + nv * k // C) * E, (vb + nv * (k + 1) // C) * E
+    if k == 0:
+        e0 = off
+    if k == C - 1:
+        e1 = off + len_
+    return e0, e1
+
+
+def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random, esize: int = 4) -> list:
     n = len(low["ranks"])
     bufs = [x.astype(np.float32).copy() for x in inputs]
     flags = {}                                  # (consumer, slot, producer, cta) -> epoch
@@ -44,8 +60,18 @@ def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random
                 return False
         st = prog[pc[r][c]]
         e = epoch[r][c]
-        for (t, slot, paired) in st["waits"]:
-            cs = [c] if paired else range(ctas)
+        for (t, slot, kind, p_off, p_len, c_off, c_len) in st["waits"]:
+            if kind == 0:
+                cs = [c]
+            elif kind == 1:
+                cs = range(ctas)
+            else:
+                m0, m1 = cta_elems(c_off, c_len, esize, c, ctas)
+                cs = []
+                for k in range(ctas):
+                    p0, p1 = cta_elems(p_off, p_len, esize, k, ctas)
+                    if m0 < m1 and p0 < p1 and m0 < p1 and p0 < m1:
+                        cs.append(k)
             if any(flags.get((r, slot, t, cc), 0) < e for cc in cs):
                 return False
         return True
@@ -53,8 +79,7 @@ def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random
     def step(r, c):
         st = low["ranks"][r]["steps"][pc[r][c]]
         for op in st["ops"]:
-            lo = op["off"] + op["len"] * c // ctas
-            hi = op["off"] + op["len"] * (c + 1) // ctas
+            lo, hi = cta_elems(op["off"], op["len"], esize, c, ctas)
             if hi <= lo:
                 continue
             acc = bufs[op["src"][0]][lo:hi].copy()
@@ -99,7 +124,7 @@ def test_lowered_protocol_random_schedules(doc, world, force):
     want = SM.simulate(oplan, SM.simulate(oplan, xs, "f32"), "f32")
     rnd = random.Random(world * 100 + len(force or ""))
     for trial in range(6):
-        got = interpret(low, xs, ctas=rnd.choice([1, 2, 3]), calls=2, rnd=rnd)
+        got = interpret(low, xs, ctas=rnd.choice([1, 2, 3, 5]), calls=2, rnd=rnd)
         for r in range(world):
             assert np.array_equal(got[r], want[r]), (force, trial, r)
 
@@ -115,7 +140,7 @@ def test_cps_is_one_fused_step_with_two_flag_rounds():
         assert sorted(entry["notify"]) == [q for q in range(8) if q != r]
         (op,) = work["ops"]
         assert op["src"] == list(range(8)) and sorted(op["dst"]) == list(range(8)) and op["dst"][0] == r
-        assert all(p == 1 for _, _, p in exit_["waits"]) and len(exit_["waits"]) == 7
+        assert all(w[2] == 0 for w in exit_["waits"]) and len(exit_["waits"]) == 7
 
 
 def test_lowering_rejects_bad_buffer_query():
