@@ -260,14 +260,28 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, uint32_t b
 __device__ __forceinline__ void mbar_arrive(unsigned long long *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// Bounded: a pipeline that never completes (a bug) must not hang the GPU — after ~20 s the
+// wait gives up and raises the device error word (reported by ar_comm_get_async_error).
+__device__ unsigned long long g_pipe_err = 0;
 __device__ __forceinline__ void mbar_wait(unsigned long long *b, uint32_t parity) {
   uint32_t ok = 0;
+  unsigned int spins = 0;
+  unsigned long long t0 = 0;
   while (!ok) {
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(ok)
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
+    if (!ok && (++spins & 4095u) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 20000000000ull) {
+        atomicExch(&g_pipe_err, 2ull);
+        return;
+      }
+    }
   }
 }
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32_t bytes, unsigned long long *bar) {
@@ -1235,6 +1249,13 @@ int ar_comm_get_async_error(ar_comm *c) {
     if (e) {
       CUDA_OK(cudaMemset(c->err, 0, sizeof e));
       throw SysError("flag wait timed out on the device (peer not progressing)");
+    }
+    unsigned long long pe = 0;
+    CUDA_OK(cudaMemcpyFromSymbol(&pe, g_pipe_err, sizeof pe));
+    if (pe) {
+      const unsigned long long z = 0;
+      CUDA_OK(cudaMemcpyToSymbol(g_pipe_err, &z, sizeof z));
+      throw SysError("bulk-copy pipeline wait timed out on the device (internal error)");
     }
     return AR_OK;
   })
