@@ -389,7 +389,10 @@ __device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v
     const int nthr = blockDim.x - 32;
     const bool storer = threadIdx.x == 32;
     uint4 *outb = (uint4 *)(smem + kStages * kStageBytes);   // 2 x kOutTile bytes
-    for (uint32_t i = 0; i < ntiles; i++) {
+    // A copy (NSRC = 1) is done by the storer alone: the other threads must not wait on the
+    // full barriers, since nothing would keep them within one phase of the storer (a thread
+    // that falls two phases behind sees the parity flip twice and waits forever).
+    for (uint32_t i = 0; i < ntiles && (NSRC > 1 || storer); i++) {
       const uint32_t gi = g + i, st = gi % kStages, use = gi / kStages;
       mbar_wait(&pp.full[st], use & 1);
       const size_t t0 = v0 + (size_t)i * TV;

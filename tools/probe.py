@@ -116,6 +116,47 @@ def trace(args):
     print(json.dumps({"probe": "host_call_us", "us": host * 1e6}), flush=True)
 
 
+def hunt(args):
+    """Repeat calls with tracing until one is slow; dump where that call waited."""
+    import time
+
+    import numpy as np
+    world, count, dtype = args.ranks, args.count, args.dtype
+    plan = G.Plan.single_switch(world, count, dtype, G.params(3e-6, 1 / 900e9, 0.0, 1 / 6.54e12, 0.0, 9),
+                                args.force)
+    comm = G.Comm.local(world, 0)
+    stride = G.rank_stride_bytes(count, dtype)
+    buf = torch.empty(world * stride, dtype=torch.uint8, device="cuda")
+    comm.set_trace(True)
+    ex = G.Executor(plan, comm, buf)
+    low = plan.lowering()
+    for it in range(args.reps):
+        t = time.perf_counter()
+        ex()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t
+        if dt > 0.05:
+            tr = comm.read_trace().astype(np.int64)
+            t0 = tr[:, :, 0].min()
+            nst = [len(rk["steps"]) for rk in low["ranks"]]
+            print(json.dumps({"probe": "hunt", "iter": it, "call_s": dt}), flush=True)
+            for r in range(world):
+                for c in range(tr.shape[1]):
+                    row = [(tr[r, c, 1 + 3 * i] - t0) / 1e3 for i in range(nst[r])]
+                    if max(row) > 10000:
+                        slow = int(np.argmax(np.array(row) > 10000))
+                        st = low["ranks"][r]["steps"][slow]
+                        print(json.dumps({"rank": r, "cta": c, "step": slow, "slot": st["slot"],
+                                          "waits": st["waits"], "wait_done_us": row}), flush=True)
+                        break
+            try:
+                comm.async_error()
+            except Exception as e:
+                print(json.dumps({"error": str(e)}))
+            return
+    print(json.dumps({"probe": "hunt", "iters": args.reps, "result": "no slow call"}))
+
+
 def copy(args):
     n = 1 << 30
     a = torch.empty(n, dtype=torch.bfloat16, device="cuda")
@@ -136,4 +177,4 @@ if __name__ == "__main__":
     ap.add_argument("--reps", type=int, default=10)
     a = ap.parse_args()
     torch.cuda.set_device(0)
-    {"fanin": fanin, "emu": emu, "copy": copy, "trace": trace}[a.what](a)
+    {"fanin": fanin, "emu": emu, "copy": copy, "trace": trace, "hunt": hunt}[a.what](a)
