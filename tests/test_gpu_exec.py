@@ -157,6 +157,34 @@ def test_repeated_calls_and_plan_interleave():
         assert_bits_equal(got[r], x[r], "f32", f"rank {r}")
 
 
+@pytest.mark.parametrize("force", ["ring", "rhd", "hcps:4,2", "rb", "cps"])
+def test_stress_back_to_back(force, monkeypatch):
+    """300 back-to-back calls (epoch progression, bulk-copy pipeline phases across ops and
+    calls) with a 2 s device wait bound: no wait may time out; then one more call checked
+    bit-exact.  Caught the copy-tile parity hang (SURVEY §4 "stress: back-to-back launches")."""
+    monkeypatch.setenv("AR_FLAG_TIMEOUT_MS", "2000")
+    world, count, dtype = 8, (1 << 22) + 5, "f32"
+    doc = single_switch(world)
+    plan = G.Plan.from_topology(doc, count, dtype, None, force)
+    comm = G.Comm.local(world, 0)
+    buf, stride = emulated_buffer(world, count, dtype, SEED, MODES["integer"])
+    ex = G.Executor(plan, comm, buf)
+    for _ in range(300):
+        ex()
+    torch.cuda.synchronize()
+    comm.async_error()
+    for r in range(world):
+        G.fill_synthetic(buf.data_ptr() + r * stride, count, dtype, SEED, r, 0)
+    ex()
+    torch.cuda.synchronize()
+    comm.async_error()
+    oplan, _ = GT.gentree(T.parse_topology(doc), count, 4, force=force)
+    want = SM.simulate(oplan, GEN.generate_all(SEED, world, count, dtype), dtype)
+    got = rank_views(buf, world, count, dtype, stride)
+    for r in (0, world - 1):
+        assert_bits_equal(got[r], want[r], dtype, f"rank {r}")
+
+
 @pytest.mark.parametrize("ctas", [1, 3, 17])
 def test_cta_counts(ctas):
     run_emulated(single_switch(8), 8, 123457, "bf16", force="hcps:4,2", ctas=ctas)
