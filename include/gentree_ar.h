@@ -118,6 +118,14 @@ int gt_plan_info(const gt_plan *plan, int32_t *n_ranks, int32_t *n_steps, uint64
 int genmodel_predict(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
 void gt_plan_free(gt_plan *plan);
 
+/* Build a plan from its canonical JSON (the gt_plan_to_json format): ranks, block
+ * indices and transfer sizes are validated and no op of a step may write a (rank, block)
+ * another op of the step reads or writes (AR_EINVAL otherwise).  *is_allreduce (optional)
+ * is set to 1 iff the plan also passes the AllReduce conservation check;
+ * data-movement plans that are not AllReduces (e.g. the x-to-x fan-in probe of P:418) are
+ * accepted and run by allreduce_exec all the same.  genmodel_predict needs explicit params. */
+int gt_plan_from_json(const char *plan_json, gt_plan **out, int32_t *is_allreduce);
+
 /* GenModel of the plan as the B200 executor runs it (reading A6x): the same
  * per-step formula applied to the lowered steps — after the last RS level is fused
  * with the first AG level — with one α per flag round (entry + one per executed step) and

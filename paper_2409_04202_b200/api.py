@@ -89,6 +89,15 @@ class Plan:
                                              force.encode() if force else None, ctypes.byref(h)))
         return cls(h)
 
+    @classmethod
+    def from_json(cls, plan_json: str) -> "Plan":
+        """Plan from canonical plan JSON (any data-movement plan; `.is_allreduce` tells)."""
+        h, flag = ctypes.c_void_p(), ctypes.c_int32()
+        check(lib.gt_plan_from_json(plan_json.encode(), ctypes.byref(h), ctypes.byref(flag)))
+        p = cls(h)
+        p.is_allreduce = bool(flag.value)
+        return p
+
     def _str(self, fn) -> str:
         need = ctypes.c_size_t()
         fn(self._h, None, 0, ctypes.byref(need))

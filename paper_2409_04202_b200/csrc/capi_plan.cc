@@ -219,4 +219,24 @@ int genmodel_predict(const gt_plan *plan, const gm_params *params, gm_breakdown 
 
 void gt_plan_free(gt_plan *plan) { delete plan; }
 
+int gt_plan_from_json(const char *plan_json, gt_plan **out, int32_t *is_allreduce) {
+  AR_TRY({
+    if (!plan_json || !out) throw InvalidArg("null argument");
+    std::string dtype;
+    bool ar = false;
+    Plan p = plan_from_json(plan_json, dtype, ar);
+    gt_plan *g = new gt_plan();
+    g->plan = std::move(p);
+    g->topo_params = false;
+    g->dtype = dtype == "f32" ? AR_F32 : AR_BF16;
+    g->esize = esize_of(g->dtype);
+    g->json = plan_to_json(g->plan, dtype.c_str());
+    g->report = "[]";
+    g->uid = next_plan_uid();
+    if (is_allreduce) *is_allreduce = ar ? 1 : 0;
+    *out = g;
+    return AR_OK;
+  })
+}
+
 }  // extern "C"

@@ -433,6 +433,76 @@ void verify_allreduce(const Plan &p) {
     }
 }
 
+Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce) {
+  Json doc;
+  try {
+    doc = JsonReader(text).parse();
+  } catch (const JsonError &e) {
+    throw InvalidArg(e.what());
+  }
+  auto num = [](const Json *v, const char *what) -> long long {
+    if (!v || v->kind != Json::Number || !v->is_integer) throw InvalidArg(std::string(what) + " must be an integer");
+    return v->ival;
+  };
+  if (doc.kind != Json::Object) throw InvalidArg("plan must be an object");
+  Plan p;
+  p.n = (int)num(doc.get("n"), "n");
+  p.count = num(doc.get("count"), "count");
+  const Json *dt = doc.get("dtype");
+  if (!dt || dt->kind != Json::String || (dt->str != "f32" && dt->str != "bf16")) throw InvalidArg("dtype must be f32|bf16");
+  dtype = dt->str;
+  if (p.n < 2 || p.n > 4096 || p.count < 1) throw InvalidArg("bad n/count");
+  const Json *steps = doc.get("steps");
+  if (!steps || steps->kind != Json::Array) throw InvalidArg("steps must be an array");
+  auto rank_ok = [&](long long r) {
+    if (r < 0 || r >= p.n) throw InvalidArg("rank out of range");
+    return (int)r;
+  };
+  for (const Json &sj : steps->arr) {
+    if (sj.kind != Json::Object) throw InvalidArg("step must be an object");
+    Step st;
+    const Json *ph = sj.get("phase");
+    if (!ph || ph->kind != Json::String || (ph->str != "rs" && ph->str != "ag")) throw InvalidArg("phase must be rs|ag");
+    st.ag = ph->str == "ag";
+    const Json *lb = sj.get("label");
+    st.label = lb && lb->kind == Json::String ? lb->str : "";
+    const Json *rds = sj.get("reduces");
+    if (rds && rds->kind == Json::Array)
+      for (const Json &rj : rds->arr) {
+        Reduce rd;
+        rd.server = rank_ok(num(rj.get("server"), "server"));
+        rd.block = rank_ok(num(rj.get("block"), "block"));
+        const Json *ins = rj.get("inputs");
+        if (!ins || ins->kind != Json::Array || ins->arr.empty()) throw InvalidArg("reduce needs inputs");
+        for (const Json &q : ins->arr) rd.inputs.push_back(rank_ok(num(&q, "input")));
+        st.reduces.push_back(rd);
+      }
+    const Json *trs = sj.get("transfers");
+    if (trs && trs->kind == Json::Array)
+      for (const Json &tj : trs->arr) {
+        Transfer t;
+        t.src = rank_ok(num(tj.get("src"), "src"));
+        t.dst = rank_ok(num(tj.get("dst"), "dst"));
+        t.block = rank_ok(num(tj.get("block"), "block"));
+        t.size = num(tj.get("size"), "size");
+        if (t.size != block_size(p.count, p.n, t.block)) throw InvalidArg("transfer size != block size");
+        if (t.src == t.dst) throw InvalidArg("transfer to itself");
+        st.transfers.push_back(t);
+      }
+    if (st.ag && !st.reduces.empty()) throw InvalidArg("ag steps carry no reduces");
+    if (!st.ag) add_implied_transfers(st, p.count, p.n);
+    p.steps.push_back(std::move(st));
+  }
+  try {
+    verify_allreduce(p);
+    allreduce = true;
+  } catch (const InvalidArg &e) {
+    if (std::string(e.what()).find("hazard") != std::string::npos) throw;
+    allreduce = false;
+  }
+  return p;
+}
+
 // ---------------------------------------------------------------- canonical JSON (O9)
 std::string plan_to_json(const Plan &p, const char *dtype) {
   std::string o = "{\"count\":" + std::to_string(p.count) + ",\"dtype\":";

@@ -108,6 +108,10 @@ struct PlanResult {
 PlanResult gentree(const Topology &t, int64_t count, int esize, const Params *explicit_params,
                    const std::string &force);
 Plan build_plan_natural(const std::string &kind, int n, int64_t count);   // standalone
+// Parse the canonical plan JSON (plan_to_json's format).  Checks structure, block indices
+// and sizes, and the within-step hazard rule; `allreduce` is set iff the plan also passes
+// verify_allreduce (data-movement probes need not).  Throws InvalidArg.
+Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce);
 void verify_allreduce(const Plan &p);                                      // throws InvalidArg
 std::string plan_to_json(const Plan &p, const char *dtype);
 std::string report_to_json(const std::vector<SwitchReport> &r);

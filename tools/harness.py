@@ -192,6 +192,58 @@ def multi(args):
     dist.destroy_process_group()
 
 
+def probe_plan(kind, n, count, dtype, x=None):
+    """Data-movement plans for the P2P probes (C3-ii) in canonical plan JSON.
+
+    pull: rank r copies block (r+k) mod n from rank (r+k) mod n, k = 1..n-1 (one step per k)
+    push: rank r copies its block r into rank (r+k) mod n
+    x-to-x (push among ranks 0..x-1 only): every receiver gets one block from each of the
+    x-1 others, i.e. fan-in x (the paper's full-mesh incast test)."""
+    m = x or n
+    steps = []
+    for k in range(1, m):
+        if kind == "pull":
+            red = [{"block": (r + k) % m, "fan_in": 1, "inputs": [(r + k) % m], "server": r} for r in range(m)]
+            steps.append({"label": f"pull{k}", "phase": "rs", "reduces": red, "transfers": []})
+        else:
+            es = 4 if dtype == "f32" else 2
+            size = lambda b: count // n + (1 if b < count % n else 0)
+            tr = [{"block": r, "dst": (r + k) % m, "size": size(r), "src": r} for r in range(m)]
+            steps.append({"label": f"push{k}", "phase": "ag", "reduces": [], "transfers": tr})
+    return json.dumps({"count": count, "dtype": dtype, "n": n, "steps": steps})
+
+
+def p2p(args):
+    """Pull vs push all-to-all bandwidth and the x-to-x fan-in test over NVLink."""
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = G.Comm.create(rank, world, local)
+    es = 4 if args.dtype == "f32" else 2
+    sizes = args.sizes or [1 << 26, 1 << 28, 1 << 30]
+    buf = torch.empty(max(sizes), dtype=torch.uint8, device="cuda")
+    timer = Timer(dist)
+    for nbytes in sizes:
+        count = nbytes // es
+        view = buf[:nbytes]
+        comm.register(view)
+        cases = [("pull", None), ("push", None)] + [("push", x) for x in range(2, world)]
+        for kind, x in cases:
+            plan = G.Plan.from_json(probe_plan(kind, world, count, args.dtype, x))
+            r = timer.run(lambda: G.Executor(plan, comm, view), 10, lambda: None, "graph")
+            m = x or world
+            per_dir = (m - 1) * (nbytes // world) / r["t_mean"] / 1e9
+            emit(rank, {"mode": "p2p", "kind": kind if x is None else f"x-to-x push (x={x})", "n": world,
+                        "x": m, "bytes": nbytes, **r, "gbs_per_direction_per_gpu": per_dir})
+    comm.async_error()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
 def emu(args):
     torch.cuda.set_device(0)
     es = 4 if args.dtype == "f32" else 2
@@ -244,7 +296,7 @@ def fanin(args):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin"])
+    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "p2p"])
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--plans", default="gentree;cps;ring;rhd;rb;hcps:2,2;hcps:4,2;hcps:2,4;hcps:2,2,2",
                     help="';'-separated plan kinds")
@@ -258,6 +310,8 @@ if __name__ == "__main__":
     a = ap.parse_args()
     if a.mode in ("sweep", "cps"):
         multi(a)
+    elif a.mode == "p2p":
+        p2p(a)
     elif a.mode == "fanin":
         fanin(a)
     else:
