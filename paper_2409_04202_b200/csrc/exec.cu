@@ -81,6 +81,7 @@ struct ExecArgs {
   unsigned long long *trace; // optional globaltimer stamps (kTraceSlots per CTA), nullptr = off
   int fence_mode;            // notify ordering: 0 membar.sys/thread, 1 release.sys, 2 fence+relaxed, 3 gpu scope
   int store_tma;             // 1 = results leave through cp.async.bulk stores (body_bulk_st)
+  int stages, stage_bytes;   // bulk-copy ring geometry
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -245,10 +246,12 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
 // in plan order from shared memory and store the result to every destination, then release
 // the stage.  kStages x kStageBytes of loads stay in flight per CTA without tying up
 // registers — the memory-level parallelism the NVLink round trip (~2 us) needs.
-constexpr int kStages = 4;
-constexpr int kStageBytes = 40 * 1024;
-constexpr int kOutTile = kStageBytes / 2;                 // >= one source tile when NSRC >= 2
-constexpr int kDynSmem = kStages * kStageBytes + 2 * kOutTile;
+constexpr int kMaxStages = 8;
+constexpr int kDefStages = 4;
+constexpr int kDefStageBytes = 40 * 1024;
+constexpr int kMaxDynSmem = 227 * 1024;
+// dynamic smem: stages x stage_bytes input ring + 2 output tiles of stage_bytes / 2
+inline int dyn_smem_bytes(int stages, int stage_bytes) { return (stages + 1) * stage_bytes; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long *b, uint32_t count) {
@@ -292,15 +295,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src, uint32
 }
 
 struct Pipe {
-  unsigned long long full[kStages];
-  unsigned long long empty[kStages];
+  unsigned long long full[kMaxStages];
+  unsigned long long empty[kMaxStages];
+  int stages, stage_bytes;   // runtime ring geometry (AR_STAGES, AR_STAGE_KB)
 };
 
 template <int NSRC, bool BF16>
 __device__ __noinline__ void body_bulk(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
                                        Pipe &pp) {
-  constexpr int T = (kStageBytes / NSRC) / 16 * 16;   // bytes per source per tile
-  constexpr int TV = T / 16;                           // 16-byte vectors per source per tile
+  const int kStages = pp.stages, kStageBytes = pp.stage_bytes;
+  const int T = (kStageBytes / NSRC) / 16 * 16;   // bytes per source per tile
+  const int TV = T / 16;                           // 16-byte vectors per source per tile
   const size_t nv = v1 - v0;
   const uint32_t ntiles = (uint32_t)((nv + TV - 1) / TV);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -366,8 +371,9 @@ __device__ __forceinline__ void consumer_bar(int nthr) {
 template <int NSRC, bool BF16>
 __device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
                                           Pipe &pp) {
-  constexpr int T = (kStageBytes / NSRC) / 16 * 16;
-  constexpr int TV = T / 16;
+  const int kStages = pp.stages, kStageBytes = pp.stage_bytes, kOutTile = pp.stage_bytes / 2;
+  const int T = (kStageBytes / NSRC) / 16 * 16;
+  const int TV = T / 16;
   const size_t nv = v1 - v0;
   const uint32_t ntiles = (uint32_t)((nv + TV - 1) / TV);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -551,7 +557,9 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
   if (a.bulk && threadIdx.x == 0) {
-    for (int s = 0; s < kStages; s++) {
+    pp.stages = a.stages;
+    pp.stage_bytes = a.stage_bytes;
+    for (int s = 0; s < a.stages; s++) {
       mbar_init(&pp.full[s], 1);
       mbar_init(&pp.empty[s], a.store_tma ? 1 : blockDim.x / 32 - 1);
     }
@@ -785,6 +793,7 @@ struct ar_comm {
   ExecArgs fast_args{};
   int fence_mode = -1;                         // -1 = default (see ExecArgs::fence_mode); AR_FENCE_MODE
   bool store_tma = true;                       // bulk-copy stores of results (AR_EXEC_STORE=regs: st.global)
+  int stages = kDefStages, stage_bytes = kDefStageBytes;   // AR_STAGES, AR_STAGE_KB
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
 };
@@ -1046,8 +1055,8 @@ static void free_lowered(Lowered &L) {
 static int resident_ctas(int device) {
   int nsm = 0, per = 0;
   CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-  CUDA_OK(cudaFuncSetAttribute(ar_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDynSmem));
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, kDynSmem));
+  CUDA_OK(cudaFuncSetAttribute(ar_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, kMaxDynSmem));
   return nsm * std::max(per, 1);
 }
 
@@ -1095,6 +1104,9 @@ static void init_comm(ar_comm *c) {
   if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
   if (const char *f = std::getenv("AR_FENCE_MODE")) c->fence_mode = std::atoi(f);
   if (const char *st = std::getenv("AR_EXEC_STORE")) c->store_tma = std::string(st) != "regs";
+  if (const char *v = std::getenv("AR_STAGES")) c->stages = std::max(2, std::min(kMaxStages, std::atoi(v)));
+  if (const char *v = std::getenv("AR_STAGE_KB")) c->stage_bytes = std::max(4, std::atoi(v)) * 1024;
+  while (dyn_smem_bytes(c->stages, c->stage_bytes) > kMaxDynSmem) c->stage_bytes -= 1024;
 }
 
 }  // namespace
@@ -1448,7 +1460,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     ++c->epoch;
     void *args[] = {&c->fast_args};
     CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
-                                        c->bulk ? kDynSmem : 0, (cudaStream_t)stream));
+                                        c->bulk ? dyn_smem_bytes(c->stages, c->stage_bytes) : 0, (cudaStream_t)stream));
     c->last_launches = 1;
     return AR_OK;
   }
@@ -1512,6 +1524,8 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.trace = c->trace;
   a.fence_mode = c->fence_mode >= 0 ? c->fence_mode : (c->local ? 3 : 1);
   a.store_tma = c->store_tma ? 1 : 0;
+  a.stages = c->stages;
+  a.stage_bytes = c->stage_bytes;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;
@@ -1519,7 +1533,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   c->fast_valid = true;
   void *args[] = {&a};
   CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
-                                      c->bulk ? kDynSmem : 0, (cudaStream_t)stream));
+                                      c->bulk ? dyn_smem_bytes(c->stages, c->stage_bytes) : 0, (cudaStream_t)stream));
   c->last_launches = 1;
   return AR_OK;
 }

@@ -55,6 +55,8 @@ def main():
     ap.add_argument("--install", action="store_true", help="write profiles/genmodel_params.json")
     ap.add_argument("--fanin", default=None, help="harness fanin JSONL (C3-i, Eq. 6)")
     ap.add_argument("--emulated", action="store_true", help="install as the emulated-ranks fit")
+    ap.add_argument("--wt-min", type=int, default=0, help="incast threshold lower bound (x-to-x probe)")
+    ap.add_argument("--wt-max", type=int, default=0)
     a = ap.parse_args()
     eq6 = None
     if a.fanin:
@@ -71,7 +73,11 @@ def main():
     cps = [r for r in load(a.cps, a.timing) if r["plan"] == "cps"]
     rows = [(r["n"], r["bytes"], r["t_mean"]) for r in cps]
     nmax = max(n for n, _, _ in rows)
-    fit, sse = G.genmodel_fit(rows, 2, max(2, nmax))
+    # w_t: from the x-to-x fan-in test when given ("no incast for 2 <= x <= w_t"),
+    # else scanned by the fit
+    wt_lo = a.wt_min or 2
+    wt_hi = max(wt_lo, a.wt_max or max(2, nmax))
+    fit, sse = G.genmodel_fit(rows, wt_lo, wt_hi)
     # (alpha, beta, gamma) model: least squares on [2, (n-1)s/n] only (delta = eps = 0)
     A = np.array([[2.0, (n - 1) * s / n] for n, s, _ in rows])
     t = np.array([x for _, _, x in rows])
