@@ -82,6 +82,7 @@ struct ExecArgs {
   int fence_mode;            // notify ordering: 0 membar.sys/thread, 1 release.sys, 2 fence+relaxed, 3 gpu scope
   int store_tma;             // 1 = results leave through cp.async.bulk stores (body_bulk_st)
   int stages, stage_bytes;   // bulk-copy ring geometry
+  unsigned int jitter_ns;    // stress mode: random delay before each notify (AR_JITTER_NS), 0 = off
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -634,6 +635,15 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
     AR_TRACE(2 + 3 * si);
     // ---- notify (release our slot on every consumer's page)
     if (st.notify_count > 0) {
+      if (a.jitter_ns && threadIdx.x == 0) {
+        // stress mode: delay this CTA's flags by a pseudo-random amount (ordering bugs surface
+        // as wrong results instead of hiding behind typical timing)
+        unsigned int h = (unsigned int)(cta * 2654435761u) ^ (unsigned int)(si * 40503u) ^
+                         (unsigned int)(me * 97u) ^ (unsigned int)epoch;
+        h ^= h >> 13;
+        h *= 0x5bd1e995u;
+        __nanosleep(h % a.jitter_ns);
+      }
       // Every thread's data stores of this step happen-before the barrier; the release
       // store(s) after it are cumulative over them (PTX memory model: bar.sync synchronises
       // the CTA, st.release is a release pattern).  fence_mode 0 additionally fences every
@@ -794,6 +804,7 @@ struct ar_comm {
   int fence_mode = -1;                         // -1 = default (see ExecArgs::fence_mode); AR_FENCE_MODE
   bool store_tma = true;                       // bulk-copy stores of results (AR_EXEC_STORE=regs: st.global)
   int stages = kDefStages, stage_bytes = kDefStageBytes;   // AR_STAGES, AR_STAGE_KB
+  unsigned int jitter_ns = 0;                  // AR_JITTER_NS (stress testing)
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
 };
@@ -1107,6 +1118,7 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_STAGES")) c->stages = std::max(2, std::min(kMaxStages, std::atoi(v)));
   if (const char *v = std::getenv("AR_STAGE_KB")) c->stage_bytes = std::max(4, std::atoi(v)) * 1024;
   while (dyn_smem_bytes(c->stages, c->stage_bytes) > kMaxDynSmem) c->stage_bytes -= 1024;
+  if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
 }
 
 }  // namespace
@@ -1526,6 +1538,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.store_tma = c->store_tma ? 1 : 0;
   a.stages = c->stages;
   a.stage_bytes = c->stage_bytes;
+  a.jitter_ns = c->jitter_ns;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;

@@ -185,6 +185,14 @@ def test_stress_back_to_back(force, monkeypatch):
         assert_bits_equal(got[r], want[r], dtype, f"rank {r}")
 
 
+@pytest.mark.parametrize("force", ["ring", "hcps:2,4", "rhd", None])
+def test_jitter_injection(force, monkeypatch):
+    """random delays (up to 20 us) before every flag post; any missing dependency
+    or ordering bug then shows up as a non-bit-exact result."""
+    monkeypatch.setenv("AR_JITTER_NS", "20000")
+    run_emulated(single_switch(8), 8, 300007, "bf16", force=force, calls=3)
+
+
 @pytest.mark.parametrize("ctas", [1, 3, 17])
 def test_cta_counts(ctas):
     run_emulated(single_switch(8), 8, 123457, "bf16", force="hcps:4,2", ctas=ctas)

@@ -23,11 +23,13 @@ def ngpus():
     return torch.cuda.device_count()
 
 
+@pytest.mark.parametrize("jitter", [0, 20000])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_multi_process_bit_exact(world):
+def test_multi_process_bit_exact(world, jitter):
+    """jitter > 0: random delays (ns) before every flag post on every GPU."""
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT)
+    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT, AR_JITTER_NS=str(jitter))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29617", os.path.join(ROOT, "tests", "mp_worker.py")]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
