@@ -250,7 +250,7 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
 constexpr int kMaxStages = 8;
 constexpr int kDefStages = 4;
 constexpr int kDefStageBytes = 40 * 1024;
-constexpr int kMaxDynSmem = 227 * 1024;
+constexpr int kMaxDynSmem = 224 * 1024;   // 227 KB per block minus the static shared state
 // dynamic smem: stages x stage_bytes input ring + 2 output tiles of stage_bytes / 2
 inline int dyn_smem_bytes(int stages, int stage_bytes) { return (stages + 1) * stage_bytes; }
 
