@@ -311,6 +311,15 @@ def main():
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": hbm_src}
+        # DRAM traffic per launch from the committed ncu --set full capture of this config
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                tr = json.load(f).get(f"emulated:r{world}:{args.dtype}:{nbytes}:{chosen}")
+            if tr and not args.ctas:
+                roof["traffic"] = tr["traffic_bytes_per_launch"]
+                roof["traffic_source"] = tr["source"]
+        except (OSError, ValueError):
+            pass
     else:
         wire = 2 * (n - 1) * nbytes / n          # Eq. 2: bytes per direction per GPU
         achieved = wire / kern_t / 1e9
