@@ -244,6 +244,50 @@ def p2p(args):
     dist.destroy_process_group()
 
 
+def mtrace(args):
+    """Per-phase in-kernel timeline of one call on N GPUs (rank 0's CTAs; globaltimer ns)."""
+    import numpy as np
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = G.Comm.create(rank, world, local)
+    es = 4 if args.dtype == "f32" else 2
+    for nbytes in args.sizes or [1 << 20]:
+        count = nbytes // es
+        buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        comm.register(buf)
+        for k in kinds_for(world, args.plans):
+            plan = G.Plan.from_topology(doc(world), count, args.dtype, None, None if k == "gentree" else k)
+            ex = G.Executor(plan, comm, buf)
+            for _ in range(5):
+                ex()
+            torch.cuda.synchronize()
+            comm.set_trace(True)
+            ex = G.Executor(plan, comm, buf)
+            dist.barrier()
+            ex()
+            tr = comm.read_trace().astype(np.int64)[0]
+            comm.set_trace(False)
+            nst = len(plan.lowering()["ranks"][rank]["steps"])
+            t0 = tr[:, 0].min()
+            C = comm_ctas = tr.shape[0]
+            used = [c for c in range(C) if tr[c, -1] > 0]
+            rows = []
+            for si in range(nst):
+                ph = [np.median([(tr[c, 1 + 3 * si + j] - t0) / 1e3 for c in used]) for j in range(3)]
+                rows.append([si] + [round(x, 2) for x in ph])
+            end = np.median([(tr[c, -1] - t0) / 1e3 for c in used])
+            emit(rank, {"mode": "mtrace", "plan": k, "n": world, "bytes": nbytes, "ctas": len(used),
+                        "steps_wait_ops_notify_us": rows, "end_us": round(float(end), 2)})
+    comm.async_error()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
 def emu(args):
     torch.cuda.set_device(0)
     es = 4 if args.dtype == "f32" else 2
@@ -296,7 +340,7 @@ def fanin(args):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "p2p"])
+    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "p2p", "mtrace"])
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--plans", default="gentree;cps;ring;rhd;rb;hcps:2,2;hcps:4,2;hcps:2,4;hcps:2,2,2",
                     help="';'-separated plan kinds")
@@ -310,6 +354,8 @@ if __name__ == "__main__":
     a = ap.parse_args()
     if a.mode in ("sweep", "cps"):
         multi(a)
+    elif a.mode == "mtrace":
+        mtrace(a)
     elif a.mode == "p2p":
         p2p(a)
     elif a.mode == "fanin":
