@@ -267,3 +267,12 @@ def test_errors_are_loud():
     mc = G.Comm.create(0, 2, 0)
     with pytest.raises(G.ArInvalid):
         G.allreduce_exec(G.Plan.from_topology(single_switch(2), 1000, "f32"), mc, buf)  # unregistered
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 2, 2), (2, 4, 2, 2)])
+def test_rearrangement_and_acps(shape):
+    """NEXT #3 rows on one GPU: a GenTree plan with data rearrangement (moves) and an
+    asymmetric CPS root, emulated ranks, bit-exact."""
+    from tests.topologies import cross_dc
+    world = shape[0] * shape[1] + shape[2] * shape[3]
+    run_emulated(cross_dc(*shape), world, 123457, "bf16")

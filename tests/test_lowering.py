@@ -109,6 +109,9 @@ def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random
 CASES = [(single_switch(w), w, k) for w in (2, 3, 4, 8) for k in (None, "cps", "ring", "rb")]
 CASES += [(single_switch(8), 8, k) for k in ("rhd", "hcps:4,2", "hcps:2,4", "hcps:2,2,2")]
 CASES += [(single_switch(6), 6, k) for k in ("hcps:3,2", "hcps:2,3")]
+from tests.topologies import cross_dc  # noqa: E402
+
+CASES += [(cross_dc(2, 2, 2, 2), 8, None), (cross_dc(2, 4, 2, 2), 12, None)]
 CASES += [(T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]), 4, None),
           (T.two_level_doc([3, 4], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]), 7, None),
           (T.two_level_doc([2, 2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]), 6, None)]

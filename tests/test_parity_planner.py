@@ -152,3 +152,13 @@ def test_fit_parity_noiseless():
         assert a == pytest.approx(b, rel=1e-9)
     lp2, _ = G.genmodel_fit(rows, 2, 8, link_bytes_per_s=900e9)
     assert lp2.beta == 1.0 / 900e9 and lp2.gamma == pytest.approx(truth[1] - 2 / 900e9, rel=1e-9)
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 2, 2), (2, 3, 2, 3), (2, 4, 2, 2)])
+def test_rearrangement_topologies(shape):
+    """Data rearrangement adopted + ACPS: library and oracle agree bit for bit."""
+    from tests.topologies import cross_dc
+    doc = cross_dc(*shape)
+    lp, op = check_topology(doc, 10 ** 6)
+    assert any(r["rearranged_children"] for r in lp.report())
+    assert any(len(r.inputs) == 1 for st in op.steps for r in st.reduces)   # moves present
