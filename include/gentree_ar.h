@@ -216,6 +216,33 @@ int ar_comm_read_trace(ar_comm *comm, uint64_t *out, size_t cap, size_t *n, int3
  * (the size query itself returns AR_EINVAL with *needed set). */
 int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed);
 
+/* ------------------------------------------------------------------ NVLS plan kind (NEXT #1) */
+
+/* In-switch reduction (NVLink SHARP) for a single NVSwitch domain: the Co-located-PS step
+ * with the fan-in-N reduce done by the switch (multimem.ld_reduce) and the broadcast
+ * by switch multicast (multimem.st) — ~S bytes per GPU and direction instead of 2(N−1)/N·S.
+ * The switch picks the summation order, so results are not bit-comparable to a plan-order
+ * oracle: they equal the exact sum on integer-valued inputs and are within the fp32/bf16
+ * accumulation bound otherwise.  Setup is collective, one process per GPU:
+ *   1. ar_nvls_create on every rank (rank 0 creates the multicast object of `bytes` + a flag
+ *      area and exports it as a POSIX fd) -> blob_out (AR_BLOB_BYTES);
+ *   2. gather the blobs (rank order), ar_nvls_attach on every rank (non-zero ranks import the
+ *      fd with pidfd_getfd; every rank adds its device), then a host barrier;
+ *   3. ar_nvls_bind on every rank (allocate, bind, map unicast + multicast) -> the unicast
+ *      device pointer of this rank's `bytes`-byte buffer (library-owned; freed by destroy),
+ *      then a host barrier before the first allreduce_exec_nvls.
+ * allreduce_exec_nvls: in-place SUM of the first `count` elements (count a multiple of
+ * world * 16 / element size), stream-ordered, graph-capturable.  Errors: AR_EINVAL for bad
+ * arguments, AR_ESYS for CUDA/driver failures (e.g. multicast unsupported). */
+typedef struct ar_nvls ar_nvls;
+int ar_nvls_create(int32_t rank, int32_t world, int32_t cuda_device, uint64_t bytes, ar_nvls **out,
+                   void *blob_out);
+int ar_nvls_attach(ar_nvls *nvls, const void *blobs);
+int ar_nvls_bind(ar_nvls *nvls, void **uc_ptr_out);
+int allreduce_exec_nvls(ar_nvls *nvls, uint64_t count, int32_t dtype, void *stream);
+int ar_nvls_get_async_error(ar_nvls *nvls);
+int ar_nvls_destroy(ar_nvls *nvls);
+
 /* ------------------------------------------------------------------ inputs and harness */
 
 /* Fill `count` elements at dptr with the seeded synthetic generator G(seed, rank, i),

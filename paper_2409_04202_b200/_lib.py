@@ -89,6 +89,12 @@ _SIGS = {
     "ar_comm_destroy": (I32, [P]),
     "ar_comm_last_launch_count": (I32, [P, ctypes.POINTER(I32)]),
     "ar_plan_lowering_json": (I32, [P, ctypes.c_char_p, SZ, ctypes.POINTER(SZ)]),
+    "ar_nvls_create": (I32, [I32, I32, I32, U64, ctypes.POINTER(P), ctypes.c_char_p]),
+    "ar_nvls_attach": (I32, [P, ctypes.c_char_p]),
+    "ar_nvls_bind": (I32, [P, ctypes.POINTER(P)]),
+    "allreduce_exec_nvls": (I32, [P, U64, I32, P]),
+    "ar_nvls_get_async_error": (I32, [P]),
+    "ar_nvls_destroy": (I32, [P]),
     "ar_comm_set_trace": (I32, [P, I32]),
     "ar_comm_read_trace": (I32, [P, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ), ctypes.POINTER(I32),
                                  ctypes.POINTER(I32)]),

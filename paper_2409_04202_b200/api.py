@@ -236,6 +236,55 @@ class Comm:
             pass
 
 
+class _CudaArray:
+    """__cuda_array_interface__ wrapper so torch can view library-owned device memory."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class Nvls:
+    """NVLS (in-switch reduction) buffer of `nbytes` per rank over torch.distributed (collective
+    construction; see include/gentree_ar.h "NVLS plan kind").  `.tensor` is this rank's buffer."""
+
+    def __init__(self, nbytes: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.device, self.nbytes = device, nbytes
+        h = ctypes.c_void_p()
+        blob = ctypes.create_string_buffer(L.AR_BLOB_BYTES)
+        check(lib.ar_nvls_create(self.rank, self.world, device, nbytes, ctypes.byref(h), blob))
+        self._h = h
+        blobs = [None] * self.world
+        dist.all_gather_object(blobs, blob.raw, group=group)
+        check(lib.ar_nvls_attach(self._h, b"".join(blobs)))
+        dist.barrier(group=group)
+        ptr = ctypes.c_void_p()
+        check(lib.ar_nvls_bind(self._h, ctypes.byref(ptr)))
+        dist.barrier(group=group)
+        self.ptr = ptr.value
+        self.tensor = torch.as_tensor(_CudaArray(self.ptr, nbytes), device=f"cuda:{device}")
+
+    def allreduce(self, count: int, dtype, stream=None):
+        check(lib.allreduce_exec_nvls(self._h, count, dtype_code(dtype), _stream(stream)))
+
+    def async_error(self):
+        check(lib.ar_nvls_get_async_error(self._h))
+
+    def destroy(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib.ar_nvls_destroy(h)
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
 def _stream(stream) -> int | None:
     if stream is None:
         try:

@@ -1,0 +1,64 @@
+"""Worker for the NVLS tests (torchrun, one process per GPU).  Integer-valued inputs must give
+the exact sum (any summation order is exact for them); gradient-shaped inputs must be within
+the north star's norm-wise bound of the float64 sum (1e-6 fp32, 1e-2 bf16; reading Q21), and
+every rank must hold identical bits (the switch multicasts one result)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2409_04202_b200 as G  # noqa: E402
+from oracle import simulate as SM  # noqa: E402
+from synth import generator as GEN  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    nbytes = 64 << 20
+    nv = G.Nvls(nbytes, local)
+    seed = GEN.config_seed(3)
+    failures = 0
+    for dtype in ("f32", "bf16"):
+        es = 4 if dtype == "f32" else 2
+        for count in (world * 16 // es, world * 4096, (nbytes // es) // (world * 8) * world * 8):
+            for mode, mid in (("integer", 1), ("gradient", 0)):
+                G.fill_synthetic(nv.ptr, count, dtype, seed, rank, mid)
+                torch.cuda.synchronize()
+                dist.barrier()
+                nv.allreduce(count, dtype)
+                torch.cuda.synchronize()
+                nv.async_error()
+                got = nv.tensor[: count * es].cpu().numpy().view(np.float32 if dtype == "f32" else np.uint16)
+                xs = GEN.generate_all(seed, world, count, dtype, mode)
+                ref = SM.exact_sum_f64(xs, dtype)
+                g64 = got.astype(np.float64) if dtype == "f32" else SM.bf16_bits_to_f32(got).astype(np.float64)
+                if mode == "integer":
+                    ok = np.array_equal(g64, ref)
+                else:
+                    err = SM.normwise_rel_err(got, ref, dtype)
+                    ok = err <= (1e-6 if dtype == "f32" else 1e-2)
+                allv = [None] * world
+                dist.all_gather_object(allv, got[:4096].tobytes())
+                same = all(a == allv[0] for a in allv)
+                if not (ok and same):
+                    print(f"rank {rank} FAIL {dtype} {mode} count={count} ok={ok} same={same}", flush=True)
+                    failures += 1
+    dist.barrier()
+    nv.destroy()
+    dist.destroy_process_group()
+    if rank == 0:
+        print(f"nvls_worker world={world}: {'OK' if failures == 0 else f'{failures} FAILURES'}", flush=True)
+    sys.exit(1 if failures else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -23,6 +23,20 @@ def ngpus():
     return torch.cuda.device_count()
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_nvls_in_switch_reduction(world):
+    """NEXT #1: NVLS plan kind (multimem.ld_reduce / multimem.st through the NVSwitch)."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29618", os.path.join(ROOT, "tests", "mp_nvls_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"nvls_worker world={world}: OK" in r.stdout
+
+
 @pytest.mark.parametrize("jitter", [0, 20000])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_multi_process_bit_exact(world, jitter):
