@@ -160,6 +160,7 @@ def multi(args):
     buf = torch.empty(max(sizes), dtype=torch.uint8, device="cuda")
     timer = Timer(dist)
     modes = args.timing.split(",")
+    nvls_buf = [None]
     for nbytes in sizes:
         count = nbytes // es
         view = buf[:nbytes]
@@ -170,6 +171,23 @@ def multi(args):
 
         plans = ["cps"] if args.mode == "cps" else kinds_for(world, args.plans)
         for k in plans:
+            if k == "nvls":     # in-switch reduction (NEXT #1), its own multicast-bound buffer
+                if nvls_buf[0] is None:
+                    nvls_buf[0] = G.Nvls(max(sizes), local)
+                nv = nvls_buf[0]
+
+                def nv_refill():
+                    G.fill_synthetic(nv.ptr, count, args.dtype, 11, rank, 0)
+
+                for mode in modes:
+                    r = timer.run(lambda: (lambda: nv.allreduce(count, args.dtype)), reps_for(nbytes), nv_refill,
+                                  mode)
+                    emit(rank, {"mode": args.mode, "impl": "ours", "plan": "nvls", "chosen": "nvls", "n": world,
+                                "bytes": nbytes, "dtype": args.dtype, **r,
+                                "busbw_med": busbw(nbytes, world, r["t_med"]),
+                                "busbw_mean": busbw(nbytes, world, r["t_mean"])})
+                nv.async_error()
+                continue
             plan = G.Plan.from_topology(doc(world), count, args.dtype, None, None if k == "gentree" else k)
             for mode in modes:
                 r = timer.run(lambda: G.Executor(plan, comm, view), reps_for(nbytes), refill, mode)
