@@ -279,6 +279,7 @@ int ar_nvls_create(int32_t rank, int32_t world, int32_t cuda_device, uint64_t by
     int nsm = 148;
     RT_CALL(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cuda_device));
     n->nctas = std::min(nsm, kNvCtaCap);
+    if (const char *v = std::getenv("AR_NVLS_CTAS")) n->nctas = std::max(1, std::min(kNvCtaCap, std::atoi(v)));
     if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) n->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
     *out = n;
     return AR_OK;
