@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-nvls", action="store_true")
     ap.add_argument("--cpu-sample-mib", type=float, default=64.0, help="oracle sample per rank (MiB)")
     return ap.parse_args()
 
@@ -328,6 +329,32 @@ def main():
                 "algorithmic_bytes_per_launch": int(wire),
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
 
+    # NVLS in-switch reduction (NEXT #1 plan kind, not a GenTree candidate), same size (N > 1)
+    nvls = None
+    if dist is not None and not args.no_nvls:
+        try:
+            nv = G.Nvls(nbytes, dev)
+            G.fill_synthetic(nv.ptr, count, args.dtype, seed, rank, 0)
+            for _ in range(args.warmup):
+                nv.allreduce(count, args.dtype)
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                nv.allreduce(count, args.dtype)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            nv.async_error()
+            tt = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            nvls = {"busbw": round(busbw(nbytes, n, float(tt.item())), 2),
+                    "ms_per_step": round(float(tt.item()) * 1e3, 4),
+                    "note": "multimem.ld_reduce/st through the NVSwitch; switch-chosen summation order"}
+            nv.destroy()
+        except Exception as e:   # multicast unavailable: report, do not fail the bench
+            nvls = {"unavailable": str(e)[:200]}
+
     # NCCL on the same buffer (N > 1)
     nccl = None
     if dist is not None and not args.no_nccl:
@@ -410,6 +437,8 @@ def main():
     }
     if nccl:
         line["nccl"] = nccl
+    if nvls:
+        line["nvls"] = nvls
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
