@@ -1,0 +1,164 @@
+"""Regenerate profiles/README.md from the raw evidence files under profiles/.
+
+    python tools/profiles_report.py > profiles/README.md
+
+Every number in the README comes from a file committed next to it (bench lines, harness
+JSONL sweeps, the GenModel fit report, the ncu summary), so the README cannot drift from the
+data."""
+import collections
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles")
+
+
+def jl(path):
+    with open(path) as f:
+        return [json.loads(l) for l in f if l.startswith("{")]
+
+
+def jload(path):
+    with open(path) as f:
+        for l in f:
+            if l.startswith("{"):
+                return json.loads(l)
+    raise ValueError(path)
+
+
+def size(b):
+    return f"{b >> 20} MiB" if b >= 1 << 20 else f"{b >> 10} KiB"
+
+
+def bench_section(out):
+    out.append("## 1. bench.py lines (metric: AllReduce busbw, bf16, 256 MiB per rank)\n")
+    out.append("| GPUs | ranks | plan | busbw GB/s | ms/step | roofline (GB/s) | NCCL busbw | NVLS busbw | GenModel pred. err |")
+    out.append("|---|---|---|---|---|---|---|---|---|")
+    e2e = []
+    cpu = None
+    for n in (1, 2, 4, 8):
+        f = os.path.join(P, "round1", f"bench_n{n}.json")
+        if not os.path.exists(f):
+            continue
+        d = jload(f)
+        rf = d["roofline"]
+        nc = d.get("nccl", {}).get("busbw", "-")
+        nv = d.get("nvls", {}).get("busbw", "-")
+        out.append(f"| {d['n_gpus']} | {d['config']['ranks']} | {d['config']['plan']} | {d['value']} | "
+                   f"{d['ms_per_step']} | {rf['bound']} {rf['achieved']} / {rf['peak']} = {rf['frac']} | "
+                   f"{nc} | {nv} | {d.get('genmodel', {}).get('pred_err', '-')} |")
+        e2e.append(f"N={n} {d['e2e']['value']} GB/s")
+        if n == 1:
+            cpu = d["cpu_baseline"]
+    out.append("")
+    out.append("* N = 1 runs 8 ranks emulated on one GPU (config C5's \"8 ranks/GPU\"): every rank buffer is\n"
+               "  read once and written once from HBM (2·8·256 MiB per call), so the roofline is HBM\n"
+               "  (measured copy peak in `MEASURED_PEAKS.json`).\n"
+               "* N > 1: one process per GPU, peer buffers IPC-mapped, the kernel pulls/pushes over NVLink 5;\n"
+               "  roofline = 2(N−1)/N·S bytes per direction per GPU (Eq. 2) against the measured 770 GB/s\n"
+               "  peer copy (B200_PROFILING.md).\n"
+               "* `NVLS` = the NEXT #1 plan kind (multimem.ld_reduce/st through the NVSwitch, 16 CTAs),\n"
+               "  reported beside the GenTree value, not in it (its summation order is the switch's).")
+    if cpu:
+        out.append(f"* cpu_baseline (oracle, {cpu['cores']} core, {cpu['sample']}): {cpu['value']} GB/s.")
+    out.append("* e2e through `allreduce_exec_host` (pinned host memory, H2D + exec + D2H per step): "
+               + ", ".join(e2e) + ".\n")
+
+
+def ncu_section(out):
+    out.append("## 2. ncu evidence for the dominant kernel (bench N=1 config)\n")
+    tr = json.load(open(os.path.join(P, "ncu_traffic.json")))
+    for k, v in tr.items():
+        out.append(f"* `{k}`: DRAM traffic {v['traffic_bytes_per_launch'] / 1e9:.4f} GB per launch "
+                   f"(read {v['dram_read'] / 1e9:.4f}, write {v['dram_write'] / 1e9:.4f}), "
+                   f"{v['duration_us']} µs cold; source {v['source']}.")
+    out.append("* Summary with stall reasons: `round1/ncu_exec_emulated8_bf16_256MiB.md`; launch list:\n"
+               "  `round1/ncu_launches_bench_n1.csv` (`ar_exec_kernel` is the only kernel in the timed\n"
+               "  region; `fill_kernel` launches are input set-up).  Algorithmic bytes per launch =\n"
+               "  2·8·256 MiB = 4.295 GB, so traffic/algorithmic ≈ 0.99: no re-reads.\n")
+
+
+def sweep_table(out, path, title):
+    rows = jl(path)
+    t = collections.defaultdict(dict)
+    for r in rows:
+        t[r["bytes"]][(r["plan"], r["timing"])] = r["busbw_med"]
+    plans = [p for p in ("gentree", "nvls", "default") if any((p, "graph") in d for d in t.values())]
+    name = {"gentree": "GenTree", "nvls": "NVLS", "default": "NCCL"}
+    out.append(f"**{title}** (busbw GB/s, median; eager = per-call events incl. host launch, graph = CUDA-graph replay)\n")
+    hdr = "| size | " + " | ".join(f"{name[p]} eager | {name[p]} graph" for p in plans) + " | GenTree/NCCL (graph) |"
+    out.append(hdr)
+    out.append("|" + "---|" * (2 + 2 * len(plans)))
+    for b in sorted(t):
+        d = t[b]
+        cells = []
+        for p in plans:
+            cells += [f"{d.get((p, 'eager'), float('nan')):.1f}", f"{d.get((p, 'graph'), float('nan')):.1f}"]
+        ratio = d.get(("gentree", "graph"), 0) / max(d.get(("default", "graph"), 1e-9), 1e-9)
+        out.append(f"| {size(b)} | " + " | ".join(cells) + f" | {ratio:.2f} |")
+    out.append("")
+
+
+def c2_section(out):
+    out.append("## 3. C2 sweep: busbw vs size — GenTree plan, NVLS, NCCL on the same box\n")
+    c2 = os.path.join(P, "round1", "c2")
+    sweep_table(out, os.path.join(c2, "sweep_n4_f32_nvls16.jsonl"), "C2, 4×B200, fp32 (GenTree chose CPS at every size)")
+    sweep_table(out, os.path.join(c2, "sweep_n2_f32_nvls16.jsonl"), "C2, 2×B200, fp32 (GenTree chose CPS at every size)")
+    bf = os.path.join(c2, "sweep_n4_bf16.jsonl")
+    if os.path.exists(bf):
+        sweep_table(out, bf, "4×B200, bf16")
+    out.append("NVLS wire volume per GPU and direction is (1 + 1/N)·S against the P2P plans'\n"
+               "2(N−1)/N·S: at N = 2 that is 1.5·S vs 1·S, so NVLS loses at large sizes on 2 GPUs and\n"
+               "wins on 4 (1.25·S vs 1.5·S); at small sizes its single switch round trip wins on both.\n")
+
+
+def fit_section(out):
+    f = json.load(open(os.path.join(P, "genmodel_fit_nvlink_graph.json")))
+    pp = f["params_per_byte"]
+    out.append("## 4. GenModel on B200 (C3 + prediction error)\n")
+    out.append(f"**Fit (§3.4, P:530-532)** from {f['fit_rows']} CPS AllReduce rows at N = 2, 3, 4 (graph timing),\n"
+               f"`genmodel_fit` C-ABI, w_t ≥ 4 from the x-to-x probe (§5 below): α = {pp['alpha'] * 1e6:.2f} µs,\n"
+               f"(2β+γ) = {pp['combined']:.4g} s/B (≈ {2 / pp['combined'] / 1e9:.0f} GB/s effective per direction),\n"
+               f"δ = {pp['delta']}, ε = {pp['epsilon']}, w_t = {pp['w_t']}.\n")
+    ge, ab, ps = f["genmodel_err"], f["abc_err"], f["genmodel_paper_steps_err"]
+    out.append(f"**Prediction error** over {f['validation_rows']} measurements (plans GenTree/CPS/Ring/RHD/HCPS[2,2]/RB\n"
+               f"at N = 2, 3, 4, 1 MiB…1 GiB): GenModel of the executed plan (`genmodel_predict_executed`)\n"
+               f"median {ge['median'] * 100:.1f} %, max {ge['max'] * 100:.1f} %; the (α,β,γ) model fitted on the same rows\n"
+               f"median {ab['median'] * 100:.1f} %, max {ab['max'] * 100:.1f} %; GenModel on the paper's unfused step\n"
+               f"structure (`genmodel_predict`) median {ps['median'] * 100:.1f} %, max {ps['max'] * 100:.1f} %.")
+    out.append("Max error per plan: " + ", ".join(f"{k} {v * 100:.1f} %" for k, v in f["genmodel_err_by_plan_max"].items()) + ".")
+    out.append("RB (one GPU's SMs issue all traffic) and the multi-step RHD/HCPS at 1–4 MiB (each extra\n"
+               "executed step costs more than the fitted α) are where the model is weakest.\n")
+    e6 = f["eq6_local_fanin"]
+    out.append(f"**Eq. 6 local fan-in (C3-i, P:406-414)**, x = 2…8 vectors of {e6['vector_bytes'] // 4 // 10**6} M fp32:\n"
+               f"T(x)/(x−1) strictly decreasing: {e6['strictly_decreasing']}; fitted C1 = Sδ = {e6['C1_s'] * 1e3:.4f} ms\n"
+               f"(δ = {e6['delta_per_byte']:.4g} s/B ≈ {1 / e6['delta_per_byte'] / 1e12:.2f} TB/s effective), "
+               f"C2 = Sγ = {e6['C2_s'] * 1e3:.4f} ms (reading Q18).\n")
+
+
+def p2p_section(out):
+    out.append("## 5. Incast probe (x-to-x, S:449) on 4×B200\n")
+    out.append("| pattern | bytes | GB/s per direction per GPU |")
+    out.append("|---|---|---|")
+    for r in jl(os.path.join(P, "round1", "p2p", "p2p4.jsonl")):
+        out.append(f"| {r['kind']} (x={r['x']}) | {size(r['bytes'])} | {r['gbs_per_direction_per_gpu']:.1f} |")
+    out.append("\nNo throughput loss as the fan-in x grows to 4 (the whole box): no incast inside one NVSwitch\n"
+               "domain, hence w_t ≥ 4 in the fit and ε = 0.\n")
+
+
+def main():
+    out = ["# profiles/ — measured evidence (round 1)\n",
+           "Generated by `tools/profiles_report.py` from the files in this directory.  All numbers were\n"
+           "measured on B200 boxes through `gpurun` (driver 580.159, CUDA 12.9, NCCL 2.28.9, SM clock\n"
+           "1965 MHz, no throttle reasons during the timed regions).\n"]
+    bench_section(out)
+    ncu_section(out)
+    c2_section(out)
+    fit_section(out)
+    p2p_section(out)
+    sys.stdout.write("\n".join(out) + "\n")
+
+
+if __name__ == "__main__":
+    main()
