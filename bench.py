@@ -351,6 +351,12 @@ def main():
             nvls = {"busbw": round(busbw(nbytes, n, float(tt.item())), 2),
                     "ms_per_step": round(float(tt.item()) * 1e3, 4),
                     "note": "multimem.ld_reduce/st through the NVSwitch; switch-chosen summation order"}
+            npath = os.path.join(ROOT, "profiles", "genmodel_params_nvls.json")
+            if os.path.exists(npath):   # GenModel's plan-vs-NVLS choice (NEXT #1 row, reading NV1)
+                nj = json.load(open(npath))
+                c = plan.choose_nvls(gp, G.params(alpha=nj["alpha"], beta=nj["beta"]))
+                nvls["genmodel"] = {"use_nvls": c["use_nvls"], "t_plan_ms": round(c["t_plan"] * 1e3, 4),
+                                    "t_nvls_ms": round(c["t_nvls"] * 1e3, 4), "params": nj["source"]}
             nv.destroy()
         except Exception as e:   # multicast unavailable: report, do not fail the bench
             nvls = {"unavailable": str(e)[:200]}

@@ -78,9 +78,18 @@ typedef struct {
 int genmodel_fit(const gm_measurement *rows, size_t n_rows, int32_t wt_min, int32_t wt_max,
                  double link_bytes_per_s, gm_params *out, double *sse);
 
+/* Fit of the NVLS plan row ("modelled in GenModel as a new plan row,
+ * with α and β fitted in C3"; reading NV1): NNLS for (α, β) in
+ * T(n, s) = 2α + ((n+1)·s/n)·β over rows of measured NVLS AllReduce times (allreduce_exec_nvls).
+ * out: alpha, beta set; gamma = delta = epsilon = 0, w_t = 1, has_combined = 0 (usable with
+ * genmodel_closed_form("nvls", ...)).  Repeated (n, bytes) rows are averaged.  `sse` may be
+ * NULL.  Errors: AR_EINVAL on a bad row or fewer than 2 distinct sizes. */
+int genmodel_fit_nvls(const gm_measurement *rows, size_t n_rows, gm_params *out, double *sse);
+
 /* Table 2 closed form (readings Q5-Q7) of `kind` ("cps", "ring", "rhd", "rb",
- * "hcps:f0,f1,...") for n ranks and `bytes` per rank, evaluated in the fixed float64
- * order of DESIGN.md.  Errors: AR_EINVAL for n < 2, unknown kind, bad factorization. */
+ * "hcps:f0,f1,...", or "nvls" = the in-switch row of reading NV1) for n ranks and `bytes`
+ * per rank, evaluated in the fixed float64 order of DESIGN.md.  Errors: AR_EINVAL for
+ * n < 2, unknown kind, bad factorization. */
 int genmodel_closed_form(const char *kind, int32_t n, uint64_t bytes, const gm_params *params,
                          gm_breakdown *out);
 
@@ -132,6 +141,14 @@ int gt_plan_from_json(const char *plan_json, gt_plan **out, int32_t *is_allreduc
  * B = max over ranks of max(bytes in, bytes out) per step, since NVLink is full duplex and a
  * fused step moves RS and AG traffic at the same time.  `params` is required (uniform). */
 int genmodel_predict_executed(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
+
+/* Plan-vs-NVLS selection by GenModel: *t_plan = the executed-plan
+ * prediction of `plan` under plan_params (genmodel_predict_executed), *t_nvls = the "nvls"
+ * closed form at the plan's (n, bytes) under nvls_params; *use_nvls = 1 iff t_nvls < t_plan
+ * (ties keep the plan, whose result is bit-reproducible).  t_plan/t_nvls may be NULL.
+ * Errors: AR_EINVAL for null plan/params/use_nvls or invalid params. */
+int genmodel_choose_nvls(const gt_plan *plan, const gm_params *plan_params, const gm_params *nvls_params,
+                         int32_t *use_nvls, double *t_plan, double *t_nvls);
 
 /* ------------------------------------------------------------------ communicator */
 

@@ -58,6 +58,26 @@ def fit_params(rows, wt_min: int, wt_max: int):
             "scan": [(w, s) for w, s, _ in scan]}
 
 
+def nvls_design_row(n: int, s: float) -> list:
+    """NVLS row of the closed forms (reading NV1): T = 2α + ((n+1)·s/n)·β."""
+    return [2.0, (n + 1) * s / n]
+
+
+def fit_nvls(rows):
+    """NNLS for (α, β) of the NVLS row ("α and β fitted in C3").
+    rows: (n, s_bytes, t_seconds), repeated (n, s) averaged.  Needs >= 2 distinct rows."""
+    rows = average_rows(rows)
+    if len(rows) < 2 or len({s for _, s, _ in rows}) < 2:
+        raise ValueError("underdetermined: need >= 2 distinct sizes")
+    A = np.array([nvls_design_row(n, s) for n, s, _ in rows])
+    t = np.array([r[2] for r in rows])
+    scale = np.maximum(np.abs(A).max(axis=0), 1e-300)
+    x, _ = nnls(A / scale, t)
+    x = x / scale
+    r = A @ x - t
+    return {"alpha": float(x[0]), "beta": float(x[1]), "sse": float(r @ r)}
+
+
 def split_combined(k: float, link_bytes_per_s: float):
     """β from the bandwidth, γ = k − 2β; error if that is negative."""
     beta = 1.0 / link_bytes_per_s

@@ -205,6 +205,13 @@ def closed_form_terms(kind: str, c: int, S: int, w_t: int, fanins: tuple = ()):
                 tail *= f[j]
             inc += max(0, f[i] - w_t) * 2 * (f[i] - 1) * tail
         return (2 * m, 2 * (c - 1) * S, (c - 1) * S, (2 * suffix_sum + c + 1) * S, inc * S, c)
+    if kind == "nvls":
+        # SURVEY §8(f) NEXT #1, reading NV1: CPS's two steps with the fan-in-N
+        # reduce done in the switch.  Per GPU and direction it sends its S/N slice to each
+        # of the N switch reductions (S) plus its reduced block once (S/N), and receives its
+        # reduced block (S/N) plus N multicast blocks (S): B = (N+1)·S/N.  No GPU-side
+        # reduce (C = D = 0) and no unicast many-to-one flows (I = 0).
+        return 2, (c + 1) * S, 0, 0, 0, c
     raise ValueError(f"no closed form for {kind!r}")
 
 

@@ -66,6 +66,10 @@ _SIGS = {
     "ar_version": (ctypes.c_char_p, []),
     "genmodel_fit": (I32, [ctypes.POINTER(GmMeasurement), SZ, I32, I32, ctypes.c_double,
                            ctypes.POINTER(GmParams), ctypes.POINTER(ctypes.c_double)]),
+    "genmodel_fit_nvls": (I32, [ctypes.POINTER(GmMeasurement), SZ, ctypes.POINTER(GmParams),
+                                ctypes.POINTER(ctypes.c_double)]),
+    "genmodel_choose_nvls": (I32, [P, ctypes.POINTER(GmParams), ctypes.POINTER(GmParams), ctypes.POINTER(I32),
+                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "genmodel_closed_form": (I32, [ctypes.c_char_p, I32, U64, ctypes.POINTER(GmParams),
                                    ctypes.POINTER(GmBreakdown)]),
     "gentree_plan": (I32, [ctypes.c_char_p, U64, I32, ctypes.POINTER(GmParams), ctypes.c_char_p,

@@ -18,7 +18,7 @@ import json
 from . import _lib as L
 from ._lib import AR_BF16, AR_F32, GmBreakdown, GmMeasurement, GmParams, check, lib
 
-__all__ = ["GmParams", "params", "genmodel_fit", "genmodel_closed_form", "Plan", "Comm",
+__all__ = ["GmParams", "params", "genmodel_fit", "genmodel_fit_nvls", "genmodel_closed_form", "Plan", "Comm",
            "allreduce_exec", "allreduce_exec_host", "fill_synthetic", "local_reduce",
            "rank_stride_bytes", "dtype_code"]
 
@@ -55,6 +55,19 @@ def genmodel_fit(rows, wt_min: int, wt_max: int, link_bytes_per_s: float = 0.0):
     sse = ctypes.c_double()
     check(lib.genmodel_fit(arr, len(rows), wt_min, wt_max, float(link_bytes_per_s), ctypes.byref(out),
                            ctypes.byref(sse)))
+    return out, sse.value
+
+
+def genmodel_fit_nvls(rows):
+    """NVLS plan row fit (reading NV1).  rows: iterable of (n, bytes, seconds).
+    Returns (GmParams with alpha, beta; sse)."""
+    rows = list(rows)
+    arr = (GmMeasurement * max(1, len(rows)))()
+    for i, (n, b, t) in enumerate(rows):
+        arr[i] = GmMeasurement(int(n), 0, int(b), float(t))
+    out = GmParams()
+    sse = ctypes.c_double()
+    check(lib.genmodel_fit_nvls(arr, len(rows), ctypes.byref(out), ctypes.byref(sse)))
     return out, sse.value
 
 
@@ -131,6 +144,14 @@ class Plan:
         out = GmBreakdown()
         check(lib.genmodel_predict_executed(self._h, ctypes.byref(params), ctypes.byref(out)))
         return out.as_dict()
+
+    def choose_nvls(self, params: GmParams, nvls_params: GmParams) -> dict:
+        """GenModel's plan-vs-NVLS choice at this plan's (n, bytes) (genmodel_choose_nvls)."""
+        use = ctypes.c_int32()
+        tp, tn = ctypes.c_double(), ctypes.c_double()
+        check(lib.genmodel_choose_nvls(self._h, ctypes.byref(params), ctypes.byref(nvls_params), ctypes.byref(use),
+                                       ctypes.byref(tp), ctypes.byref(tn)))
+        return {"use_nvls": bool(use.value), "t_plan": tp.value, "t_nvls": tn.value}
 
     @property
     def handle(self):

@@ -93,6 +93,42 @@ int genmodel_fit(const gm_measurement *rows, size_t n_rows, int32_t wt_min, int3
   })
 }
 
+int genmodel_fit_nvls(const gm_measurement *rows, size_t n_rows, gm_params *out, double *sse) {
+  AR_TRY({
+    if (!rows || !out) throw InvalidArg("null argument");
+    std::vector<Measurement> m;
+    for (size_t i = 0; i < n_rows; i++) {
+      if (rows[i].n < 2 || rows[i].bytes < 1 || !(rows[i].seconds > 0)) throw InvalidArg("bad measurement row");
+      m.push_back({rows[i].n, (double)rows[i].bytes, rows[i].seconds});
+    }
+    NvlsFit f = fit_nvls(m);
+    gm_params o{};
+    o.alpha = f.alpha;
+    o.beta = f.beta;
+    o.w_t = 1;
+    *out = o;
+    if (sse) *sse = f.sse;
+    return AR_OK;
+  })
+}
+
+int genmodel_choose_nvls(const gt_plan *plan, const gm_params *plan_params, const gm_params *nvls_params,
+                         int32_t *use_nvls, double *t_plan, double *t_nvls) {
+  AR_TRY({
+    if (!plan || !plan_params || !nvls_params || !use_nvls) throw InvalidArg("null argument");
+    check_params(plan_params);
+    check_params(nvls_params);
+    gm_breakdown bp{};
+    if (genmodel_predict_executed(plan, plan_params, &bp) != AR_OK) return AR_EINVAL;
+    const int64_t S = plan->plan.count * (int64_t)plan->esize;
+    Breakdown bn = closed_form_f64("nvls", plan->plan.n, S, to_params(nvls_params), {});
+    *use_nvls = bn.total < bp.total ? 1 : 0;   // ties keep the plan (bit-reproducible order)
+    if (t_plan) *t_plan = bp.total;
+    if (t_nvls) *t_nvls = bn.total;
+    return AR_OK;
+  })
+}
+
 int genmodel_closed_form(const char *kind, int32_t n, uint64_t bytes, const gm_params *params, gm_breakdown *out) {
   AR_TRY({
     if (!kind || !params || !out) throw InvalidArg("null argument");

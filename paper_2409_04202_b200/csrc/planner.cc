@@ -707,6 +707,9 @@ static void closed_form_terms(const std::string &kind, int c, int64_t S, int w_t
       inc += ov * 2 * (f[i] - 1) * tail;
     }
     A = 2 * m; Bn = 2 * cm1 * S; Cn = cm1 * S; Dn = (2 * suffix + c + 1) * S; In = inc * S; den = c;
+  } else if (kind == "nvls") {
+    // DESIGN.md reading NV1: in-switch fan-in-N reduce + multicast; (N+1)S/N per direction
+    A = 2; Bn = (int64_t)(c + 1) * S; Cn = 0; Dn = 0; In = 0; den = c;
   } else {
     throw InvalidArg("no closed form for " + kind);
   }
@@ -1309,6 +1312,43 @@ FitResult fit_params(const std::vector<Measurement> &rows_in, int wt_min, int wt
       return f;
     }
   throw InvalidArg("fit failed");
+}
+
+NvlsFit fit_nvls(const std::vector<Measurement> &rows_in) {
+  std::map<std::pair<int, double>, std::vector<double>> acc;
+  for (auto &r : rows_in) acc[{r.n, r.s}].push_back(r.t);
+  std::vector<Measurement> rows;
+  std::set<double> ss;
+  for (auto &kv : acc) {
+    double sum = 0;
+    for (double v : kv.second) sum += v;
+    rows.push_back({kv.first.first, kv.first.second, sum / kv.second.size()});
+    ss.insert(kv.first.second);
+  }
+  if (rows.size() < 2 || ss.size() < 2) throw InvalidArg("underdetermined: need >= 2 distinct sizes");
+  std::vector<std::vector<double>> A;
+  std::vector<double> b;
+  for (auto &r : rows) {
+    double n = r.n, s = r.s;
+    A.push_back({2.0, (n + 1) * s / n});
+    b.push_back(r.t);
+  }
+  double scale[2] = {1e-300, 1e-300};
+  for (auto &row : A)
+    for (int j = 0; j < 2; j++) scale[j] = std::max(scale[j], std::fabs(row[j]));
+  auto As = A;
+  for (auto &row : As)
+    for (int j = 0; j < 2; j++) row[j] /= scale[j];
+  auto x = nnls(As, b);
+  for (int j = 0; j < 2; j++) x[j] /= scale[j];
+  NvlsFit f;
+  f.alpha = x[0];
+  f.beta = x[1];
+  for (size_t i = 0; i < A.size(); i++) {
+    double r = A[i][0] * x[0] + A[i][1] * x[1] - b[i];
+    f.sse += r * r;
+  }
+  return f;
 }
 
 }  // namespace gtar

@@ -123,5 +123,7 @@ struct FitResult {
   int w_t = 0;
 };
 FitResult fit_params(const std::vector<Measurement> &rows, int wt_min, int wt_max);
+struct NvlsFit { double alpha = 0, beta = 0, sse = 0; };
+NvlsFit fit_nvls(const std::vector<Measurement> &rows);   // NVLS row (reading NV1)
 
 }  // namespace gtar

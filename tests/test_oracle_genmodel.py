@@ -199,3 +199,53 @@ def test_hcps_memory_nonincreasing_in_f0():
         d = {f[0]: Fraction(G.closed_form_terms("hcps", n, 1, 99, f)[3], n) for f in fs}
         keys = sorted(d)
         assert all(d[a] >= d[b] for a, b in zip(keys, keys[1:]))
+
+
+def _nvls_wire_bytes(n: int, S: int):
+    """Brute-force byte count of the NVLS data movement (DESIGN.md §6 NVLS, reading NV1):
+    owner r of block r issues one switch reduce (every GPU g ships its copy of block r into
+    the switch; the sum comes back to r) and one multicast store (r ships the sum; the switch
+    delivers it to every GPU).  Returns per-GPU (bytes out, bytes in)."""
+    blk = S // n
+    out = [0] * n
+    inn = [0] * n
+    for r in range(n):
+        for g in range(n):            # multimem.ld_reduce: each GPU serves its copy
+            out[g] += blk
+        inn[r] += blk                 # reduced vector returns to the issuer
+        out[r] += blk                 # multimem.st: issuer sends once
+        for g in range(n):            # switch replicates to every GPU
+            inn[g] += blk
+    return out, inn
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8, 16])
+def test_nvls_row_matches_wire_count(n):
+    """NEXT #1 row: B = max per-GPU bytes per direction of the counted movement; C = D = I = 0;
+    two latency rounds (reduce, multicast).  Also CPS's B by the same count ratio at N = 2."""
+    S = n * 1000
+    out, inn = _nvls_wire_bytes(n, S)
+    A, Bn, Cn, Dn, In, den = G.closed_form_terms("nvls", n, S, 1)
+    assert Fraction(Bn, den) == max(max(out), max(inn))
+    assert (A, Cn, Dn, In) == (2, 0, 0, 0)
+    p = G.Params(Fraction(3, 10**6), Fraction(7, 10**13), 0, 0, 0, 1)
+    e = G.closed_form_exact("nvls", n, S, p)
+    assert e["total"] == 2 * p.alpha + max(max(out), max(inn)) * p.beta
+    # vs P2P CPS's 2(N-1)S/N (Eq. 2, P:200-203): more at N = 2, equal at 3, less from 4 on
+    _, Bc, _, _, _, dc = G.closed_form_terms("cps", n, S, 99)
+    assert (Fraction(Bn, den) > Fraction(Bc, dc)) == (n == 2)
+    assert (Fraction(Bn, den) == Fraction(Bc, dc)) == (n == 3)
+
+
+def test_nvls_fit_recovers_parameters():
+    """fit_nvls on rows built from the wire count (not from the closed form) recovers α, β."""
+    from oracle import fit as F
+    alpha, beta = 11e-6, 1.75e-12
+    rows = []
+    for n in (2, 4, 8):
+        for S in (1 << 20, 1 << 24, 1 << 28):
+            out, inn = _nvls_wire_bytes(n, S)
+            rows.append((n, S, 2 * alpha + max(max(out), max(inn)) * beta))
+    f = F.fit_nvls(rows)
+    assert f["alpha"] == pytest.approx(alpha, rel=1e-9)
+    assert f["beta"] == pytest.approx(beta, rel=1e-9)

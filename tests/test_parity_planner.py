@@ -162,3 +162,35 @@ def test_rearrangement_topologies(shape):
     lp, op = check_topology(doc, 10 ** 6)
     assert any(r["rearranged_children"] for r in lp.report())
     assert any(len(r.inputs) == 1 for st in op.steps for r in st.reduces)   # moves present
+
+
+def test_nvls_row_and_fit_parity():
+    """NEXT #1: the NVLS closed-form row and its (α, β) fit, library vs oracle."""
+    p = OG.Params(9.4e-6, 1.7e-12, 0, 0, 0, 1)
+    for n in (2, 4, 8):
+        for S in (4, 1 << 20, 123456789):
+            same_breakdown(G.genmodel_closed_form("nvls", n, S, lib_params(p)),
+                           OG.closed_form_f64("nvls", n, S, p))
+    rows = [(n, s, 2 * 9e-6 + (n + 1) * s / n * 1.8e-12 * (1 + 0.01 * ((n * s) % 7)))
+            for n in (2, 4) for s in (1 << 20, 1 << 24, 1 << 28)]
+    lp, sse = G.genmodel_fit_nvls(rows)
+    o = OF.fit_nvls(rows)
+    assert lp.alpha == pytest.approx(o["alpha"], rel=1e-9)
+    assert lp.beta == pytest.approx(o["beta"], rel=1e-9)
+    assert sse == pytest.approx(o["sse"], rel=1e-6)
+
+
+def test_choose_nvls():
+    """genmodel_choose_nvls = (executed-plan prediction) vs (NVLS closed form)."""
+    pp = G.params(alpha=9.4e-6, combined=2.93e-12, w_t=4)
+    nv = G.params(alpha=8e-6, beta=1.75e-12)
+    for n, count in ((2, 1 << 26), (4, 1 << 26), (2, 1 << 12), (4, 1 << 12)):
+        plan = G.Plan.single_switch(n, count, "bf16", pp)
+        c = plan.choose_nvls(pp, nv)
+        assert c["t_plan"] == plan.predict_executed(pp)["total"]
+        assert c["t_nvls"] == G.genmodel_closed_form("nvls", n, 2 * count, nv)["total"]
+        assert c["use_nvls"] == (c["t_nvls"] < c["t_plan"])
+    # the wire model: NVLS loses at N = 2 and wins at N = 4 for large messages with equal β
+    eq = G.params(alpha=9.4e-6, beta=1.465e-12)
+    assert not G.Plan.single_switch(2, 1 << 27, "bf16", pp).choose_nvls(pp, eq)["use_nvls"]
+    assert G.Plan.single_switch(4, 1 << 27, "bf16", pp).choose_nvls(pp, eq)["use_nvls"]

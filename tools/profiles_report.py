@@ -137,6 +137,19 @@ def fit_section(out):
                f"C2 = Sγ = {e6['C2_s'] * 1e3:.4f} ms (reading Q18).\n")
 
 
+def nvls_fit_section(out):
+    path = os.path.join(P, "genmodel_fit_nvls_graph.json")
+    if not os.path.exists(path):
+        return
+    f = json.load(open(path))
+    out.append("**NVLS plan row (NEXT #1, reading NV1)**, T = 2α + (N+1)S/N·β fitted on the NVLS sweeps\n"
+               f"(N = 2 and 4, ≥ {size(f['min_bytes'])}, {f['fit_rows']} rows, `genmodel_fit_nvls`): α = {f['alpha'] * 1e6:.2f} µs,\n"
+               f"β = {f['beta']:.4g} s/B ({f['beta_gbs']:.0f} GB/s per direction); prediction error median\n"
+               f"{f['pred_err_median'] * 100:.1f} %, max {f['pred_err_max'] * 100:.1f} %.  GenModel's plan-vs-NVLS choice\n"
+               f"(`genmodel_choose_nvls`) matched the measured winner in {f['choice_correct']} of {f['choice_total']} (N, size)\n"
+               f"cells; the wrong picks are near the crossover, max regret {f['choice_max_regret'] * 100:.1f} %.\n")
+
+
 def p2p_section(out):
     out.append("## 5. Incast probe (x-to-x, S:449) on 4×B200\n")
     out.append("| pattern | bytes | GB/s per direction per GPU |")
@@ -156,6 +169,7 @@ def main():
     ncu_section(out)
     c2_section(out)
     fit_section(out)
+    nvls_fit_section(out)
     p2p_section(out)
     sys.stdout.write("\n".join(out) + "\n")
 
