@@ -202,6 +202,19 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
 int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
                    void *stream);
 
+/* Reduction operators of allreduce_exec_op.  AR_OP_AVG (DESIGN.md
+ * reading AV1): the last ReduceScatter op writing each block divides its fp32 sum by the
+ * world size N with one correctly rounded IEEE fp32 division, before the store's rounding
+ * (bf16: RNE of the fp32 quotient); the AllGather then copies that value, so every rank ends
+ * with the same bits. */
+#define AR_OP_SUM 0
+#define AR_OP_AVG 1
+
+/* allreduce_exec with an explicit operator (AR_OP_SUM = allreduce_exec).  Same contract and
+ * errors; AR_EINVAL for an unknown op. */
+int allreduce_exec_op(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype, int32_t op,
+                      void *stream);
+
 /* The same, end to end from host memory: copies `host` (pinned recommended; for an emulated
  * comm world consecutive rank buffers at the same stride) into dptr, executes, copies the
  * result back into `host`, all on `stream`. */

@@ -7,6 +7,9 @@ Follows the plan semantics of `oracle.plans` literally:
     re-association); bf16 data is widened exactly and rounded to bf16 (RNE) once, when the
     partial is stored (reading Q2).  A one-input Reduce is a raw bit move.
   * AG Transfer(src, dst, b): raw bit copy.
+  * op "avg" (reading AV1): the Reduce(s) of block b in the
+    last RS step that reduces b divide the fp32 sum by N (one correctly rounded IEEE binary32
+    division) before the store's rounding; a one-input Reduce there widens, divides, stores.
 Every step's hazard-freedom is checked first (`check_step_hazards`), so applying its ops in
 any order is equivalent to the concurrent semantics.
 
@@ -37,33 +40,51 @@ def f32_to_bf16_rne(x: np.ndarray) -> np.ndarray:
     return rounded.astype(np.uint16)
 
 
-def simulate(plan: Plan, inputs: list, dtype: str) -> list:
+def last_rs_step(plan: Plan) -> dict:
+    """block -> index of the last RS step that has a Reduce writing it (reading AV1)."""
+    last = {}
+    for i, st in enumerate(plan.steps):
+        if st.phase == "rs":
+            for rd in st.reduces:
+                last[rd.block] = i
+    return last
+
+
+def simulate(plan: Plan, inputs: list, dtype: str, op: str = "sum") -> list:
     """Run `plan` on per-rank inputs (float32 arrays, or uint16 bf16 bit arrays).
     Returns the per-rank output buffers (new arrays)."""
     n, count = plan.n, plan.count
+    if op not in ("sum", "avg"):
+        raise ValueError(op)
+    last = last_rs_step(plan)
     bufs = [np.array(x, copy=True) for x in inputs]
     for x in bufs:
         if x.shape != (count,):
             raise ValueError("input length != plan count")
-    for st in plan.steps:
+    for si, st in enumerate(plan.steps):
         check_step_hazards(st)
         if st.phase == "rs":
             for rd in st.reduces:
                 o, sz = block_offset(count, n, rd.block), block_size(count, n, rd.block)
                 if sz == 0:
                     continue
-                if len(rd.inputs) == 1:
+                div = op == "avg" and last[rd.block] == si
+                if len(rd.inputs) == 1 and not div:
                     bufs[rd.server][o:o + sz] = bufs[rd.inputs[0]][o:o + sz]
                     continue
                 if dtype == "f32":
                     acc = bufs[rd.inputs[0]][o:o + sz].astype(np.float32, copy=True)
                     for q in rd.inputs[1:]:
                         acc = acc + bufs[q][o:o + sz]
+                    if div:
+                        acc = acc / np.float32(n)
                     bufs[rd.server][o:o + sz] = acc
                 else:
                     acc = bf16_bits_to_f32(bufs[rd.inputs[0]][o:o + sz]).copy()
                     for q in rd.inputs[1:]:
                         acc = acc + bf16_bits_to_f32(bufs[q][o:o + sz])
+                    if div:
+                        acc = acc / np.float32(n)
                     bufs[rd.server][o:o + sz] = f32_to_bf16_rne(acc)
         else:
             for t in st.transfers:
@@ -110,9 +131,16 @@ def _bf16_round(v: float) -> int:
     return lo if (lo & 1) == 0 else (hi & 0xFFFF)
 
 
-def simulate_scalar(plan: Plan, inputs: list, dtype: str) -> list:
-    """Element-by-element re-implementation for tiny cases (pins `simulate`)."""
+def simulate_scalar(plan: Plan, inputs: list, dtype: str, op: str = "sum") -> list:
+    """Element-by-element re-implementation for tiny cases (pins `simulate`).  AVG: the
+    double quotient of binary32 values rounded once to binary32 is the correctly rounded
+    binary32 quotient (53 >= 2*24 + 2)."""
     n, count = plan.n, plan.count
+    final = {}
+    for i, st in enumerate(plan.steps):
+        if st.phase == "rs":
+            for rd in st.reduces:
+                final[rd.block] = i
     if dtype == "f32":
         bufs = [[float(v) for v in x] for x in inputs]
     else:
@@ -123,18 +151,21 @@ def simulate_scalar(plan: Plan, inputs: list, dtype: str) -> list:
             return bufs[q][e]
         return struct.unpack("<f", struct.pack("<I", bufs[q][e] << 16))[0]
 
-    for st in plan.steps:
+    for si, st in enumerate(plan.steps):
         new = {}
         if st.phase == "rs":
             for rd in st.reduces:
                 o = block_offset(count, n, rd.block)
+                div = op == "avg" and final[rd.block] == si
                 for e in range(o, o + block_size(count, n, rd.block)):
-                    if len(rd.inputs) == 1:
+                    if len(rd.inputs) == 1 and not div:
                         new[(rd.server, e)] = bufs[rd.inputs[0]][e]
                         continue
                     acc = val(rd.inputs[0], e)
                     for q in rd.inputs[1:]:
                         acc = _f32(acc + val(q, e))
+                    if div:
+                        acc = _f32(acc / n)
                     new[(rd.server, e)] = acc if dtype == "f32" else _bf16_round(acc)
         else:
             for t in st.transfers:
@@ -148,7 +179,7 @@ def simulate_scalar(plan: Plan, inputs: list, dtype: str) -> list:
     return [np.array(b, dtype=np.uint16) for b in bufs]
 
 
-def simulate_at(plan: Plan, idx, values: list, dtype: str) -> list:
+def simulate_at(plan: Plan, idx, values: list, dtype: str, op: str = "sum") -> list:
     """The plan's outputs at selected element indices only (for full-size checks).
 
     idx: sorted element indices; values[r][k] = rank r's input at idx[k] (float32 values or
@@ -159,24 +190,30 @@ def simulate_at(plan: Plan, idx, values: list, dtype: str) -> list:
     bufs = [np.array(v, copy=True) for v in values]
     starts = np.array([block_offset(count, n, b) for b in range(n)], dtype=np.int64)
     blk = np.searchsorted(starts, idx, side="right") - 1
-    for st in plan.steps:
+    last = last_rs_step(plan)
+    for si, st in enumerate(plan.steps):
         if st.phase == "rs":
             for rd in st.reduces:
                 sel = np.nonzero(blk == rd.block)[0]
                 if sel.size == 0:
                     continue
-                if len(rd.inputs) == 1:
+                div = op == "avg" and last[rd.block] == si
+                if len(rd.inputs) == 1 and not div:
                     bufs[rd.server][sel] = bufs[rd.inputs[0]][sel]
                     continue
                 if dtype == "f32":
                     acc = bufs[rd.inputs[0]][sel].astype(np.float32, copy=True)
                     for q in rd.inputs[1:]:
                         acc = acc + bufs[q][sel]
+                    if div:
+                        acc = acc / np.float32(n)
                     bufs[rd.server][sel] = acc
                 else:
                     acc = bf16_bits_to_f32(bufs[rd.inputs[0]][sel]).copy()
                     for q in rd.inputs[1:]:
                         acc = acc + bf16_bits_to_f32(bufs[q][sel])
+                    if div:
+                        acc = acc / np.float32(n)
                     bufs[rd.server][sel] = f32_to_bf16_rne(acc)
         else:
             for t in st.transfers:

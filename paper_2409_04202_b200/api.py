@@ -323,12 +323,12 @@ class Executor:
     (e.g. every training step, or inside torch.cuda.graph capture: the kernel launch carries no
     per-call host state, the call epoch lives on the device)."""
 
-    def __init__(self, plan: Plan, comm: Comm, buf, stream=None):
+    def __init__(self, plan: Plan, comm: Comm, buf, stream=None, op: str = "sum"):
         info = plan.info()
         self._keep = (plan, comm, buf)
         self._args = (plan.handle, comm.handle, ctypes.c_void_p(_ptr(buf)), info["count"], info["dtype"],
-                      ctypes.c_void_p(_stream(stream)))
-        self._f = lib.allreduce_exec
+                      OPS[op], ctypes.c_void_p(_stream(stream)))
+        self._f = lib.allreduce_exec_op
 
     def __call__(self):
         rc = self._f(*self._args)
@@ -336,14 +336,21 @@ class Executor:
             check(rc)
 
 
-def allreduce_exec(plan: Plan, comm: Comm, buf, count: int | None = None, dtype=None, stream=None):
-    """In-place AllReduce of `buf` (torch tensor or device pointer) with `plan`."""
+OPS = {"sum": 0, "avg": 1}
+
+
+def allreduce_exec(plan: Plan, comm: Comm, buf, count: int | None = None, dtype=None, stream=None, op: str = "sum"):
+    """In-place AllReduce of `buf` (torch tensor or device pointer) with `plan`; op "sum" or
+    "avg" (allreduce_exec_op, reading AV1)."""
     info = None
     if count is None or dtype is None:
         info = plan.info()
     count = info["count"] if count is None else count
     dt = info["dtype"] if dtype is None else dtype_code(dtype)
-    check(lib.allreduce_exec(plan.handle, comm.handle, _ptr(buf), count, dt, _stream(stream)))
+    if op == "sum":
+        check(lib.allreduce_exec(plan.handle, comm.handle, _ptr(buf), count, dt, _stream(stream)))
+    else:
+        check(lib.allreduce_exec_op(plan.handle, comm.handle, _ptr(buf), count, dt, OPS[op], _stream(stream)))
 
 
 def allreduce_exec_host(plan: Plan, comm: Comm, dbuf, host_ptr: int, count: int, dtype, stream=None):

@@ -47,6 +47,8 @@ struct DevOp {
   long long off, len;        // elements
   int nsrc, ndst;
   int src_begin, dst_begin;  // into the rank list
+  int fin;                   // 1 = the last RS op writing this region (AVG divides here)
+  int pad;
 };
 struct DevStep {
   int slot;                  // flag slot written after this step (0 = entry)
@@ -83,6 +85,7 @@ struct ExecArgs {
   int store_tma;             // 1 = results leave through cp.async.bulk stores (body_bulk_st)
   int stages, stage_bytes;   // bulk-copy ring geometry
   unsigned int jitter_ns;    // stress mode: random delay before each notify (AR_JITTER_NS), 0 = off
+  int avg_n;                 // AR_OP_AVG: divide final reduces by avg_n (IEEE fp32 division); 0 = SUM
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -164,7 +167,15 @@ struct OpShared {
   const uint4 *src[AR_MAX_RANKS];
   uint4 *dst[AR_MAX_RANKS];
   int nsrc, ndst;
+  int div;                   // > 0: this op's result is divided by div (AVG, reading AV1)
 };
+
+// AVG (reading AV1): the fp32 sum of a final reduce is divided by N with one correctly
+// rounded IEEE division before the store's rounding.
+__device__ __forceinline__ void acc_div(float (&acc)[8], float d) {
+#pragma unroll
+  for (int i = 0; i < 8; i++) acc[i] = __fdiv_rn(acc[i], d);
+}
 
 // Vector body, NSRC sources known at compile time (1 = copy).  UNROLL vectors per thread
 // per iteration, all loads issued before any add (memory-level parallelism).
@@ -194,6 +205,7 @@ __device__ __noinline__ void body_fixed(const OpShared &s, size_t v0, size_t v1)
           acc_first<BF16>(acc, x[u][0]);
 #pragma unroll
           for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[u][k]);
+          if (s.div) acc_div(acc, (float)s.div);
           o = acc_pack<BF16>(acc);
         }
         for (int d = 0; d < ndst; d++) st_v4(s.dst[d] + v, o);
@@ -220,6 +232,7 @@ __device__ __noinline__ void body_generic(const OpShared &s, size_t v0, size_t v
         else acc_add<BF16>(acc, x[k]);
       }
     }
+    if (s.div) acc_div(acc, (float)s.div);
     uint4 o = acc_pack<BF16>(acc);
     for (int d = 0; d < s.ndst; d++) st_v4(s.dst[d] + v, o);
   }
@@ -227,6 +240,10 @@ __device__ __noinline__ void body_generic(const OpShared &s, size_t v0, size_t v
 
 template <bool BF16>
 __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
+  if (s.div && s.nsrc == 1) {
+    body_generic<BF16>(s, v0, v1);
+    return;
+  }
   switch (s.nsrc) {
     case 1: body_fixed<1, 4, BF16>(s, v0, v1); break;
     case 2: body_fixed<2, 2, BF16>(s, v0, v1); break;
@@ -344,6 +361,7 @@ __device__ __noinline__ void body_bulk(const OpShared &s, size_t v0, size_t v1, 
           acc_first<BF16>(acc, x[0]);
 #pragma unroll
           for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[k]);
+          if (s.div) acc_div(acc, (float)s.div);
           o = acc_pack<BF16>(acc);
         }
         for (int d = 0; d < ndst; d++) st_v4(s.dst[d] + t0 + v, o);
@@ -417,6 +435,7 @@ __device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v
           acc_first<BF16>(acc, x[0]);
 #pragma unroll
           for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[k]);
+          if (s.div) acc_div(acc, (float)s.div);
           o[v] = acc_pack<BF16>(acc);
         }
         consumer_bar(nthr);     // output tile complete, input stage fully read
@@ -447,6 +466,10 @@ __device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v
 template <bool BF16>
 __device__ void body_dispatch_bulk_st(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
                                       Pipe &pp) {
+  if (s.div && s.nsrc == 1) {
+    body_generic<BF16>(s, v0, v1);
+    return;
+  }
   switch (s.nsrc) {
     case 1: body_bulk_st<1, BF16>(s, v0, v1, g, smem, pp); break;
     case 2: body_bulk_st<2, BF16>(s, v0, v1, g, smem, pp); break;
@@ -462,6 +485,10 @@ __device__ void body_dispatch_bulk_st(const OpShared &s, size_t v0, size_t v1, u
 
 template <bool BF16>
 __device__ void body_dispatch_bulk(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem, Pipe &pp) {
+  if (s.div && s.nsrc == 1) {
+    body_generic<BF16>(s, v0, v1);
+    return;
+  }
   switch (s.nsrc) {
     case 1: body_bulk<1, BF16>(s, v0, v1, g, smem, pp); break;
     case 2: body_bulk<2, BF16>(s, v0, v1, g, smem, pp); break;
@@ -482,7 +509,7 @@ __device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, 
     if (bf16) {
       const unsigned short *p0 = (const unsigned short *)(a.bufs[src_ranks[0]]) + e;
       unsigned short out;
-      if (s.nsrc == 1) {
+      if (s.nsrc == 1 && !s.div) {
         out = *(volatile const unsigned short *)p0;
       } else {
         float acc = __uint_as_float((uint32_t)(*(volatile const unsigned short *)p0) << 16);
@@ -490,13 +517,14 @@ __device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, 
           const unsigned short *pk = (const unsigned short *)(a.bufs[src_ranks[k]]) + e;
           acc = __fadd_rn(acc, __uint_as_float((uint32_t)(*(volatile const unsigned short *)pk) << 16));
         }
+        if (s.div) acc = __fdiv_rn(acc, (float)s.div);
         out = (unsigned short)f2bf(acc);
       }
       for (int d = 0; d < s.ndst; d++) ((unsigned short *)(a.bufs[dst_ranks[d]]))[e] = out;
     } else {
       const uint32_t *p0 = (const uint32_t *)(a.bufs[src_ranks[0]]) + e;
       uint32_t out;
-      if (s.nsrc == 1) {
+      if (s.nsrc == 1 && !s.div) {
         out = *(volatile const uint32_t *)p0;
       } else {
         float acc = __uint_as_float(*(volatile const uint32_t *)p0);
@@ -504,6 +532,7 @@ __device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, 
           const uint32_t *pk = (const uint32_t *)(a.bufs[src_ranks[k]]) + e;
           acc = __fadd_rn(acc, __uint_as_float(*(volatile const uint32_t *)pk));
         }
+        if (s.div) acc = __fdiv_rn(acc, (float)s.div);
         out = __float_as_uint(acc);
       }
       for (int d = 0; d < s.ndst; d++) ((uint32_t *)(a.bufs[dst_ranks[d]]))[e] = out;
@@ -609,7 +638,11 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       __syncthreads();
       if (threadIdx.x < op.nsrc) sh.src[threadIdx.x] = (const uint4 *)a.bufs[sr[threadIdx.x]];
       if (threadIdx.x < op.ndst) sh.dst[threadIdx.x] = (uint4 *)a.bufs[dr[threadIdx.x]];
-      if (threadIdx.x == 0) { sh.nsrc = op.nsrc; sh.ndst = op.ndst; }
+      if (threadIdx.x == 0) {
+        sh.nsrc = op.nsrc;
+        sh.ndst = op.ndst;
+        sh.div = op.fin ? a.avg_n : 0;
+      }
       __syncthreads();
       if (vb >= ve) {
         if (cta == 0) scalar_elems(sh, a, sr, dr, op.off, op.off + op.len, bf16);
@@ -841,6 +874,7 @@ static void base_of(void *p, char **base, size_t *size) {
 struct HostOp {
   long long off, len;
   std::vector<int> src, dst;
+  bool fin = false;          // last RS op writing this region (reading AV1)
 };
 struct Access {
   int step, rank;              // executing rank
@@ -865,6 +899,10 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
   if (S + 1 > kMaxSlots) throw InvalidArg("plan has too many steps");
   // ops[step][rank]
   std::vector<std::vector<std::vector<HostOp>>> H(S, std::vector<std::vector<HostOp>>(n));
+  std::vector<int> last_rs(n, -1);   // block -> last RS step with a Reduce writing it
+  for (int s = 0; s < S; s++)
+    if (!p.steps[s].ag)
+      for (auto &rd : p.steps[s].reduces) last_rs[rd.block] = s;
   for (int s = 0; s < S; s++) {
     const Step &st = p.steps[s];
     if (!st.ag) {
@@ -876,8 +914,10 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
           long long off = block_offset(p.count, n, rd->block), len = block_size(p.count, n, rd->block);
           if (len == 0) continue;
           auto &v = H[s][r];
-          if (!v.empty() && v.back().off + v.back().len == off && v.back().src == rd->inputs) v.back().len += len;
-          else v.push_back({off, len, rd->inputs, {r}});
+          const bool fin = last_rs[rd->block] == s;
+          if (!v.empty() && v.back().off + v.back().len == off && v.back().src == rd->inputs && v.back().fin == fin)
+            v.back().len += len;
+          else v.push_back({off, len, rd->inputs, {r}, fin});
         }
       }
     } else {
@@ -891,7 +931,7 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
           if (len == 0) continue;
           auto &v = H[s][r];
           if (!v.empty() && v.back().off + v.back().len == off && v.back().dst == d) v.back().len += len;
-          else v.push_back({off, len, {r}, d});
+          else v.push_back({off, len, {r}, d, false});
         }
     }
   }
@@ -1000,6 +1040,7 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
           x.len = o.len;
           x.nsrc = (int)o.src.size();
           x.ndst = (int)o.dst.size();
+          x.fin = o.fin ? 1 : 0;
           x.src_begin = (int)ranks.size();
           ranks.insert(ranks.end(), o.src.begin(), o.src.end());
           x.dst_begin = (int)ranks.size();
@@ -1444,7 +1485,7 @@ int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *ne
           for (int j = 0; j < x.nsrc; j++) o += (j ? "," : "") + std::to_string(rk[x.src_begin + j]);
           o += "],\"dst\":[";
           for (int j = 0; j < x.ndst; j++) o += (j ? "," : "") + std::to_string(rk[x.dst_begin + j]);
-          o += "]}";
+          o += "],\"fin\":" + std::to_string(x.fin) + "}";
         }
         o += "],\"waits\":[";
         for (int k = 0; k < d.wait_count; k++) {
@@ -1467,8 +1508,11 @@ int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *ne
   })
 }
 
-static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream) {
+static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream,
+                     int op = AR_OP_SUM) {
   if (!plan || !c || !dptr) throw InvalidArg("null argument");
+  if (op != AR_OP_SUM && op != AR_OP_AVG) throw InvalidArg("unknown reduction op");
+  const int avg_n = op == AR_OP_AVG ? plan->plan.n : 0;
   if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");
   if ((uint64_t)plan->plan.count != count || plan->dtype != dtype) throw InvalidArg("count/dtype differ from the plan's");
   if ((uintptr_t)dptr % 16) throw InvalidArg("buffer must be 16-byte aligned");
@@ -1479,6 +1523,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   if (c->fast_valid && c->fast_uid == plan->uid && c->fast_dptr == dptr && c->fast_nctas == c->nctas) {
     // steady state: same plan and buffer as the previous call — launch the cached arguments
     ++c->epoch;
+    c->fast_args.avg_n = avg_n;
     void *args[] = {&c->fast_args};
     CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
                                         c->bulk ? dyn_smem_bytes(c->stages, c->stage_bytes) : 0, (cudaStream_t)stream));
@@ -1548,6 +1593,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.stages = c->stages;
   a.stage_bytes = c->stage_bytes;
   a.jitter_ns = c->jitter_ns;
+  a.avg_n = avg_n;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;
@@ -1562,6 +1608,11 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
 
 int allreduce_exec(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream) {
   SYS_TRY({ return exec_impl(plan, c, dptr, count, dtype, stream); })
+}
+
+int allreduce_exec_op(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, int32_t op,
+                      void *stream) {
+  SYS_TRY({ return exec_impl(plan, c, dptr, count, dtype, stream, op); })
 }
 
 int allreduce_exec_host(const gt_plan *plan, ar_comm *c, void *dptr, void *host, uint64_t count, int32_t dtype,

@@ -51,12 +51,14 @@ def main():
                 plan = G.Plan.from_topology(doc, count, dtype, None, force)
                 oplan, _ = GT.gentree(topo, count, es, force=force)
                 assert plan.to_json() == OP.plan_to_json(oplan, dtype)
-                for _ in range(2):
-                    G.allreduce_exec(plan, comm, buf)
+                # second call: AVG on ring/default plans (reading AV1), SUM otherwise
+                op2 = "avg" if force in (None, "ring") else "sum"
+                G.allreduce_exec(plan, comm, buf)
+                G.allreduce_exec(plan, comm, buf, op=op2)
                 torch.cuda.synchronize()
                 comm.async_error()
                 xs = GEN.generate_all(seed, world, count, dtype)
-                want = SM.simulate(oplan, SM.simulate(oplan, xs, dtype), dtype)[rank]
+                want = SM.simulate(oplan, SM.simulate(oplan, xs, dtype), dtype, op=op2)[rank]
                 got = buf.cpu().numpy()[: count * es].view(np.float32 if dtype == "f32" else np.uint16)
                 try:
                     assert_bits_equal(got, want, dtype, f"rank {rank} {dtype} count={count} plan={force}")

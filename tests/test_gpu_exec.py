@@ -60,7 +60,7 @@ def test_device_generator_matches_numpy(dtype, mode):
         assert np.array_equal(got, want)
 
 
-def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1):
+def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1, op="sum"):
     plan = G.Plan.from_topology(doc, count, dtype, params, force)
     comm = G.Comm.local(world, 0)
     if ctas:
@@ -77,8 +77,8 @@ def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=N
     assert plan.to_json() == OP.plan_to_json(oplan, dtype)
     want = inputs
     for _ in range(calls):
-        G.allreduce_exec(plan, comm, buf)
-        want = SM.simulate(oplan, want, dtype)
+        G.allreduce_exec(plan, comm, buf, op=op)
+        want = SM.simulate(oplan, want, dtype, op=op)
     torch.cuda.synchronize()
     comm.async_error()
     got = rank_views(buf, world, count, dtype, stride)
@@ -191,6 +191,24 @@ def test_jitter_injection(force, monkeypatch):
     or ordering bug then shows up as a non-bit-exact result."""
     monkeypatch.setenv("AR_JITTER_NS", "20000")
     run_emulated(single_switch(8), 8, 300007, "bf16", force=force, calls=3)
+
+
+@pytest.mark.parametrize("force", ["cps", "ring", "rhd", "rb", "hcps:3,2", "hcps:2,3", None])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_avg_op(force, dtype):
+    """AR_OP_AVG (NEXT #4, reading AV1): fused division in the final reduce, bit-exact vs the
+    oracle, ragged sizes, alternating with SUM on the same plan (cached launch arguments)."""
+    world = 6 if force != "rhd" else 8
+    for count in (world - 1, 4096 * world + 5, 200003):
+        run_emulated(single_switch(world), world, count, dtype, force=force, op="avg", calls=2)
+        run_emulated(single_switch(world), world, count, dtype, force=force, op="sum")
+
+
+def test_avg_rearrangement_and_c5():
+    from tests.topologies import cross_dc
+    run_emulated(cross_dc(2, 4, 2, 2), 12, 77777, "bf16", op="avg")
+    doc = T.two_level_doc([8] * 8, T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    run_emulated(doc, 64, 64 * 1000 + 17, "bf16", op="avg")
 
 
 @pytest.mark.parametrize("ctas", [1, 3, 17])

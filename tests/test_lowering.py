@@ -42,7 +42,8 @@ def cta_elems(off, len_, esize, k, C):
     return e0, e1
 
 
-def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random, esize: int = 4) -> list:
+def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random, esize: int = 4,
+              avg: bool = False) -> list:
     n = len(low["ranks"])
     bufs = [x.astype(np.float32).copy() for x in inputs]
     flags = {}                                  # (consumer, slot, producer, cta) -> epoch
@@ -85,6 +86,8 @@ def interpret(low: dict, inputs: list, ctas: int, calls: int, rnd: random.Random
             acc = bufs[op["src"][0]][lo:hi].copy()
             for q in op["src"][1:]:
                 acc = acc + bufs[q][lo:hi]
+            if avg and op["fin"]:
+                acc = acc / np.float32(n)
             for d in op["dst"]:
                 bufs[d][lo:hi] = acc
         for consumer in st["notify"]:
@@ -149,3 +152,20 @@ def test_cps_is_one_fused_step_with_two_flag_rounds():
 def test_lowering_rejects_bad_buffer_query():
     plan = G.Plan.from_topology(single_switch(2), 10, "f32")
     assert plan.lowering()["ranks"][1]["steps"]
+
+
+@pytest.mark.parametrize("doc,world,force", [c for c in CASES if c[2] in ("ring", "hcps:3,2", "rb", None)])
+def test_lowered_avg_divides_once_at_the_final_reduce(doc, world, force):
+    """AR_OP_AVG (reading AV1): the lowering's `fin` ops are exactly the plan's last RS
+    reduces of each block (the interpreter divides there) — two AVG calls match the oracle."""
+    count = 29 * world + 3
+    plan = G.Plan.from_topology(doc, count, "f32", None, force)
+    low = plan.lowering()
+    oplan, _ = GT.gentree(T.parse_topology(doc), count, 4, force=force)
+    xs = [(GEN.generate(5, r, count, "f32", "gradient")) for r in range(world)]
+    want = SM.simulate(oplan, SM.simulate(oplan, xs, "f32", op="avg"), "f32", op="avg")
+    rnd = random.Random(world * 7 + 1)
+    for trial in range(3):
+        got = interpret(low, xs, ctas=rnd.choice([1, 2, 3]), calls=2, rnd=rnd, avg=True)
+        for r in range(world):
+            assert np.array_equal(got[r].view(np.uint32), want[r].view(np.uint32)), (force, trial, r)

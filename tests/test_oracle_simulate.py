@@ -207,3 +207,59 @@ def test_generator_properties():
     assert np.all(np.abs(f) <= 2.0 ** -7)
     ints = GEN.generate(9, 0, 5000, "f32", "integer")
     assert np.all(ints == np.round(ints)) and np.abs(ints).max() <= 1024
+
+
+# ---------------------------------------------------------------- AVG (NEXT #4, reading AV1)
+
+AVG_CASES = [("cps", 4), ("cps", 3), ("ring", 3), ("ring", 5), ("rhd", 4), ("rhd", 3), ("rb", 4),
+             ("hcps:2,2", 4), ("hcps:3,2", 6)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("kind,n", AVG_CASES)
+def test_avg_numpy_equals_scalar_bruteforce(kind, n, dtype):
+    count = 40 + n - 1
+    xs = GEN.generate_all(13, n, count, dtype, "gradient")
+    plan = P.build_plan(kind, n, count)
+    a = SM.simulate(plan, xs, dtype, op="avg")
+    b = SM.simulate_scalar(plan, xs, dtype, op="avg")
+    for r in range(n):
+        va = a[r].view(np.uint32) if dtype == "f32" else a[r]
+        vb = b[r].view(np.uint32) if dtype == "f32" else b[r]
+        assert np.array_equal(va, vb)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("kind,n", AVG_CASES)
+def test_avg_of_identical_inputs_is_the_input(kind, n, dtype):
+    """The mean of N equal integer values is that value, exactly, on every rank."""
+    count = 50 + n
+    x = GEN.generate_all(17, 1, count, dtype, "integer")[0]
+    out = SM.simulate(P.build_plan(kind, n, count), [x.copy() for _ in range(n)], dtype, op="avg")
+    for r in range(n):
+        assert np.array_equal(out[r], x)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", KINDS8)
+def test_avg_pow2_is_sum_scaled_once(kind, dtype):
+    """N = 8: division by 2^3 is exact and commutes with RNE (no under/overflow here), so the
+    AVG result is the SUM result times 1/8 — dividing twice or never would fail."""
+    n, count = 8, 333
+    xs = GEN.generate_all(19, n, count, dtype, "gradient")
+    plan = P.build_plan(kind, n, count)
+    s = SM.simulate(plan, xs, dtype)
+    a = SM.simulate(plan, xs, dtype, op="avg")
+    for r in range(n):
+        assert np.array_equal(GEN.as_f64(a[r], dtype), GEN.as_f64(s[r], dtype) / 8)
+
+
+def test_avg_simulate_at_matches_simulate():
+    n, count = 5, 1001
+    xs = GEN.generate_all(23, n, count, "bf16", "gradient")
+    plan = P.build_plan("ring", n, count)
+    full = SM.simulate(plan, xs, "bf16", op="avg")
+    idx = np.array([0, 1, 199, 200, 201, 600, 1000])
+    part = SM.simulate_at(plan, idx, [x[idx] for x in xs], "bf16", op="avg")
+    for r in range(n):
+        assert np.array_equal(part[r], full[r][idx])
