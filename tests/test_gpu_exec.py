@@ -60,7 +60,7 @@ def test_device_generator_matches_numpy(dtype, mode):
         assert np.array_equal(got, want)
 
 
-def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1, op="sum"):
+def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1, red="sum"):
     plan = G.Plan.from_topology(doc, count, dtype, params, force)
     comm = G.Comm.local(world, 0)
     if ctas:
@@ -77,8 +77,8 @@ def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=N
     assert plan.to_json() == OP.plan_to_json(oplan, dtype)
     want = inputs
     for _ in range(calls):
-        G.allreduce_exec(plan, comm, buf, op=op)
-        want = SM.simulate(oplan, want, dtype, op=op)
+        G.allreduce_exec(plan, comm, buf, op=red)
+        want = SM.simulate(oplan, want, dtype, op=red)
     torch.cuda.synchronize()
     comm.async_error()
     got = rank_views(buf, world, count, dtype, stride)
@@ -200,15 +200,15 @@ def test_avg_op(force, dtype):
     oracle, ragged sizes, alternating with SUM on the same plan (cached launch arguments)."""
     world = 6 if force != "rhd" else 8
     for count in (world - 1, 4096 * world + 5, 200003):
-        run_emulated(single_switch(world), world, count, dtype, force=force, op="avg", calls=2)
-        run_emulated(single_switch(world), world, count, dtype, force=force, op="sum")
+        run_emulated(single_switch(world), world, count, dtype, force=force, red="avg", calls=2)
+        run_emulated(single_switch(world), world, count, dtype, force=force, red="sum")
 
 
 def test_avg_rearrangement_and_c5():
     from tests.topologies import cross_dc
-    run_emulated(cross_dc(2, 4, 2, 2), 12, 77777, "bf16", op="avg")
+    run_emulated(cross_dc(2, 4, 2, 2), 12, 77777, "bf16", red="avg")
     doc = T.two_level_doc([8] * 8, T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
-    run_emulated(doc, 64, 64 * 1000 + 17, "bf16", op="avg")
+    run_emulated(doc, 64, 64 * 1000 + 17, "bf16", red="avg")
 
 
 @pytest.mark.parametrize("ctas", [1, 3, 17])
