@@ -159,6 +159,18 @@ typedef struct ar_comm ar_comm; /* opaque; one per process and device; single-th
  * rank/world, AR_ESYS on CUDA failure. */
 int ar_comm_create(int32_t rank, int32_t world, int32_t cuda_device, ar_comm **out);
 
+/* Multi-level execution (SURVEY §8(f) NEXT #3, config C5's "8 ranks/GPU" across GPUs):
+ * process `proc` of `nproc` hosts the ranks_per_proc consecutive ranks
+ * proc·ranks_per_proc … proc·ranks_per_proc + ranks_per_proc − 1 of a world of
+ * nproc·ranks_per_proc ranks on `cuda_device`.  Its registered buffer holds those ranks'
+ * buffers at ar_rank_stride_bytes(count, dtype) apart (as for an emulated comm); peers'
+ * buffers are IPC-mapped, so a plan's leaf levels move data inside HBM and its upper levels
+ * over NVLink, all in one cooperative launch per process.  ar_comm_register / open_peers
+ * exchange one blob per process (blobs = nproc × AR_BLOB_BYTES, process order).
+ * ranks_per_proc = 1 is ar_comm_create(proc, nproc, ...).  Errors: AR_EINVAL for bad
+ * arguments, nproc == 1 (use ar_comm_create_local) or world > AR_MAX_RANKS. */
+int ar_comm_create_multi(int32_t proc, int32_t nproc, int32_t ranks_per_proc, int32_t cuda_device, ar_comm **out);
+
 /* Emulated communicator: all `world` ranks live in this process on one device (each rank's
  * buffer is a separate region of device memory; "8 ranks/GPU" of config C5).  The executor
  * runs all ranks in one cooperative launch, with the same step tables and flag protocol. */
@@ -175,7 +187,8 @@ int ar_comm_set_ctas(ar_comm *comm, int32_t ctas);
  * Not used by emulated communicators. */
 int ar_comm_register(ar_comm *comm, void *dptr, size_t bytes, void *blob_out);
 /* Map every peer's registered buffer (and flag page, first time) into this process.
- * blobs = world * AR_BLOB_BYTES, rank order, from ar_comm_register on every rank for the
+ * blobs = nproc * AR_BLOB_BYTES (= world * AR_BLOB_BYTES for ar_comm_create), process
+ * order, from ar_comm_register on every process for the
  * same logical buffer (same size).  Collective: call on all ranks before the first
  * allreduce_exec on that buffer. */
 int ar_comm_open_peers(ar_comm *comm, const void *blobs);

@@ -176,15 +176,25 @@ def _ptr(x) -> int:
 class Comm:
     """Communicator (opaque ar_comm*)."""
 
-    def __init__(self, handle, world: int, rank: int, local: bool, device: int):
+    def __init__(self, handle, world: int, rank: int, local: bool, device: int, nproc: int | None = None,
+                 ranks_per_proc: int = 1):
         self._h = handle
         self.world, self.rank, self.local, self.device = world, rank, local, device
+        self.ranks_per_proc = ranks_per_proc
+        self.nproc = world // ranks_per_proc if nproc is None else nproc
 
     @classmethod
     def create(cls, rank: int, world: int, device: int) -> "Comm":
         h = ctypes.c_void_p()
         check(lib.ar_comm_create(rank, world, device, ctypes.byref(h)))
         return cls(h, world, rank, False, device)
+
+    @classmethod
+    def create_multi(cls, proc: int, nproc: int, ranks_per_proc: int, device: int) -> "Comm":
+        """ranks_per_proc consecutive ranks per process (ar_comm_create_multi; NEXT #3)."""
+        h = ctypes.c_void_p()
+        check(lib.ar_comm_create_multi(proc, nproc, ranks_per_proc, device, ctypes.byref(h)))
+        return cls(h, nproc * ranks_per_proc, proc * ranks_per_proc, False, device, nproc, ranks_per_proc)
 
     @classmethod
     def local(cls, world: int, device: int = 0) -> "Comm":
@@ -208,7 +218,7 @@ class Comm:
         return blob.raw
 
     def open_peers(self, blobs: list):
-        assert len(blobs) == self.world
+        assert len(blobs) == self.nproc
         data = b"".join(blobs)
         check(lib.ar_comm_open_peers(self._h, data))
 
@@ -216,7 +226,7 @@ class Comm:
         """Collective over torch.distributed: export + all_gather_object + open_peers."""
         import torch.distributed as dist
         blob = self.export(tensor)
-        blobs = [None] * self.world
+        blobs = [None] * self.nproc
         dist.all_gather_object(blobs, blob, group=group)
         self.open_peers(blobs)
 

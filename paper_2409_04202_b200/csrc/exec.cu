@@ -796,7 +796,7 @@ struct SysError : std::runtime_error {
 struct Registration {
   char *local = nullptr;
   size_t bytes = 0;
-  std::vector<char *> peer;   // rank -> mapped pointer (own = local)
+  std::vector<char *> peer;   // process -> mapped pointer (own = local)
   bool opened = false;
 };
 
@@ -813,8 +813,10 @@ struct Lowered {
 }  // namespace
 
 struct ar_comm {
-  int rank = 0, world = 0, device = 0;
+  int rank = 0, world = 0, device = 0;         // rank = first rank hosted by this process
   bool local = false;
+  int rpp = 1;                                 // ranks hosted by this process (grid.y)
+  int proc = 0, nproc = 1;                     // process index / count (multi-process comms)
   int nctas = 0, cta_cap = 0, max_ctas = 0;
   unsigned long long epoch = 0;
   size_t page_elems = 0;                       // uint64 per flag page
@@ -1131,27 +1133,23 @@ static void init_comm(ar_comm *c) {
   int nsm = 0;
   CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
   c->max_ctas = resident_ctas(c->device);
-  if (c->local) {
-    c->cta_cap = std::max(1, c->max_ctas / c->world);
+  if (c->rpp > 1) {   // emulated, or several ranks per process: the SMs are shared
+    c->cta_cap = std::max(1, c->max_ctas / c->rpp);
     c->nctas = c->cta_cap;
   } else {
     c->cta_cap = kCtaCapMulti;
     c->nctas = std::min(nsm, kCtaCapMulti);
   }
   c->page_elems = (size_t)kMaxSlots * c->world * c->cta_cap;
-  const size_t pages = c->local ? c->world : 1;
+  const size_t pages = c->rpp;
   CUDA_OK(cudaMalloc(&c->sig_local, pages * c->page_elems * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->sig_local, 0, pages * c->page_elems * sizeof(unsigned long long)));
   // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter
   CUDA_OK(cudaMalloc(&c->err, 4 * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->err, 0, 4 * sizeof(unsigned long long)));
   c->sig.assign(c->world, nullptr);
-  if (c->local) {
-    for (int r = 0; r < c->world; r++) c->sig[r] = c->sig_local + (size_t)r * c->page_elems;
-    c->sig_opened = true;
-  } else {
-    c->sig[c->rank] = c->sig_local;
-  }
+  for (int i = 0; i < c->rpp; i++) c->sig[c->rank + i] = c->sig_local + (size_t)i * c->page_elems;
+  if (c->local) c->sig_opened = true;
   if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) c->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
   if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
   if (const char *f = std::getenv("AR_FENCE_MODE")) c->fence_mode = std::atoi(f);
@@ -1185,12 +1183,22 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype) {
 }
 
 int ar_comm_create(int32_t rank, int32_t world, int32_t cuda_device, ar_comm **out) {
+  return ar_comm_create_multi(rank, world, 1, cuda_device, out);
+}
+
+int ar_comm_create_multi(int32_t proc, int32_t nproc, int32_t ranks_per_proc, int32_t cuda_device, ar_comm **out) {
   SYS_TRY({
     if (!out) throw InvalidArg("null out");
-    if (world < 2 || world > AR_MAX_RANKS || rank < 0 || rank >= world) throw InvalidArg("bad rank/world");
+    const long long world = (long long)nproc * ranks_per_proc;
+    if (nproc < 1 || ranks_per_proc < 1 || world < 2 || world > AR_MAX_RANKS || proc < 0 || proc >= nproc)
+      throw InvalidArg("bad proc/nproc/ranks_per_proc");
+    if (nproc == 1) throw InvalidArg("one process: use ar_comm_create_local");
     ar_comm *c = new ar_comm();
-    c->rank = rank;
-    c->world = world;
+    c->rank = proc * ranks_per_proc;
+    c->world = (int)world;
+    c->rpp = ranks_per_proc;
+    c->proc = proc;
+    c->nproc = nproc;
     c->device = cuda_device;
     try {
       init_comm(c);
@@ -1210,6 +1218,7 @@ int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out) {
     ar_comm *c = new ar_comm();
     c->rank = 0;
     c->world = world;
+    c->rpp = world;
     c->device = cuda_device;
     c->local = true;
     try {
@@ -1230,10 +1239,10 @@ int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out) {
 int ar_comm_set_ctas(ar_comm *c, int32_t ctas) {
   SYS_TRY({
     if (!c) throw InvalidArg("null comm");
-    int want = ctas > 0 ? ctas : (c->local ? c->cta_cap : std::min(c->max_ctas, kCtaCapMulti));
+    int want = ctas > 0 ? ctas : (c->rpp > 1 ? c->cta_cap : std::min(c->max_ctas, kCtaCapMulti));
     if (want > c->cta_cap) throw InvalidArg("ctas exceeds the flag page capacity");
-    if ((long long)want * (c->local ? c->world : 1) > c->max_ctas) throw InvalidArg("ctas exceeds resident capacity");
-    if (ctas <= 0 && !c->local) {
+    if ((long long)want * c->rpp > c->max_ctas) throw InvalidArg("ctas exceeds resident capacity");
+    if (ctas <= 0 && c->rpp == 1) {
       int nsm = 0;
       CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
       want = std::min(nsm, kCtaCapMulti);
@@ -1256,7 +1265,7 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     Blob b{};
     b.magic = kBlobMagic;
     b.version = 1;
-    b.rank = c->rank;
+    b.rank = c->proc;
     b.world = c->world;
     b.bytes = bytes;
     b.offset = (uint64_t)((char *)dptr - base);
@@ -1267,8 +1276,8 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     Registration reg;
     reg.local = (char *)dptr;
     reg.bytes = bytes;
-    reg.peer.assign(c->world, nullptr);
-    reg.peer[c->rank] = (char *)dptr;
+    reg.peer.assign(c->nproc, nullptr);
+    reg.peer[c->proc] = (char *)dptr;
     for (auto it = c->regs.begin(); it != c->regs.end(); ++it)
       if (it->local == reg.local) { c->regs.erase(it); break; }
     c->regs.push_back(reg);
@@ -1283,7 +1292,7 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
     if (c->local) throw InvalidArg("emulated communicators need no peers");
     CUDA_OK(cudaSetDevice(c->device));
     const char *bb = (const char *)blobs;
-    const Blob *mine = (const Blob *)(bb + (size_t)c->rank * AR_BLOB_BYTES);
+    const Blob *mine = (const Blob *)(bb + (size_t)c->proc * AR_BLOB_BYTES);
     Registration *reg = nullptr;
     for (auto &r : c->regs)
       if ((uint64_t)r.bytes == mine->bytes) reg = &r;
@@ -1291,11 +1300,11 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
     for (auto it = c->regs.rbegin(); it != c->regs.rend(); ++it)
       if ((uint64_t)it->bytes == mine->bytes) { reg = &*it; break; }
     if (!reg) throw InvalidArg("no local registration matches the blobs");
-    for (int t = 0; t < c->world; t++) {
+    for (int t = 0; t < c->nproc; t++) {   // one blob per process
       const Blob *b = (const Blob *)(bb + (size_t)t * AR_BLOB_BYTES);
       if (b->magic != kBlobMagic || b->world != c->world || b->rank != t) throw InvalidArg("corrupt or misordered blob");
       if (b->bytes != mine->bytes) throw InvalidArg("ranks registered buffers of different sizes");
-      if (t == c->rank) continue;
+      if (t == c->proc) continue;
       auto open = [&](const cudaIpcMemHandle_t &h) -> char * {
         std::string key((const char *)&h, sizeof h);
         key += std::to_string(t);
@@ -1307,7 +1316,12 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
         return (char *)p;
       };
       reg->peer[t] = open(b->data) + b->offset;
-      if (!c->sig[t]) c->sig[t] = (unsigned long long *)open(b->sig);
+      unsigned long long *pages = nullptr;
+      for (int i = 0; i < c->rpp; i++)
+        if (!c->sig[t * c->rpp + i]) {
+          if (!pages) pages = (unsigned long long *)open(b->sig);
+          c->sig[t * c->rpp + i] = pages + (size_t)i * c->page_elems;
+        }
     }
     reg->opened = true;
     c->fast_valid = false;
@@ -1437,7 +1451,7 @@ int ar_comm_set_trace(ar_comm *c, int32_t enable) {
       c->trace_elems = 0;
     }
     if (enable) {
-      c->trace_elems = (size_t)(c->local ? c->world : 1) * c->cta_cap * kTraceSlots;
+      c->trace_elems = (size_t)c->rpp * c->cta_cap * kTraceSlots;
       CUDA_OK(cudaMalloc(&c->trace, c->trace_elems * sizeof(unsigned long long)));
       CUDA_OK(cudaMemset(c->trace, 0, c->trace_elems * sizeof(unsigned long long)));
     }
@@ -1451,7 +1465,7 @@ int ar_comm_read_trace(ar_comm *c, uint64_t *out, size_t cap, size_t *n, int32_t
   SYS_TRY({
     if (!c) throw InvalidArg("null comm");
     if (!c->trace) throw InvalidArg("tracing is off (ar_comm_set_trace)");
-    const size_t used = (size_t)(c->local ? c->world : 1) * c->cta_cap * kTraceSlots;
+    const size_t used = (size_t)c->rpp * c->cta_cap * kTraceSlots;
     if (n) *n = used;
     if (slots_per_cta) *slots_per_cta = kTraceSlots;
     if (ctas_per_rank) *ctas_per_rank = c->cta_cap;
@@ -1519,7 +1533,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   int cur = -1;
   CUDA_OK(cudaGetDevice(&cur));
   if (cur != c->device) CUDA_OK(cudaSetDevice(c->device));
-  dim3 grid(c->nctas, c->local ? c->world : 1);
+  dim3 grid(c->nctas, c->rpp);
   if (c->fast_valid && c->fast_uid == plan->uid && c->fast_dptr == dptr && c->fast_nctas == c->nctas) {
     // steady state: same plan and buffer as the previous call — launch the cached arguments
     ++c->epoch;
@@ -1539,12 +1553,16 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       a.sigs[r] = c->sig[r];
     }
   } else {
+    // several ranks per process: consecutive rank buffers at the emulated stride
+    const uint64_t stride = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) : 0;
+    const size_t need = c->rpp > 1 ? stride * c->rpp : bytes;
     Registration *reg = nullptr;
     for (auto &r : c->regs)
-      if (r.local == (char *)dptr && r.opened && r.bytes >= bytes) reg = &r;
-    if (!reg) throw InvalidArg("buffer is not registered and opened on this communicator");
+      if (r.local == (char *)dptr && r.opened && r.bytes >= need) reg = &r;
+    if (!reg) throw InvalidArg("buffer is not registered and opened on this communicator (or too small)");
     for (int r = 0; r < c->world; r++) {
-      a.bufs[r] = reg->peer[r];
+      char *base = reg->peer[r / c->rpp];
+      a.bufs[r] = base ? base + stride * (r % c->rpp) : nullptr;
       a.sigs[r] = c->sig[r];
       if (!a.bufs[r] || !a.sigs[r]) throw InvalidArg("peer buffer not opened");
     }
@@ -1557,8 +1575,9 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     std::vector<int> rk, pb, pl;
     lower_plan(plan->plan, c->world, st, ops, w, rk, pb, pl);
     Lowered L;
-    if (!c->local) {  // this process runs only its own rank's program
-      std::vector<int> pb1{pb[c->rank]}, pl1{pl[c->rank]};
+    if (!c->local) {  // this process runs only the programs of the ranks it hosts
+      std::vector<int> pb1(pb.begin() + c->rank, pb.begin() + c->rank + c->rpp);
+      std::vector<int> pl1(pl.begin() + c->rank, pl.begin() + c->rank + c->rpp);
       pb = pb1;
       pl = pl1;
     }
@@ -1621,8 +1640,8 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *c, void *dptr, void *host,
     if (!host) throw InvalidArg("null host buffer");
     if (!c) throw InvalidArg("null comm");
     CUDA_OK(cudaSetDevice(c->device));
-    const size_t bytes = c->local ? ar_rank_stride_bytes(count, dtype) * c->world
-                                  : count * (size_t)(dtype == AR_BF16 ? 2 : 4);
+    const size_t bytes = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) * c->rpp
+                                    : count * (size_t)(dtype == AR_BF16 ? 2 : 4);
     cudaStream_t s = (cudaStream_t)stream;
     CUDA_OK(cudaMemcpyAsync(dptr, host, bytes, cudaMemcpyHostToDevice, s));
     int rc = exec_impl(plan, c, dptr, count, dtype, stream);

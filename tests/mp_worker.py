@@ -29,7 +29,6 @@ def main():
     comm = G.Comm.create(rank, world, local)
     doc = T.single_switch_doc(world, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
                               {"gamma": 0.0, "delta": 4 / 6.54e12})
-    topo = T.parse_topology(doc)
     kinds = [None, "cps", "ring", "rb"]
     if world & (world - 1) == 0:
         kinds.append("rhd")
@@ -37,6 +36,15 @@ def main():
         kinds.append("hcps:2,2")
     if world == 8:
         kinds += ["hcps:4,2", "hcps:2,4", "hcps:2,2,2"]
+    cases = [(doc, k) for k in kinds]
+    # NEXT #3: multi-level trees executed across GPUs — C1's 2x2 tree on 4 GPUs (P:1034,
+    # Table 5 rows), a 2x4 tree and a rearranging cross-DC tree on 8
+    tl = lambda sizes: T.two_level_doc(sizes, T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    if world == 4:
+        cases.append((tl([2, 2]), None))
+    if world == 8:
+        from tests.topologies import cross_dc
+        cases += [(tl([4, 4]), None), (tl([3, 5]), None), (cross_dc(2, 2, 2, 2), None)]
     seed = GEN.config_seed(2)
     keep = []
     failures = 0
@@ -46,9 +54,10 @@ def main():
             buf = torch.zeros(max(16, count * es), dtype=torch.uint8, device="cuda")
             keep.append(buf)
             comm.register(buf)
-            for force in kinds:
+            for doc_i, force in cases:
+                topo = T.parse_topology(doc_i)
                 G.fill_synthetic(buf, count, dtype, seed, rank, 0)
-                plan = G.Plan.from_topology(doc, count, dtype, None, force)
+                plan = G.Plan.from_topology(doc_i, count, dtype, None, force)
                 oplan, _ = GT.gentree(topo, count, es, force=force)
                 assert plan.to_json() == OP.plan_to_json(oplan, dtype)
                 # second call: AVG on ring/default plans (reading AV1), SUM otherwise

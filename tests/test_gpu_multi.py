@@ -50,3 +50,18 @@ def test_multi_process_bit_exact(world, jitter):
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"mp_worker world={world}: OK" in r.stdout
+
+
+@pytest.mark.parametrize("world,R", [(2, 4), (2, 8), (4, 8), (8, 8)])
+def test_multi_level_ranks_per_gpu(world, R):
+    """NEXT #3: R ranks per GPU across GPUs (C5's 8 ranks/GPU; 8 x 8 = C5's 64 ranks)."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29619", os.path.join(ROOT, "tests", "mp_hybrid_worker.py"),
+           str(R)]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"hybrid_worker nproc={world} R={R}: OK" in r.stdout
