@@ -38,6 +38,26 @@ NOMINAL = {"alpha": 3e-6, "beta": 1 / 900e9, "gamma": 0.0, "delta": 1 / 6.54e12,
 SIZES = [1 << k for k in range(16, 31)]       # 64 KiB .. 1 GiB
 
 
+def tree_doc(groups, mid_link, leaf_link, compute):
+    """Topology document (SPEC format): root switch -> len(groups) middle switches -> servers."""
+    nodes = [{"id": "R", "kind": "switch", "parent": None, "uplink": None}]
+    k = 0
+    for g, cnt in enumerate(groups):
+        nodes.append({"id": f"M{g}", "kind": "switch", "parent": "R", "uplink": dict(mid_link)})
+        for _ in range(cnt):
+            nodes.append({"id": f"s{k}", "kind": "server", "parent": f"M{g}", "uplink": dict(leaf_link),
+                          "compute": dict(compute)})
+            k += 1
+    return json.dumps({"nodes": nodes})
+
+
+def flat_doc(world, link, compute):
+    nodes = [{"id": "sw", "kind": "switch", "parent": None, "uplink": None}]
+    nodes += [{"id": f"s{i}", "kind": "server", "parent": "sw", "uplink": dict(link), "compute": dict(compute)}
+              for i in range(world)]
+    return json.dumps({"nodes": nodes})
+
+
 def doc(world, p=NOMINAL):
     nodes = [{"id": "sw", "kind": "switch", "parent": None, "uplink": None}]
     for i in range(world):
@@ -339,6 +359,54 @@ def emu(args):
         comm.destroy()
 
 
+def hybrid(args):
+    """NEXT #3: R = --ranks ranks per GPU across the torchrun processes (ar_comm_create_multi);
+    plans: GenTree on the two-level tree (leaves = one GPU's ranks, root over NVLink) and
+    forced flat kinds over all N*R ranks."""
+    import torch.distributed as dist
+    proc = int(os.environ["RANK"])
+    nproc = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", proc))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    R = args.ranks
+    world = nproc * R
+    comm = G.Comm.create_multi(proc, nproc, R, local)
+    es = 4 if args.dtype == "f32" else 2
+    nvl = {"alpha": 1e-5, "beta": 4.0 / 770e9, "epsilon": 0.0, "w_t": 9}
+    hbm = {"alpha": 3e-6, "beta": 4.0 / 3000e9, "epsilon": 0.0, "w_t": 64}
+    server = {"gamma": 0.0, "delta": 4.0 / 6.5e12}
+    tree = tree_doc([R] * nproc, nvl, hbm, server)
+    flat = flat_doc(world, nvl, server)
+    timer = Timer(dist)
+    modes = args.timing.split(",")
+    sizes = args.sizes or [1 << 20, 1 << 22, 1 << 24, 1 << 26, 1 << 28]
+    for nbytes in sizes:
+        count = nbytes // es
+        stride = G.rank_stride_bytes(count, args.dtype)
+        buf = torch.empty(R * stride, dtype=torch.uint8, device="cuda")
+        comm.register(buf)
+
+        def refill():
+            for i in range(R):
+                G.fill_synthetic(buf.data_ptr() + i * stride, count, args.dtype, 11, proc * R + i, 0)
+
+        for name, d, force in (("tree", tree, None), ("cps", flat, "cps"), ("ring", flat, "ring")):
+            if name not in args.plans.split(";"):
+                continue
+            plan = G.Plan.from_topology(d, count, args.dtype, None, force)
+            for mode in modes:
+                r = timer.run(lambda: G.Executor(plan, comm, buf), reps_for(nbytes), refill, mode)
+                emit(proc, {"mode": "hybrid", "impl": "ours", "plan": name, "chosen": plan.report()[-1]["chosen"],
+                            "n": world, "gpus": nproc, "ranks_per_gpu": R, "bytes": nbytes, "dtype": args.dtype,
+                            **r, "busbw_med": busbw(nbytes, world, r["t_med"])})
+        del buf
+    comm.async_error()
+    dist.barrier()
+    comm.destroy()
+    dist.destroy_process_group()
+
+
 def fanin(args):
     """C3-i: k-way local reduce of 150M-float vectors, Eq. 6."""
     torch.cuda.set_device(0)
@@ -358,7 +426,7 @@ def fanin(args):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "p2p", "mtrace"])
+    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "p2p", "mtrace", "hybrid"])
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--plans", default="gentree;cps;ring;rhd;rb;hcps:2,2;hcps:4,2;hcps:2,4;hcps:2,2,2",
                     help="';'-separated plan kinds")
@@ -374,6 +442,8 @@ if __name__ == "__main__":
         multi(a)
     elif a.mode == "mtrace":
         mtrace(a)
+    elif a.mode == "hybrid":
+        hybrid(a)
     elif a.mode == "p2p":
         p2p(a)
     elif a.mode == "fanin":
