@@ -150,6 +150,31 @@ def nvls_fit_section(out):
                f"cells; the wrong picks are near the crossover, max regret {f['choice_max_regret'] * 100:.1f} %.\n")
 
 
+def hybrid_section(out):
+    d = os.path.join(P, "round1", "hybrid")
+    if not os.path.isdir(d):
+        return
+    out.append("## 6. Multi-level execution across GPUs (NEXT #3, C5's 8 ranks per GPU)\n")
+    out.append("R = 8 ranks per GPU (`ar_comm_create_multi`), bf16, S per rank; `tree` = GenTree on the two-level\n"
+               "tree (leaves = one GPU's ranks in HBM, root over NVLink), `cps`/`ring` = flat plans over all\n"
+               "ranks.  busbw over all N·R ranks, graph timing, median.\n")
+    out.append("| GPUs × R | S | tree (GenTree) | flat CPS | flat Ring | tree / best flat |")
+    out.append("|---|---|---|---|---|---|")
+    for f in sorted(os.listdir(d)):
+        rows = [r for r in jl(os.path.join(d, f)) if r["timing"] == "graph"]
+        t = collections.defaultdict(dict)
+        for r in rows:
+            t[r["bytes"]][r["plan"]] = r["busbw_med"]
+            g, R = r["gpus"], r["ranks_per_gpu"]
+        for b in sorted(t):
+            x = t[b]
+            best = max(x.get("cps", 0), x.get("ring", 0))
+            out.append(f"| {g} × {R} | {size(b)} | {x.get('tree', 0):.1f} | {x.get('cps', 0):.1f} | "
+                       f"{x.get('ring', 0):.1f} | {x.get('tree', 0) / max(best, 1e-9):.2f} |")
+    out.append("\nThe paper's point (§4, P:557-560) on B200: a plan that follows the hierarchy (reduce among a\n"
+               "GPU's ranks in HBM, then across GPUs over NVLink) beats any flat plan over the same ranks.\n")
+
+
 def p2p_section(out):
     out.append("## 5. Incast probe (x-to-x, S:449) on 4×B200\n")
     out.append("| pattern | bytes | GB/s per direction per GPU |")
@@ -171,6 +196,7 @@ def main():
     fit_section(out)
     nvls_fit_section(out)
     p2p_section(out)
+    hybrid_section(out)
     sys.stdout.write("\n".join(out) + "\n")
 
 
