@@ -172,6 +172,8 @@ def multi(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = G.Comm.create(rank, world, local)
+    if args.ctas:
+        comm.set_ctas(args.ctas)
     es = 4 if args.dtype == "f32" else 2
     tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
     sizes = args.sizes or SIZES
@@ -212,7 +214,7 @@ def multi(args):
             for mode in modes:
                 r = timer.run(lambda: G.Executor(plan, comm, view), reps_for(nbytes), refill, mode)
                 emit(rank, {"mode": args.mode, "impl": "ours", "plan": k, "chosen": plan.report()[-1]["chosen"],
-                            "n": world, "bytes": nbytes, "dtype": args.dtype, **r,
+                            "n": world, "bytes": nbytes, "dtype": args.dtype, "ctas": args.ctas or "auto", **r,
                             "busbw_med": busbw(nbytes, world, r["t_med"]),
                             "busbw_mean": busbw(nbytes, world, r["t_mean"])})
         if args.mode == "sweep" and not args.no_nccl:
@@ -292,6 +294,8 @@ def mtrace(args):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = G.Comm.create(rank, world, local)
+    if args.ctas:
+        comm.set_ctas(args.ctas)
     es = 4 if args.dtype == "f32" else 2
     for nbytes in args.sizes or [1 << 20]:
         count = nbytes // es
@@ -437,6 +441,7 @@ if __name__ == "__main__":
     ap.add_argument("--count", type=int, default=150_000_000)
     ap.add_argument("--kmax", type=int, default=8)
     ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--ctas", type=int, default=0, help="CTAs per rank (0 = the comm's default)")
     a = ap.parse_args()
     if a.mode in ("sweep", "cps"):
         multi(a)
