@@ -722,6 +722,128 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------ low-latency one-shot path
+// Small messages on one rank per GPU, CPS-shaped plans (one fan-in-N reduce per block, every
+// block with the same input order): every rank pushes its whole input to every peer's
+// scratch as 16-byte lines {d0, e, d1, e} (8 payload bytes + the call's epoch twice; each
+// 8-byte half is written atomically over NVLink, so a line is valid once both flags read e),
+// then computes *every* block itself in the plan's order — bit-identical to the plan (same
+// inputs, same association) — and writes only its own buffer.  No entry or exit flag round
+// trips: inputs are read only by their owner, outputs written only by their owner.  Scratch
+// is double-buffered by epoch parity: a peer that writes call e's lines has finished call
+// e-1, which consumed this rank's call e-1 lines, pushed after this rank finished call e-2.
+struct LLArgs {
+  char *buf;                              // this rank's data (in place)
+  char *peer_scratch[AR_MAX_RANKS];       // rank -> its scratch base as seen here
+  char *my_scratch;
+  int order[AR_MAX_RANKS];                // summation order (the plan's reduce inputs)
+  long long bytes, cap_lines;
+  int me, world, esize, avg_n;
+  unsigned long long *epoch_dev;          // last completed LL call (device-resident)
+  unsigned int *done_ctr;
+  unsigned long long *err;
+  unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ void st_vol_v4(void *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint4 ld_vol_v4(const void *p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+// 8 payload bytes of line i (zero-padded past the end of the buffer)
+__device__ __forceinline__ uint2 ll_load(const char *buf, long long bytes, long long i) {
+  if ((i + 1) * 8 <= bytes) return *(const uint2 *)(buf + i * 8);
+  uint32_t w[2] = {0u, 0u};
+  for (long long b = i * 8; b < bytes; b++) ((unsigned char *)w)[b - i * 8] = (unsigned char)buf[b];
+  return make_uint2(w[0], w[1]);
+}
+
+__global__ void __launch_bounds__(kThreads) ar_ll_kernel(const __grid_constant__ LLArgs a) {
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const uint32_t e = (uint32_t)epoch;
+  const int par = (int)(epoch & 1ull);
+  const long long L = (a.bytes + 7) / 8;
+  const long long nthr = (long long)gridDim.x * blockDim.x;
+  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t plane = (size_t)a.cap_lines * 16;
+  // phase 1: push my lines to every peer
+  for (long long i = t0; i < L; i += nthr) {
+    const uint2 v = ll_load(a.buf, a.bytes, i);
+    for (int t = 0; t < a.world; t++) {
+      if (t == a.me) continue;
+      char *dst = a.peer_scratch[t] + ((size_t)par * a.world + a.me) * plane + (size_t)i * 16;
+      st_vol_v4(dst, v.x, e, v.y, e);
+    }
+  }
+  // phase 2: reduce every line in plan order (same thread <-> line mapping as phase 1)
+  const unsigned long long start = globaltimer();
+  const bool bf16 = a.esize == 2;
+  for (long long i = t0; i < L; i += nthr) {
+    float acc[4];
+    const int per = bf16 ? 4 : 2;
+    for (int k = 0; k < a.world; k++) {
+      const int src = a.order[k];
+      uint2 v;
+      if (src == a.me) {
+        v = ll_load(a.buf, a.bytes, i);
+      } else {
+        const char *p = a.my_scratch + ((size_t)par * a.world + src) * plane + (size_t)i * 16;
+        uint4 x = ld_vol_v4(p);
+        unsigned int spins = 0;
+        while (x.y != e || x.w != e) {
+          if ((++spins & 1023u) == 0 && globaltimer() - start > a.timeout_ns) {
+            atomicExch(a.err, 1ull);
+            break;
+          }
+          x = ld_vol_v4(p);
+        }
+        v = make_uint2(x.x, x.z);
+      }
+      float f[4];
+      if (bf16) {
+        f[0] = bf_lo(v.x); f[1] = bf_hi(v.x); f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
+      } else {
+        f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+      }
+      for (int j = 0; j < per; j++) acc[j] = k == 0 ? f[j] : __fadd_rn(acc[j], f[j]);
+    }
+    if (a.avg_n)
+      for (int j = 0; j < per; j++) acc[j] = __fdiv_rn(acc[j], (float)a.avg_n);
+    uint2 o;
+    if (bf16) {
+      o.x = f2bf(acc[0]) | (f2bf(acc[1]) << 16);
+      o.y = f2bf(acc[2]) | (f2bf(acc[3]) << 16);
+    } else {
+      o.x = __float_as_uint(acc[0]);
+      o.y = __float_as_uint(acc[1]);
+    }
+    if ((i + 1) * 8 <= a.bytes) {
+      *(uint2 *)(a.buf + i * 8) = o;
+    } else {
+      const uint32_t w[2] = {o.x, o.y};
+      for (long long b = i * 8; b < a.bytes; b++) a.buf[b] = (char)((const unsigned char *)w)[b - i * 8];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(a.done_ctr, 1u) == gridDim.x - 1) {
+      *(volatile unsigned int *)a.done_ctr = 0;
+      *(volatile unsigned long long *)a.epoch_dev = epoch;
+      __threadfence();
+    }
+  }
+}
+
 // ------------------------------------------------------------------ synthetic inputs
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -808,6 +930,8 @@ struct Lowered {
   int *prog_begin = nullptr;
   int *prog_len = nullptr;
   int nctas = 0;
+  bool ll_shape = false;     // CPS-shaped: one all-rank reduce per block, identical input order
+  std::vector<int> ll_order;
 };
 
 }  // namespace
@@ -840,6 +964,14 @@ struct ar_comm {
   bool store_tma = true;                       // bulk-copy stores of results (AR_EXEC_STORE=regs: st.global)
   int stages = kDefStages, stage_bytes = kDefStageBytes;   // AR_STAGES, AR_STAGE_KB
   unsigned int jitter_ns = 0;                  // AR_JITTER_NS (stress testing)
+  // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
+  long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
+  long long ll_cap_lines = 0;
+  char *ll_scratch = nullptr;
+  std::vector<char *> ll_peer;                 // rank -> scratch as seen here
+  bool ll_opened = false;
+  int ll_ctas = 32;
+  std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
 };
@@ -851,6 +983,8 @@ struct Blob {
   int32_t rank, world;
   uint64_t bytes, offset;
   cudaIpcMemHandle_t data, sig;
+  cudaIpcMemHandle_t ll;      // low-latency scratch (valid iff has_ll)
+  int32_t has_ll, pad;
 };
 static_assert(sizeof(Blob) <= AR_BLOB_BYTES, "blob too large");
 
@@ -1128,6 +1262,26 @@ static int resident_ctas(int device) {
     return AR_ESYS;                                            \
   }
 
+constexpr long long kLLDefaultMaxBytes = 256 * 1024;
+
+// A plan the one-shot path can run with identical bits: two steps (RS, AG) whose RS step has
+// one reduce per block, every reduce over all ranks in the same order.  Returns that order.
+static std::vector<int> ll_order_of(const Plan &P) {
+  if (P.steps.size() != 2 || P.steps[0].ag || !P.steps[1].ag || (int)P.steps[0].reduces.size() != P.n) return {};
+  const std::vector<int> &ord = P.steps[0].reduces[0].inputs;
+  if ((int)ord.size() != P.n) return {};
+  std::vector<char> seen(P.n, 0), blk(P.n, 0);
+  for (int x : ord) {
+    if (x < 0 || x >= P.n || seen[x]) return {};
+    seen[x] = 1;
+  }
+  for (auto &rd : P.steps[0].reduces) {
+    if (rd.inputs != ord || rd.block < 0 || rd.block >= P.n || blk[rd.block]) return {};
+    blk[rd.block] = 1;
+  }
+  return ord;
+}
+
 static void init_comm(ar_comm *c) {
   CUDA_OK(cudaSetDevice(c->device));
   int nsm = 0;
@@ -1145,8 +1299,10 @@ static void init_comm(ar_comm *c) {
   CUDA_OK(cudaMalloc(&c->sig_local, pages * c->page_elems * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->sig_local, 0, pages * c->page_elems * sizeof(unsigned long long)));
   // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter
-  CUDA_OK(cudaMalloc(&c->err, 4 * sizeof(unsigned long long)));
-  CUDA_OK(cudaMemset(c->err, 0, 4 * sizeof(unsigned long long)));
+  // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter,
+  // [3] last completed LL epoch, [4] LL finished-CTA counter
+  CUDA_OK(cudaMalloc(&c->err, 6 * sizeof(unsigned long long)));
+  CUDA_OK(cudaMemset(c->err, 0, 6 * sizeof(unsigned long long)));
   c->sig.assign(c->world, nullptr);
   for (int i = 0; i < c->rpp; i++) c->sig[c->rank + i] = c->sig_local + (size_t)i * c->page_elems;
   if (c->local) c->sig_opened = true;
@@ -1167,6 +1323,19 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_STAGE_KB")) c->stage_bytes = std::max(4, std::atoi(v)) * 1024;
   while (dyn_smem_bytes(c->stages, c->stage_bytes) > kMaxDynSmem) c->stage_bytes -= 1024;
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
+  if (!c->local && c->rpp == 1) {
+    c->ll_max_bytes = kLLDefaultMaxBytes;
+    if (const char *v = std::getenv("AR_LL_MAX_KB")) c->ll_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
+    if (c->ll_max_bytes > 0) {
+      c->ll_cap_lines = (c->ll_max_bytes + 7) / 8;
+      const size_t sz = (size_t)2 * c->world * c->ll_cap_lines * 16;
+      CUDA_OK(cudaMalloc(&c->ll_scratch, sz));
+      CUDA_OK(cudaMemset(c->ll_scratch, 0, sz));
+      c->ll_peer.assign(c->world, nullptr);
+      c->ll_peer[c->rank] = c->ll_scratch;
+    }
+  }
+  if (const char *v = std::getenv("AR_LL_CTAS")) c->ll_ctas = std::max(1, std::atoi(v));
 }
 
 }  // namespace
@@ -1271,6 +1440,10 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     b.offset = (uint64_t)((char *)dptr - base);
     CUDA_OK(cudaIpcGetMemHandle(&b.data, base));
     CUDA_OK(cudaIpcGetMemHandle(&b.sig, c->sig_local));
+    if (c->ll_scratch) {
+      CUDA_OK(cudaIpcGetMemHandle(&b.ll, c->ll_scratch));
+      b.has_ll = 1;
+    }
     std::memset(blob_out, 0, AR_BLOB_BYTES);
     std::memcpy(blob_out, &b, sizeof b);
     Registration reg;
@@ -1316,6 +1489,7 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
         return (char *)p;
       };
       reg->peer[t] = open(b->data) + b->offset;
+      if (c->ll_scratch && b->has_ll && !c->ll_peer[t]) c->ll_peer[t] = open(b->ll);
       unsigned long long *pages = nullptr;
       for (int i = 0; i < c->rpp; i++)
         if (!c->sig[t * c->rpp + i]) {
@@ -1326,6 +1500,11 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
     reg->opened = true;
     c->fast_valid = false;
     c->sig_opened = true;
+    if (c->ll_scratch) {
+      bool all = true;
+      for (int t = 0; t < c->world; t++) all = all && c->ll_peer[t] != nullptr;
+      c->ll_opened = all;
+    }
     return AR_OK;
   })
 }
@@ -1359,6 +1538,7 @@ int ar_comm_destroy(ar_comm *c) {
   for (auto &kv : c->lowered) free_lowered(kv.second);
   for (auto &kv : c->ipc_opened) cudaIpcCloseMemHandle(kv.second);
   cudaFree(c->sig_local);
+  cudaFree(c->ll_scratch);
   cudaFree(c->err);
   cudaFree(c->trace);
   delete c;
@@ -1534,6 +1714,35 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   CUDA_OK(cudaGetDevice(&cur));
   if (cur != c->device) CUDA_OK(cudaSetDevice(c->device));
   dim3 grid(c->nctas, c->rpp);
+  const size_t nbytes_call = count * (size_t)plan->esize;
+  if (c->ll_opened && (long long)nbytes_call <= c->ll_max_bytes) {
+    // low-latency one-shot path for CPS-shaped plans (see ar_ll_kernel)
+    auto lit = c->ll_shape.find(plan->uid);
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+    if (!lit->second.empty()) {
+      LLArgs la{};
+      la.buf = (char *)dptr;
+      for (int t = 0; t < c->world; t++) la.peer_scratch[t] = c->ll_peer[t];
+      la.my_scratch = c->ll_scratch;
+      for (int k = 0; k < c->world; k++) la.order[k] = lit->second[k];
+      la.bytes = (long long)nbytes_call;
+      la.cap_lines = c->ll_cap_lines;
+      la.me = c->rank;
+      la.world = c->world;
+      la.esize = plan->esize;
+      la.avg_n = avg_n;
+      la.epoch_dev = c->err + 3;
+      la.done_ctr = (unsigned int *)(c->err + 4);
+      la.err = c->err;
+      la.timeout_ns = c->timeout_ns;
+      const long long lines = (la.bytes + 7) / 8;
+      const int ctas = (int)std::max(1LL, std::min<long long>(c->ll_ctas, (lines + kThreads - 1) / kThreads));
+      ar_ll_kernel<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      CUDA_OK(cudaGetLastError());
+      c->last_launches = 1;
+      return AR_OK;
+    }
+  }
   if (c->fast_valid && c->fast_uid == plan->uid && c->fast_dptr == dptr && c->fast_nctas == c->nctas) {
     // steady state: same plan and buffer as the previous call — launch the cached arguments
     ++c->epoch;

@@ -75,6 +75,37 @@ def main():
                     print(e, flush=True)
                     failures += 1
                 dist.barrier()
+    # back-to-back small calls without host syncs: the one-shot low-latency path (double-
+    # buffered scratch, epoch-tagged lines) interleaved with the flag-protocol path
+    for dtype in ("f32", "bf16"):
+        es = 4 if dtype == "f32" else 2
+        count = 3001
+        buf = torch.zeros(count * es + 16, dtype=torch.uint8, device="cuda")
+        keep.append(buf)
+        comm.register(buf)
+        topo = T.parse_topology(doc)
+        pc = G.Plan.from_topology(doc, count, dtype, None, "cps")
+        pr = G.Plan.from_topology(doc, count, dtype, None, "ring")
+        oc, _ = GT.gentree(topo, count, es, force="cps")
+        orr, _ = GT.gentree(topo, count, es, force="ring")
+        seq = ["cps"] * 6 + ["ring"] + ["cps"] * 5 + ["ring", "cps"]
+        G.fill_synthetic(buf, count, dtype, seed + 1, rank, 0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for k in seq:
+            G.allreduce_exec(pc if k == "cps" else pr, comm, buf)
+        torch.cuda.synchronize()
+        comm.async_error()
+        want = GEN.generate_all(seed + 1, world, count, dtype)
+        for k in seq:
+            want = SM.simulate(oc if k == "cps" else orr, want, dtype)
+        got = buf.cpu().numpy()[: count * es].view(np.float32 if dtype == "f32" else np.uint16)
+        try:
+            assert_bits_equal(got, want[rank], dtype, f"rank {rank} {dtype} back-to-back small calls")
+        except AssertionError as e:
+            print(e, flush=True)
+            failures += 1
+        dist.barrier()
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
