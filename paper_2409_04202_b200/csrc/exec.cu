@@ -1262,7 +1262,7 @@ static int resident_ctas(int device) {
     return AR_ESYS;                                            \
   }
 
-constexpr long long kLLDefaultMaxBytes = 1024 * 1024;
+constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
 
 // A plan the one-shot path can run with identical bits: two steps (RS, AG) whose RS step has
 // one reduce per block, every reduce over all ranks in the same order.  Returns that order.
@@ -1326,7 +1326,7 @@ static void init_comm(ar_comm *c) {
   if (!c->local && c->rpp == 1) {
     // measured on 4 x B200 (profiles/README.md): the one-shot path costs ~(N-1)·2S of line
     // traffic per GPU; it beats the flag protocol up to ~768 KiB at N = 4 (13.6 vs 21.4 us at
-    // 512 KiB, 25.2 vs 21.9 at 1 MiB), so the cut-off scales as 1.5 MiB / (N - 1), max 1 MiB
+    // 512 KiB, 25.2 vs 21.9 at 1 MiB), so the cut-off scales as 1.5 MiB / (N - 1)
     c->ll_max_bytes = std::min<long long>(kLLDefaultMaxBytes, (3LL << 19) / (c->world - 1)) / 256 * 256;
     if (const char *v = std::getenv("AR_LL_MAX_KB")) c->ll_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
     if (c->ll_max_bytes > 0) {

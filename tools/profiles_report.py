@@ -103,8 +103,8 @@ def sweep_table(out, path, title):
 def c2_section(out):
     out.append("## 3. C2 sweep: busbw vs size — GenTree plan, NVLS, NCCL on the same box\n")
     c2 = os.path.join(P, "round1", "c2")
-    sweep_table(out, os.path.join(c2, "sweep_n4_f32_nvls16.jsonl"), "C2, 4×B200, fp32 (GenTree chose CPS at every size)")
-    sweep_table(out, os.path.join(c2, "sweep_n2_f32_nvls16.jsonl"), "C2, 2×B200, fp32 (GenTree chose CPS at every size)")
+    sweep_table(out, os.path.join(c2, "sweep_n4_f32_ll.jsonl"), "C2, 4×B200, fp32 (GenTree chose CPS at every size; ≤ 512 KiB via the one-shot path)")
+    sweep_table(out, os.path.join(c2, "sweep_n2_f32_ll.jsonl"), "C2, 2×B200, fp32 (GenTree chose CPS at every size; ≤ 1 MiB via the one-shot path)")
     bf = os.path.join(c2, "sweep_n4_bf16.jsonl")
     if os.path.exists(bf):
         sweep_table(out, bf, "4×B200, bf16")
