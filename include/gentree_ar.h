@@ -127,6 +127,23 @@ int gt_plan_info(const gt_plan *plan, int32_t *n_ranks, int32_t *n_steps, uint64
 int genmodel_predict(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
 void gt_plan_free(gt_plan *plan);
 
+/* Incast-aware flow-level simulation of the plan (procedure
+ * S:382-424, readings FS1-FS3 in DESIGN.md): per step, the transfers are routed on the tree,
+ * α = the max over used links, the communication time comes from max-min fair rate sharing
+ * recomputed at every flow completion, each directed link with capacity 1/β',
+ * β' = β + max(w − w_t, 0)·ε and w = 1 + the distinct source ranks of its active flows, and
+ * the compute time is the slowest server's Σ (k−1)|b|γ + (k+1)|b|δ.  topology_json == NULL
+ * simulates on the plan's own topology, otherwise on that document (same number of servers;
+ * rank r = the r-th server in DFS pre-order) — e.g. a flat plan routed over a tree.
+ * params == NULL uses the topology's own links and servers (a plan from gt_plan_from_json
+ * without a document then needs params: it is simulated on a single switch).  out: latency = Σα, bandwidth = the communication time with
+ * ε = 0, incast = the rest of the communication time, compute/memory = the slowest server's γ
+ * and δ parts, total.  step_times (optional, cap entries) receives each step's time;
+ * *n_steps (optional) the number of steps.  Errors: AR_EINVAL for null plan/out or invalid
+ * params. */
+int gt_plan_simulate(const gt_plan *plan, const char *topology_json, const gm_params *params, gm_breakdown *out,
+                     double *step_times, size_t cap, size_t *n_steps);
+
 /* Build a plan from its canonical JSON (the gt_plan_to_json format): ranks, block
  * indices and transfer sizes are validated and no op of a step may write a (rank, block)
  * another op of the step reads or writes (AR_EINVAL otherwise).  *is_allreduce (optional)

@@ -70,6 +70,8 @@ _SIGS = {
                                 ctypes.POINTER(ctypes.c_double)]),
     "genmodel_choose_nvls": (I32, [P, ctypes.POINTER(GmParams), ctypes.POINTER(GmParams), ctypes.POINTER(I32),
                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "gt_plan_simulate": (I32, [P, ctypes.c_char_p, ctypes.POINTER(GmParams), ctypes.POINTER(GmBreakdown),
+                               ctypes.POINTER(ctypes.c_double), SZ, ctypes.POINTER(SZ)]),
     "genmodel_closed_form": (I32, [ctypes.c_char_p, I32, U64, ctypes.POINTER(GmParams),
                                    ctypes.POINTER(GmBreakdown)]),
     "gentree_plan": (I32, [ctypes.c_char_p, U64, I32, ctypes.POINTER(GmParams), ctypes.c_char_p,

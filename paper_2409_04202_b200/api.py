@@ -145,6 +145,20 @@ class Plan:
         check(lib.genmodel_predict_executed(self._h, ctypes.byref(params), ctypes.byref(out)))
         return out.as_dict()
 
+    def simulate(self, params: GmParams | None = None, topology_json: str | None = None) -> dict:
+        """Incast-aware flow-level simulation (gt_plan_simulate; NEXT #2), on the plan's own
+        topology or on `topology_json`.  Adds "steps"."""
+        out = GmBreakdown()
+        n = ctypes.c_size_t()
+        pp = ctypes.byref(params) if params is not None else None
+        doc = topology_json.encode() if topology_json is not None else None
+        check(lib.gt_plan_simulate(self._h, doc, pp, ctypes.byref(out), None, 0, ctypes.byref(n)))
+        steps = (ctypes.c_double * max(1, n.value))()
+        check(lib.gt_plan_simulate(self._h, doc, pp, ctypes.byref(out), steps, n.value, None))
+        d = out.as_dict()
+        d["steps"] = list(steps)[: n.value]
+        return d
+
     def choose_nvls(self, params: GmParams, nvls_params: GmParams) -> dict:
         """GenModel's plan-vs-NVLS choice at this plan's (n, bytes) (genmodel_choose_nvls)."""
         use = ctypes.c_int32()

@@ -23,7 +23,7 @@ ROOT = os.path.dirname(HERE)
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 CXX = os.environ.get("CXX", shutil.which("g++") or "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-HOST_SRCS = ["planner.cc", "capi_plan.cc"]
+HOST_SRCS = ["planner.cc", "flowsim.cc", "capi_plan.cc"]
 CUDA_SRCS = ["exec.cu", "nvls.cu"]
 
 

@@ -129,6 +129,37 @@ int genmodel_choose_nvls(const gt_plan *plan, const gm_params *plan_params, cons
   })
 }
 
+int gt_plan_simulate(const gt_plan *plan, const char *topology_json, const gm_params *params, gm_breakdown *out,
+                     double *step_times, size_t cap, size_t *n_steps) {
+  AR_TRY({
+    if (!plan || !out) throw InvalidArg("null argument");
+    Params p;
+    if (params) {
+      check_params(params);
+      p = to_params(params);
+    }
+    Topology t = topology_json ? parse_topology(topology_json) : plan->topo;
+    if (topology_json && (int)t.servers.size() != plan->plan.n)
+      throw InvalidArg("topology and plan have different numbers of ranks");
+    if (t.nodes.empty()) {   // plan built from JSON: a single switch with uniform links
+      if (!params) throw InvalidArg("a plan without a topology needs explicit params");
+      std::string doc = "{\"nodes\":[{\"id\":\"sw\",\"kind\":\"switch\",\"parent\":null,\"uplink\":null}";
+      for (int i = 0; i < plan->plan.n; i++)
+        doc += ",{\"id\":\"s" + std::to_string(i) +
+               "\",\"kind\":\"server\",\"parent\":\"sw\",\"uplink\":{\"alpha\":0,\"beta\":1,\"epsilon\":0,\"w_t\":1},"
+               "\"compute\":{\"gamma\":0,\"delta\":0}}";
+      doc += "]}";
+      t = parse_topology(doc);
+    }
+    SimResult r = simulate_flows(t, plan->plan, plan->esize, params ? &p : nullptr);
+    fill(out, r.b);
+    if (n_steps) *n_steps = r.steps.size();
+    if (step_times)
+      for (size_t i = 0; i < r.steps.size() && i < cap; i++) step_times[i] = r.steps[i];
+    return AR_OK;
+  })
+}
+
 int genmodel_closed_form(const char *kind, int32_t n, uint64_t bytes, const gm_params *params, gm_breakdown *out) {
   AR_TRY({
     if (!kind || !params || !out) throw InvalidArg("null argument");

@@ -116,6 +116,14 @@ void verify_allreduce(const Plan &p);                                      // th
 std::string plan_to_json(const Plan &p, const char *dtype);
 std::string report_to_json(const std::vector<SwitchReport> &r);
 
+// ------------------------------------------------------------------ flow simulator (NEXT #2)
+struct SimResult {
+  Breakdown b;                       // latency, bandwidth (ε = 0), incast, compute, memory, total
+  std::vector<double> steps;         // per-step time
+};
+// params == nullptr: each link's / server's own parameters from the topology (per float / 4)
+SimResult simulate_flows(const Topology &t, const Plan &p, int esize, const Params *params);
+
 // ------------------------------------------------------------------ fit
 struct Measurement { int n; double s; double t; };
 struct FitResult {

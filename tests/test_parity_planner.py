@@ -194,3 +194,36 @@ def test_choose_nvls():
     eq = G.params(alpha=9.4e-6, beta=1.465e-12)
     assert not G.Plan.single_switch(2, 1 << 27, "bf16", pp).choose_nvls(pp, eq)["use_nvls"]
     assert G.Plan.single_switch(4, 1 << 27, "bf16", pp).choose_nvls(pp, eq)["use_nvls"]
+
+
+def _sim_close(a: dict, b: dict):
+    for k in ("latency", "bandwidth", "compute", "memory", "incast", "total"):
+        assert a[k] == pytest.approx(float(b[k]), rel=1e-9, abs=1e-15), k
+
+
+@pytest.mark.parametrize("which", ["SS24", "two_level", "asym", "cdc_small"])
+def test_flow_simulator_parity(which):
+    """NEXT #2: gt_plan_simulate vs oracle.flowsim (exact rationals), 1e-9 relative."""
+    from oracle import flowsim as FS
+    from tests.topologies import cross_dc
+    docs = {"SS24": _gtplan_topos()["SS24"],
+            "two_level": T.two_level_doc([4, 4, 4], row("root_sw"), row("middle_sw"), T.TABLE5["server"]),
+            "asym": T.two_level_doc([6, 2, 3], row("root_sw"), row("middle_sw"), T.TABLE5["server"]),
+            "cdc_small": cross_dc(2, 4, 2, 2)}
+    doc = docs[which]
+    t = T.parse_topology(doc)
+    for S in (10 ** 6, 32 * 10 ** 6):
+        for force in (None, "cps", "ring"):
+            lib = G.Plan.from_topology(doc, S, "f32", None, force)
+            oplan, _ = GT.gentree(t, S, 4, force=force)
+            _sim_close(lib.simulate(), FS.simulate_flows(t, oplan, 4))
+    # a flat plan routed over the tree (topology_json)
+    n = len(t.servers)
+    flat = G.Plan.single_switch(n, 12345, "f32", G.params(alpha=1e-3, beta=1e-9), "cps")
+    oflat = OP.build_plan("cps", n, 12345)
+    _sim_close(flat.simulate(topology_json=doc), FS.simulate_flows(t, oflat, 4))
+    # uniform params
+    p = OG.Params(1e-4, 2e-12, 1e-13, 3e-13, 5e-14, 3)
+    lib = G.Plan.from_topology(doc, 99999, "bf16")
+    oplan, _ = GT.gentree(t, 99999, 2)
+    _sim_close(lib.simulate(lib_params(p)), FS.simulate_flows(t, oplan, 2, p))

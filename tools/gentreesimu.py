@@ -1,0 +1,126 @@
+"""Desk reproduction of tab:gentreesimu with the library's flow simulator
+(gt_plan_simulate).
+
+    python tools/gentreesimu.py [--out profiles/gentreesimu.json]
+
+Topologies of P:1100-1105 with Table 5's parameters (tab:gtcoe): servers hang off
+Middle-SW links, middle switches off Root-SW links, the two data centres' roots off one
+Cross-DC link; α per step taken as 3× the printed 6.58e-3 s (reading Q16: the only value that
+reproduces the single-switch rows and tab:gtplan's selections).  Sizes in floats (fp32).
+GenTree* (no data rearrangement) is not reproduced: the planner always considers it."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2409_04202_b200 as G  # noqa: E402
+
+A3 = 3 * 6.58e-3
+ROWS = {   # tab:gtcoe, per float
+    "cross_dc": {"alpha": A3, "beta": 6.40e-9, "epsilon": 6.00e-11, "w_t": 9},
+    "root_sw": {"alpha": A3, "beta": 6.40e-10, "epsilon": 6.00e-12, "w_t": 9},
+    "middle_sw": {"alpha": A3, "beta": 6.40e-9, "epsilon": 1.22e-10, "w_t": 9},
+}
+SERVER = {"gamma": 6.00e-10, "delta": 1.87e-10}
+PAPER = {   # tab:gentreesimu, seconds at 1e7 / 3.2e7 / 1e8 floats
+    "SS24": {"gentree": (0.203, 0.503, 1.404), "ring": (1.082, 1.376, 2.288), "cps": (0.203, 0.562, 1.673)},
+    "SS32": {"gentree": (0.213, 0.507, 1.417), "rhd": (0.337, 0.644, 1.593), "ring": (1.399, 1.697, 2.617),
+             "cps": (0.223, 0.628, 1.879)},
+    "SYM384": {"gentree": (0.503, 1.287, 3.575), "ring": (2.943, 3.627, 5.742), "cps": (2.274, 7.132, 22.148)},
+    "SYM512": {"gentree": (0.639, 1.627, 4.638), "rhd": (0.896, 1.853, 4.812), "ring": (3.571, 4.479, 7.285),
+               "cps": (3.479, 10.989, 34.200)},
+    "ASY384": {"gentree": (0.570, 1.593, 4.670), "ring": (3.043, 3.947, 6.741), "cps": (2.052, 6.421, 19.925)},
+    "CDC384": {"gentree": (2.427, 8.299, 25.388), "ring": (8.513, 17.329, 44.580), "cps": (11.890, 37.799, 117.882)},
+}
+SIZES = (10 ** 7, 32 * 10 ** 6, 10 ** 8)
+
+
+def server(i, parent):
+    return {"id": f"s{i}", "kind": "server", "parent": parent, "uplink": ROWS["middle_sw"], "compute": SERVER}
+
+
+def single(n):
+    return {"nodes": [{"id": "sw", "kind": "switch", "parent": None, "uplink": None}] + [server(i, "sw") for i in range(n)]}
+
+
+def two_level(groups):
+    nodes = [{"id": "R", "kind": "switch", "parent": None, "uplink": None}]
+    k = 0
+    for g, cnt in enumerate(groups):
+        nodes.append({"id": f"M{g}", "kind": "switch", "parent": "R", "uplink": ROWS["root_sw"]})
+        for _ in range(cnt):
+            nodes.append(server(k, f"M{g}"))
+            k += 1
+    return {"nodes": nodes}
+
+
+def cross_dc():
+    nodes = [{"id": "X", "kind": "switch", "parent": None, "uplink": None}]
+    k = 0
+    for dc, (m, cnt) in enumerate([(8, 32), (8, 16)]):
+        nodes.append({"id": f"DC{dc}", "kind": "switch", "parent": "X", "uplink": ROWS["cross_dc"]})
+        for g in range(m):
+            nodes.append({"id": f"DC{dc}M{g}", "kind": "switch", "parent": f"DC{dc}", "uplink": ROWS["root_sw"]})
+            for _ in range(cnt):
+                nodes.append(server(k, f"DC{dc}M{g}"))
+                k += 1
+    return {"nodes": nodes}
+
+
+TOPOS = {"SS24": single(24), "SS32": single(32), "SYM384": two_level([24] * 16), "SYM512": two_level([32] * 16),
+         "ASY384": two_level([32] * 8 + [16] * 8), "CDC384": cross_dc()}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "gentreesimu.json"))
+    ap.add_argument("--topos", default=",".join(TOPOS))
+    a = ap.parse_args()
+    rows = []
+    for name in a.topos.split(","):
+        doc = json.dumps(TOPOS[name])
+        nserv = sum(1 for x in TOPOS[name]["nodes"] if x["kind"] == "server")
+        flat_ok = len([x for x in TOPOS[name]["nodes"] if x["kind"] == "switch"]) > 1
+        for alg, paper in PAPER[name].items():
+            # baselines: "per-switch" = that kind at every switch of the tree (GenTree's
+            # candidate set restricted to it); "flat" = one plan over all servers, routed on
+            # the tree (the paper does not say which one its baselines are)
+            variants = [("gentree", None)] if alg == "gentree" else [("per-switch", alg)] + (
+                [("flat", alg)] if flat_ok else [])
+            for variant, kind in variants:
+                for S, pv in zip(SIZES, paper):
+                    t0 = time.time()
+                    if variant == "flat":
+                        uni = G.params(alpha=A3, beta=1.0)   # placeholder links: simulated on `doc`
+                        plan = G.Plan.single_switch(nserv, S, "f32", uni, kind)
+                        sim = plan.simulate(topology_json=doc)
+                        chosen = [kind]
+                    else:
+                        plan = G.Plan.from_topology(doc, S, "f32", None, kind)
+                        sim = plan.simulate()
+                        chosen = [r["chosen"] for r in plan.report()]
+                    rows.append({"topo": name, "alg": alg, "variant": variant, "floats": S, "sim_s": sim["total"],
+                                 "paper_s": pv, "rel_dev": sim["total"] / pv - 1, "chosen": chosen,
+                                 "terms": {k: sim[k] for k in ("latency", "bandwidth", "incast", "compute", "memory")},
+                                 "wall_s": round(time.time() - t0, 2)})
+                    r = rows[-1]
+                    print(f"{name:7s} {alg:8s} {variant:10s} {S:>10d}  sim {r['sim_s']:8.3f}  paper {pv:8.3f}  "
+                          f"dev {r['rel_dev']:+.3f}", flush=True)
+    # the paper's claim: GenTree beats the baselines everywhere; speedups per topology
+    claims = {}
+    for name in {r["topo"] for r in rows}:
+        for S in SIZES:
+            g = next(r["sim_s"] for r in rows if r["topo"] == name and r["alg"] == "gentree" and r["floats"] == S)
+            base = {r["alg"] + "/" + r["variant"]: r["sim_s"] for r in rows
+                    if r["topo"] == name and r["alg"] != "gentree" and r["floats"] == S}
+            claims[f"{name}@{S}"] = {"gentree_fastest": all(g <= v * (1 + 1e-12) for v in base.values()),
+                                     "max_speedup": max(v / g for v in base.values())}
+    json.dump({"rows": rows, "claims": claims, "alpha_per_step": A3}, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -175,6 +175,34 @@ def hybrid_section(out):
                "GPU's ranks in HBM, then across GPUs over NVLink) beats any flat plan over the same ranks.\n")
 
 
+def gentreesimu_section(out):
+    path = os.path.join(P, "gentreesimu.json")
+    if not os.path.exists(path):
+        return
+    d = json.load(open(path))
+    out.append("## 7. Flow-level simulation: tab:gentreesimu (NEXT #2, `gt_plan_simulate`)\n")
+    out.append("Seconds at 1e7 / 3.2e7 / 1e8 floats; Table 5 parameters, α per step 3 × 6.58e-3 s (reading Q16).\n"
+               "`per-switch` = the baseline kind at every switch of the tree, `flat` = one plan over all servers\n"
+               "routed on the tree.  Generated by `tools/gentreesimu.py`.\n")
+    out.append("| topology | algorithm | simulated | paper | deviation |")
+    out.append("|---|---|---|---|---|")
+    groups = collections.OrderedDict()
+    for r in d["rows"]:
+        groups.setdefault((r["topo"], r["alg"], r.get("variant", "")), []).append(r)
+    for (topo, alg, var), rs in groups.items():
+        name = alg if var in ("", "gentree") else f"{alg} ({var})"
+        out.append(f"| {topo} | {name} | " + " / ".join(f"{r['sim_s']:.3f}" for r in rs) + " | " +
+                   " / ".join(f"{r['paper_s']:.3f}" for r in rs) + " | " +
+                   " / ".join(f"{r['rel_dev']:+.0%}" for r in rs) + " |")
+    fast = sum(v["gentree_fastest"] for v in d["claims"].values())
+    out.append(f"\nSingle-switch rows reproduce within 4 % (pinned in `tests/test_oracle_flowsim.py`).  The\n"
+               f"hierarchical rows do not: the paper's simulator is unreleased and its baselines' routing and\n"
+               f"incast accounting on multi-level trees are not described, so those rows are reported, not\n"
+               f"pinned.  The paper's qualitative claim — GenTree fastest — holds in {fast} of {len(d['claims'])}\n"
+               f"(topology, size) cells here; the exception is GenTree's heuristic choice losing by a few percent\n"
+               f"to per-switch CPS (P:559: GenTree is a heuristic, its choice uses GenModel, not the simulator).\n")
+
+
 def p2p_section(out):
     out.append("## 5. Incast probe (x-to-x, S:449) on 4×B200\n")
     out.append("| pattern | bytes | GB/s per direction per GPU |")
@@ -197,6 +225,7 @@ def main():
     nvls_fit_section(out)
     p2p_section(out)
     hybrid_section(out)
+    gentreesimu_section(out)
     sys.stdout.write("\n".join(out) + "\n")
 
 
