@@ -898,7 +898,12 @@ template <bool BF16>
 __global__ void __launch_bounds__(kThreads, 2) local_reduce_kernel(const __grid_constant__ LocalReduceArgs a) {
   __shared__ OpShared sh;
   if (threadIdx.x < a.k) sh.src[threadIdx.x] = a.in[threadIdx.x];
-  if (threadIdx.x == 0) { sh.nsrc = a.k; sh.ndst = 1; sh.dst[0] = a.out; }
+  if (threadIdx.x == 0) {
+    sh.nsrc = a.k;
+    sh.ndst = 1;
+    sh.dst[0] = a.out;
+    sh.div = 0;
+  }
   __syncthreads();
   const size_t v0 = a.nvec * blockIdx.x / gridDim.x, v1 = a.nvec * (blockIdx.x + 1) / gridDim.x;
   body_dispatch<BF16>(sh, v0, v1);
