@@ -86,7 +86,20 @@ struct ExecArgs {
   int stages, stage_bytes;   // bulk-copy ring geometry
   unsigned int jitter_ns;    // stress mode: random delay before each notify (AR_JITTER_NS), 0 = off
   int avg_n;                 // AR_OP_AVG: divide final reduces by avg_n (IEEE fp32 division); 0 = SUM
+  // push protocol (lower_push): rank -> its push scratch as seen here; [parity][src][slot]
+  char *scr[AR_MAX_RANKS];
+  long long scr_plane, scr_slot;
 };
+
+// Buffer references in op rank lists: r < kScrRef is rank r's data buffer; kScrRef + o·64 + s
+// is the push scratch slot on owner o for source s (parity = the call's epoch & 1).
+constexpr int kScrRef = 1 << 12;
+__device__ __forceinline__ char *ref_base(const ExecArgs &a, int id, long long off, unsigned long long epoch) {
+  if (id < kScrRef) return a.bufs[id];
+  const int o = (id - kScrRef) / AR_MAX_RANKS, src = (id - kScrRef) % AR_MAX_RANKS;
+  const long long ob = off * a.esize;   // slot keeps the buffer's 16-byte phase of element `off`
+  return a.scr[o] + (long long)(epoch & 1ull) * a.scr_plane + (long long)src * a.scr_slot + (ob & 15) - ob;
+}
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
@@ -503,39 +516,38 @@ __device__ void body_dispatch_bulk(const OpShared &s, size_t v0, size_t v1, uint
 }
 
 // Scalar elements [e0, e1) (unaligned head / tail), same summation order.
-__device__ __noinline__ void scalar_elems(const OpShared &s, const ExecArgs &a, const int *src_ranks, const int *dst_ranks,
-                             long long e0, long long e1, bool bf16) {
+__device__ __noinline__ void scalar_elems(const OpShared &s, long long e0, long long e1, bool bf16) {
   for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     if (bf16) {
-      const unsigned short *p0 = (const unsigned short *)(a.bufs[src_ranks[0]]) + e;
+      const unsigned short *p0 = (const unsigned short *)(s.src[0]) + e;
       unsigned short out;
       if (s.nsrc == 1 && !s.div) {
         out = *(volatile const unsigned short *)p0;
       } else {
         float acc = __uint_as_float((uint32_t)(*(volatile const unsigned short *)p0) << 16);
         for (int k = 1; k < s.nsrc; k++) {
-          const unsigned short *pk = (const unsigned short *)(a.bufs[src_ranks[k]]) + e;
+          const unsigned short *pk = (const unsigned short *)(s.src[k]) + e;
           acc = __fadd_rn(acc, __uint_as_float((uint32_t)(*(volatile const unsigned short *)pk) << 16));
         }
         if (s.div) acc = __fdiv_rn(acc, (float)s.div);
         out = (unsigned short)f2bf(acc);
       }
-      for (int d = 0; d < s.ndst; d++) ((unsigned short *)(a.bufs[dst_ranks[d]]))[e] = out;
+      for (int d = 0; d < s.ndst; d++) ((unsigned short *)(s.dst[d]))[e] = out;
     } else {
-      const uint32_t *p0 = (const uint32_t *)(a.bufs[src_ranks[0]]) + e;
+      const uint32_t *p0 = (const uint32_t *)(s.src[0]) + e;
       uint32_t out;
       if (s.nsrc == 1 && !s.div) {
         out = *(volatile const uint32_t *)p0;
       } else {
         float acc = __uint_as_float(*(volatile const uint32_t *)p0);
         for (int k = 1; k < s.nsrc; k++) {
-          const uint32_t *pk = (const uint32_t *)(a.bufs[src_ranks[k]]) + e;
+          const uint32_t *pk = (const uint32_t *)(s.src[k]) + e;
           acc = __fadd_rn(acc, __uint_as_float(*(volatile const uint32_t *)pk));
         }
         if (s.div) acc = __fdiv_rn(acc, (float)s.div);
         out = __float_as_uint(acc);
       }
-      for (int d = 0; d < s.ndst; d++) ((uint32_t *)(a.bufs[dst_ranks[d]]))[e] = out;
+      for (int d = 0; d < s.ndst; d++) ((uint32_t *)(s.dst[d]))[e] = out;
     }
   }
 }
@@ -636,8 +648,8 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       const long long b0 = op.off * a.esize, b1 = (op.off + op.len) * a.esize;
       const long long vb = (b0 + 15) / 16, ve = b1 / 16;   // whole 16-byte vectors
       __syncthreads();
-      if (threadIdx.x < op.nsrc) sh.src[threadIdx.x] = (const uint4 *)a.bufs[sr[threadIdx.x]];
-      if (threadIdx.x < op.ndst) sh.dst[threadIdx.x] = (uint4 *)a.bufs[dr[threadIdx.x]];
+      if (threadIdx.x < op.nsrc) sh.src[threadIdx.x] = (const uint4 *)ref_base(a, sr[threadIdx.x], op.off, epoch);
+      if (threadIdx.x < op.ndst) sh.dst[threadIdx.x] = (uint4 *)ref_base(a, dr[threadIdx.x], op.off, epoch);
       if (threadIdx.x == 0) {
         sh.nsrc = op.nsrc;
         sh.ndst = op.ndst;
@@ -645,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       }
       __syncthreads();
       if (vb >= ve) {
-        if (cta == 0) scalar_elems(sh, a, sr, dr, op.off, op.off + op.len, bf16);
+        if (cta == 0) scalar_elems(sh, op.off, op.off + op.len, bf16);
         continue;
       }
       const long long nv = ve - vb;
@@ -662,8 +674,8 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
         if (bf16) body_dispatch<true>(sh, v0, v1);
         else body_dispatch<false>(sh, v0, v1);
       }
-      if (cta == 0 && vb * 16 > b0) scalar_elems(sh, a, sr, dr, op.off, vb * vec_elems, bf16);
-      if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(sh, a, sr, dr, ve * vec_elems, op.off + op.len, bf16);
+      if (cta == 0 && vb * 16 > b0) scalar_elems(sh, op.off, vb * vec_elems, bf16);
+      if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(sh, ve * vec_elems, op.off + op.len, bf16);
     }
     AR_TRACE(2 + 3 * si);
     // ---- notify (release our slot on every consumer's page)
@@ -972,6 +984,10 @@ struct ar_comm {
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
+  // push protocol (lower_push) for CPS-shaped plans up to push_max_bytes (AR_PUSH_MAX_MB; 0 = off):
+  // its scratch follows the LL region in the same allocation, [parity][src][push_slot]
+  long long ll_region = 0, push_max_bytes = 0, push_slot = 0, push_plane = 0;
+  std::map<uint64_t, Lowered> lowered_push;
   char *ll_scratch = nullptr;
   std::vector<char *> ll_peer;                 // rank -> scratch as seen here
   bool ll_opened = false;
@@ -1227,6 +1243,103 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
   }
 }
 
+// Push protocol for CPS-shaped plans (see exec_impl): per rank three steps —
+//   slot 1: copy block o of my buffer into owner o's scratch slot [parity][me], for every
+//           o != me; notify every owner;
+//   slot 2: (paired waits on every source's slot 1) reduce my block in the plan's order from
+//           my buffer and the scratch slots, write it to every rank's buffer; notify all;
+//   exit:   paired waits on every owner's slot 2 (its block landed in my buffer).
+// No entry barrier: only the owner reads its own input, and a peer's scratch slot of parity
+// p is rewritten only two calls later (see ar_ll_kernel's argument).  Same-index CTAs slice
+// the same block range in both steps, so paired waits are exact.
+static void lower_push(const Plan &p, const std::vector<int> &order, std::vector<DevStep> &steps,
+                       std::vector<DevOp> &ops, std::vector<DevWait> &waits, std::vector<int> &ranks,
+                       std::vector<int> &prog_begin, std::vector<int> &prog_len) {
+  const int n = p.n;
+  prog_begin.assign(n, 0);
+  prog_len.assign(n, 0);
+  auto scr = [](int owner, int src) { return kScrRef + owner * AR_MAX_RANKS + src; };
+  for (int r = 0; r < n; r++) {
+    prog_begin[r] = (int)steps.size();
+    auto add_op = [&](long long off, long long len, const std::vector<int> &src, const std::vector<int> &dst,
+                      int fin) {
+      DevOp x{};
+      x.off = off;
+      x.len = len;
+      x.nsrc = (int)src.size();
+      x.ndst = (int)dst.size();
+      x.src_begin = (int)ranks.size();
+      ranks.insert(ranks.end(), src.begin(), src.end());
+      x.dst_begin = (int)ranks.size();
+      ranks.insert(ranks.end(), dst.begin(), dst.end());
+      x.fin = fin;
+      ops.push_back(x);
+    };
+    // slot 1: scatter my input blocks to their owners' scratch
+    DevStep a{};
+    a.slot = 1;
+    a.op_begin = (int)ops.size();
+    for (int o = 0; o < n; o++) {
+      if (o == r) continue;
+      const long long len = block_size(p.count, n, o);
+      if (len > 0) add_op(block_offset(p.count, n, o), len, {r}, {scr(o, r)}, 0);
+    }
+    a.op_count = (int)ops.size() - a.op_begin;
+    a.wait_begin = (int)waits.size();
+    a.wait_count = 0;
+    a.notify_begin = (int)ranks.size();
+    for (int o = 0; o < n; o++)
+      if (o != r) ranks.push_back(o);
+    a.notify_count = (int)ranks.size() - a.notify_begin;
+    steps.push_back(a);
+    // slot 2: reduce my block, broadcast it
+    DevStep b{};
+    b.slot = 2;
+    b.wait_begin = (int)waits.size();
+    for (int s2 = 0; s2 < n; s2++) {
+      if (s2 == r) continue;
+      DevWait w{};
+      w.rank = s2;
+      w.slot = 1;
+      w.kind = kWaitPaired;
+      waits.push_back(w);
+    }
+    b.wait_count = (int)waits.size() - b.wait_begin;
+    b.op_begin = (int)ops.size();
+    const long long len = block_size(p.count, n, r);
+    if (len > 0) {
+      std::vector<int> src, dst{r};
+      for (int q : order) src.push_back(q == r ? r : scr(r, q));
+      for (int d = 0; d < n; d++)
+        if (d != r) dst.push_back(d);
+      add_op(block_offset(p.count, n, r), len, src, dst, 1);
+    }
+    b.op_count = (int)ops.size() - b.op_begin;
+    b.notify_begin = (int)ranks.size();
+    for (int d = 0; d < n; d++)
+      if (d != r) ranks.push_back(d);
+    b.notify_count = (int)ranks.size() - b.notify_begin;
+    steps.push_back(b);
+    // exit: every other block has landed
+    DevStep e{};
+    e.slot = 0;
+    e.op_begin = (int)ops.size();
+    e.wait_begin = (int)waits.size();
+    for (int o = 0; o < n; o++) {
+      if (o == r) continue;
+      DevWait w{};
+      w.rank = o;
+      w.slot = 2;
+      w.kind = kWaitPaired;
+      waits.push_back(w);
+    }
+    e.wait_count = (int)waits.size() - e.wait_begin;
+    e.notify_begin = (int)ranks.size();
+    steps.push_back(e);
+    prog_len[r] = (int)steps.size() - prog_begin[r];
+  }
+}
+
 template <typename T>
 static T *upload(const std::vector<T> &v) {
   T *d = nullptr;
@@ -1268,6 +1381,7 @@ static int resident_ctas(int device) {
   }
 
 constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
+constexpr long long kPushDefaultMaxBytes = 32LL << 20;
 
 // A plan the one-shot path can run with identical bits: two steps (RS, AG) whose RS step has
 // one reduce per block, every reduce over all ranks in the same order.  Returns that order.
@@ -1303,7 +1417,6 @@ static void init_comm(ar_comm *c) {
   const size_t pages = c->rpp;
   CUDA_OK(cudaMalloc(&c->sig_local, pages * c->page_elems * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->sig_local, 0, pages * c->page_elems * sizeof(unsigned long long)));
-  // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter
   // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter,
   // [3] last completed LL epoch, [4] LL finished-CTA counter
   CUDA_OK(cudaMalloc(&c->err, 6 * sizeof(unsigned long long)));
@@ -1329,14 +1442,22 @@ static void init_comm(ar_comm *c) {
   while (dyn_smem_bytes(c->stages, c->stage_bytes) > kMaxDynSmem) c->stage_bytes -= 1024;
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
   if (!c->local && c->rpp == 1) {
+    c->push_max_bytes = kPushDefaultMaxBytes;
+    if (const char *v = std::getenv("AR_PUSH_MAX_MB")) c->push_max_bytes = std::strtoll(v, nullptr, 10) << 20;
     // measured on 4 x B200 (profiles/README.md): the one-shot path costs ~(N-1)·2S of line
     // traffic per GPU; it beats the flag protocol up to ~768 KiB at N = 4 (13.6 vs 21.4 us at
     // 512 KiB, 25.2 vs 21.9 at 1 MiB), so the cut-off scales as 1.5 MiB / (N - 1)
     c->ll_max_bytes = std::min<long long>(kLLDefaultMaxBytes, (3LL << 19) / (c->world - 1)) / 256 * 256;
     if (const char *v = std::getenv("AR_LL_MAX_KB")) c->ll_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
-    if (c->ll_max_bytes > 0) {
+    c->ll_max_bytes = std::max(0LL, c->ll_max_bytes);
+    c->push_max_bytes = std::max(0LL, c->push_max_bytes);
+    if (c->ll_max_bytes > 0 || c->push_max_bytes > 0) {
       c->ll_cap_lines = (c->ll_max_bytes + 7) / 8;
-      const size_t sz = (size_t)2 * c->world * c->ll_cap_lines * 16;
+      c->ll_region = ((long long)2 * c->world * c->ll_cap_lines * 16 + 255) / 256 * 256;
+      // one block of the largest pushed message + 16 bytes of alignment phase
+      c->push_slot = ((c->push_max_bytes + c->world - 1) / c->world + 16 + 255) / 256 * 256;
+      c->push_plane = c->push_slot * c->world;
+      const size_t sz = (size_t)c->ll_region + (c->push_max_bytes > 0 ? (size_t)2 * c->push_plane : 0);
       CUDA_OK(cudaMalloc(&c->ll_scratch, sz));
       CUDA_OK(cudaMemset(c->ll_scratch, 0, sz));
       c->ll_peer.assign(c->world, nullptr);
@@ -1544,6 +1665,7 @@ int ar_comm_destroy(ar_comm *c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (auto &kv : c->lowered) free_lowered(kv.second);
+  for (auto &kv : c->lowered_push) free_lowered(kv.second);
   for (auto &kv : c->ipc_opened) cudaIpcCloseMemHandle(kv.second);
   cudaFree(c->sig_local);
   cudaFree(c->ll_scratch);
@@ -1784,13 +1906,22 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       if (!a.bufs[r] || !a.sigs[r]) throw InvalidArg("peer buffer not opened");
     }
   }
-  auto it = c->lowered.find(plan->uid);
-  if (it == c->lowered.end()) {
+  // push protocol for CPS-shaped plans of moderate size (one rank per GPU)
+  bool use_push = false;
+  if (c->ll_opened && c->push_max_bytes > 0 && (long long)bytes <= c->push_max_bytes) {
+    auto lit = c->ll_shape.find(plan->uid);
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+    use_push = !lit->second.empty();
+  }
+  std::map<uint64_t, Lowered> &cache = use_push ? c->lowered_push : c->lowered;
+  auto it = cache.find(plan->uid);
+  if (it == cache.end()) {
     std::vector<DevStep> st;
     std::vector<DevOp> ops;
     std::vector<DevWait> w;
     std::vector<int> rk, pb, pl;
-    lower_plan(plan->plan, c->world, st, ops, w, rk, pb, pl);
+    if (use_push) lower_push(plan->plan, c->ll_shape[plan->uid], st, ops, w, rk, pb, pl);
+    else lower_plan(plan->plan, c->world, st, ops, w, rk, pb, pl);
     Lowered L;
     if (!c->local) {  // this process runs only the programs of the ranks it hosts
       std::vector<int> pb1(pb.begin() + c->rank, pb.begin() + c->rank + c->rpp);
@@ -1804,8 +1935,12 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     L.ranks = upload(rk);
     L.prog_begin = upload(pb);
     L.prog_len = upload(pl);
-    it = c->lowered.emplace(plan->uid, L).first;
+    it = cache.emplace(plan->uid, L).first;
   }
+  if (use_push)
+    for (int t = 0; t < c->world; t++) a.scr[t] = c->ll_peer[t] + c->ll_region;
+  a.scr_plane = c->push_plane;
+  a.scr_slot = c->push_slot;
   const Lowered &L = it->second;
   a.steps = L.steps;
   a.ops = L.ops;

@@ -77,9 +77,9 @@ def main():
                 dist.barrier()
     # back-to-back small calls without host syncs: the one-shot low-latency path (double-
     # buffered scratch, epoch-tagged lines) interleaved with the flag-protocol path
-    for dtype in ("f32", "bf16"):
+    # (3001 elements: one-shot path; 600_001: push protocol; ring: flag protocol)
+    for dtype, count in (("f32", 3001), ("bf16", 3001), ("f32", 600_001), ("bf16", 600_001)):
         es = 4 if dtype == "f32" else 2
-        count = 3001
         buf = torch.zeros(count * es + 16, dtype=torch.uint8, device="cuda")
         keep.append(buf)
         comm.register(buf)
@@ -101,7 +101,7 @@ def main():
             want = SM.simulate(oc if k == "cps" else orr, want, dtype)
         got = buf.cpu().numpy()[: count * es].view(np.float32 if dtype == "f32" else np.uint16)
         try:
-            assert_bits_equal(got, want[rank], dtype, f"rank {rank} {dtype} back-to-back small calls")
+            assert_bits_equal(got, want[rank], dtype, f"rank {rank} {dtype} count={count} back-to-back calls")
         except AssertionError as e:
             print(e, flush=True)
             failures += 1
