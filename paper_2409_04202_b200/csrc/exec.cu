@@ -1381,7 +1381,11 @@ static int resident_ctas(int device) {
   }
 
 constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
-constexpr long long kPushDefaultMaxBytes = 32LL << 20;
+// Off by default: measured slower than the pull protocol on 2 and 4 B200s (4 GPUs, 1 MiB:
+// 27.7 vs 22.0 us; 16 MiB: 66.9 vs 55.4 us — the scatter step's per-block copies serialise
+// load -> store -> completion per tile, and the owner cannot start before every source's
+// scatter has landed).  Kept for A/B measurement behind AR_PUSH_MAX_MB.
+constexpr long long kPushDefaultMaxBytes = 0;
 
 // A plan the one-shot path can run with identical bits: two steps (RS, AG) whose RS step has
 // one reduce per block, every reduce over all ranks in the same order.  Returns that order.
