@@ -65,3 +65,17 @@ def test_multi_level_ranks_per_gpu(world, R):
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"hybrid_worker nproc={world} R={R}: OK" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_push_protocol_bit_exact(world):
+    """The A/B push protocol (AR_PUSH_MAX_MB, off by default) keeps the plan's bits."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT, AR_PUSH_MAX_MB="64")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29620", os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"mp_worker world={world}: OK" in r.stdout
