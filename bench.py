@@ -181,6 +181,19 @@ def cpu_baseline(world, dtype, sample_mib, force, p):
                       f"numpy single-threaded step-by-step simulation; {secs:.2f} s per AllReduce"}
 
 
+def arm_config(args, n, world, chosen, p_src):
+    """The `config` both arms report (the reference arm times the oracle on the same one)."""
+    es = 2 if args.dtype == "bf16" else 4
+    dbytes = (world if n == 1 else 1) * (args.mib * MIB // es) * es
+    return {"workload": (f"C4: GenTree-plan AllReduce, {args.dtype}, {args.mib} MiB per rank, "
+                         + (f"{world} ranks emulated on 1 GPU (8 ranks/GPU, C5 mode)" if n == 1
+                            else f"{n} ranks = {n} GPUs over NVLink/NVSwitch")),
+            "ranks": world, "bytes_per_rank": args.mib * MIB, "plan": chosen,
+            "plan_source": args.force or f"GenTree with {p_src} GenModel params",
+            "l2": f"working set {dbytes / MIB:.0f} MiB per GPU > 126 MB L2 (no flush needed)",
+            "ctas_per_rank": args.ctas or "auto"}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle timed as the reference arm (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -188,9 +201,16 @@ def run_reference(args):
         return
     n = args.gpus
     world = args.ranks if n == 1 else n
-    p, _ = model_params(world, emulated=n == 1)
+    p, p_src = model_params(world, emulated=n == 1)
     es = 2 if args.dtype == "bf16" else 4
     count = int(args.cpu_sample_mib * MIB) // es
+    from oracle import gentree as GT
+    from oracle import topology as T
+    from oracle import genmodel as OG
+    op = OG.Params(p["alpha"], p["beta"], p["gamma"], p["delta"], p["epsilon"], int(p["w_t"]))
+    _, reps = GT.gentree(T.parse_topology(single_switch_doc(world, p)), args.mib * MIB // es, es, params=op,
+                         force=args.force)
+    chosen = reps[-1].chosen
     for _ in range(min(args.warmup, 1)):
         oracle_sample_time(world, args.dtype, count, args.force, p)
     times = [oracle_sample_time(world, args.dtype, count, args.force, p) for _ in range(max(1, min(args.steps, 3)))]
@@ -200,11 +220,11 @@ def run_reference(args):
             "n_gpus": n, "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": round(t * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic",
-            "config": {"workload": f"C4 {'emulated ' + str(world) + ' ranks/GPU' if n == 1 else str(n) + ' ranks'}"
-                                   f", {args.dtype}, bounded sample of the {args.mib} MiB/rank buffer",
-                       "ranks": world, "bytes_per_rank": count * es, "plan": args.force or "gentree"},
+            "config": arm_config(args, n, world, chosen, p_src),
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": f"{world} ranks x {count} elements per step"},
+                             "sample": f"each step: the oracle's step-by-step simulation of the same plan on a "
+                                       f"bounded sample, {world} ranks x {count} {args.dtype} elements "
+                                       f"({args.cpu_sample_mib:g} MiB/rank), numpy single-threaded"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -421,13 +441,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic",
-        "config": {"workload": (f"C4: GenTree-plan AllReduce, {args.dtype}, {args.mib} MiB per rank, "
-                                + (f"{world} ranks emulated on 1 GPU (8 ranks/GPU, C5 mode)" if n == 1
-                                   else f"{n} ranks = {n} GPUs over NVLink/NVSwitch")),
-                   "ranks": world, "bytes_per_rank": nbytes, "plan": chosen,
-                   "plan_source": args.force or f"GenTree with {p_src} GenModel params",
-                   "l2": f"working set {dbytes / MIB:.0f} MiB per GPU > 126 MB L2 (no flush needed)",
-                   "ctas_per_rank": args.ctas or "auto"},
+        "config": arm_config(args, n, world, chosen, p_src),
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
