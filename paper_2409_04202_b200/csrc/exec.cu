@@ -981,6 +981,7 @@ struct ar_comm {
   bool store_tma = true;                       // bulk-copy stores of results (AR_EXEC_STORE=regs: st.global)
   int stages = kDefStages, stage_bytes = kDefStageBytes;   // AR_STAGES, AR_STAGE_KB
   unsigned int jitter_ns = 0;                  // AR_JITTER_NS (stress testing)
+  bool plain_launch = false;                   // AR_LAUNCH=plain (see launch_exec)
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
@@ -1445,6 +1446,7 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_STAGE_KB")) c->stage_bytes = std::max(4, std::atoi(v)) * 1024;
   while (dyn_smem_bytes(c->stages, c->stage_bytes) > kMaxDynSmem) c->stage_bytes -= 1024;
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
+  if (const char *v = std::getenv("AR_LAUNCH")) c->plain_launch = std::string(v) == "plain";
   if (!c->local && c->rpp == 1) {
     c->push_max_bytes = kPushDefaultMaxBytes;
     if (const char *v = std::getenv("AR_PUSH_MAX_MB")) c->push_max_bytes = std::strtoll(v, nullptr, 10) << 20;
@@ -1836,6 +1838,18 @@ int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *ne
   })
 }
 
+// Cooperative launch guarantees the co-residency the intra-GPU CTA waits need; a plain launch
+// of the same grid (1 CTA per SM, grid <= resident capacity) is co-resident whenever the GPU
+// is otherwise idle — AR_LAUNCH=plain selects it for latency measurements.
+static void launch_exec(ar_comm *c, dim3 grid, void **args, cudaStream_t stream) {
+  const size_t smem = c->bulk ? dyn_smem_bytes(c->stages, c->stage_bytes) : 0;
+  if (c->plain_launch) {
+    CUDA_OK(cudaLaunchKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args, smem, stream));
+  } else {
+    CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args, smem, stream));
+  }
+}
+
 static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream,
                      int op = AR_OP_SUM) {
   if (!plan || !c || !dptr) throw InvalidArg("null argument");
@@ -1882,8 +1896,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     ++c->epoch;
     c->fast_args.avg_n = avg_n;
     void *args[] = {&c->fast_args};
-    CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
-                                        c->bulk ? dyn_smem_bytes(c->stages, c->stage_bytes) : 0, (cudaStream_t)stream));
+    launch_exec(c, grid, args, (cudaStream_t)stream);
     c->last_launches = 1;
     return AR_OK;
   }
@@ -1975,8 +1988,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   c->fast_nctas = c->nctas;
   c->fast_valid = true;
   void *args[] = {&a};
-  CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_exec_kernel, grid, dim3(kThreads), args,
-                                      c->bulk ? dyn_smem_bytes(c->stages, c->stage_bytes) : 0, (cudaStream_t)stream));
+  launch_exec(c, grid, args, (cudaStream_t)stream);
   c->last_launches = 1;
   return AR_OK;
 }
