@@ -310,9 +310,25 @@ def mtrace(args):
             comm.set_trace(True)
             ex = G.Executor(plan, comm, buf)
             dist.barrier()
+            for _ in range(args.steady):    # back-to-back calls: the trace keeps the last one
+                ex()
             ex()
             tr = comm.read_trace().astype(np.int64)[0]
             comm.set_trace(False)
+            if args.steady:
+                # every rank's phases of the same (last) call on one clock: %globaltimer
+                allt = [None] * world
+                dist.all_gather_object(allt, tr.tolist())
+                if rank == 0:
+                    g0 = min(min(x[0] for x in a_ if x[-1] > 0) for a_ in allt)
+                    for q, a_ in enumerate(allt):
+                        a_ = np.array(a_)
+                        u = [c for c in range(a_.shape[0]) if a_[c, -1] > 0]
+                        med = lambda j: round(float(np.median([(a_[c, j] - g0) / 1e3 for c in u])), 2)
+                        nst2 = len(plan.lowering()["ranks"][q]["steps"])
+                        print(json.dumps({"mode": "mtrace-steady", "rank": q, "bytes": nbytes, "start": med(0),
+                                          "steps": [[med(1 + 3 * i), med(2 + 3 * i), med(3 + 3 * i)]
+                                                    for i in range(nst2)], "end": med(-1)}), flush=True)
             nst = len(plan.lowering()["ranks"][rank]["steps"])
             t0 = tr[:, 0].min()
             C = comm_ctas = tr.shape[0]
@@ -442,6 +458,7 @@ if __name__ == "__main__":
     ap.add_argument("--kmax", type=int, default=8)
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--ctas", type=int, default=0, help="CTAs per rank (0 = the comm's default)")
+    ap.add_argument("--steady", type=int, default=0, help="mtrace: back-to-back calls before the traced one")
     a = ap.parse_args()
     if a.mode in ("sweep", "cps"):
         multi(a)
