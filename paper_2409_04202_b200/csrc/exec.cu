@@ -693,6 +693,21 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       // store(s) after it are cumulative over them (PTX memory model: bar.sync synchronises
       // the CTA, st.release is a release pattern).  fence_mode 0 additionally fences every
       // thread at system scope (membar.sys per thread: ~10 us on B200, measured).
+      if (st.slot == 0 && st.op_count == 0 && a.fence_mode != 0) {
+        // entry flag: this kernel wrote nothing yet, and the buffer it announces was made
+        // final by stream order (earlier kernels) and by the previous call's exit waits, so
+        // there is nothing for a release to order — a relaxed system-scope store suffices
+        // (st.release.sys costs ~5 us on B200 even with no prior writes: measured with
+        // `harness.py mtrace --steady`)
+        for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
+          const int consumer = a.ranks[st.notify_begin + i];
+          asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(flag_ptr(a, consumer, st.slot, me, cta)),
+                       "l"(epoch)
+                       : "memory");
+        }
+        AR_TRACE(3 + 3 * si);
+        continue;
+      }
       if (a.fence_mode == 0) __threadfence_system();
       __syncthreads();
       if (a.fence_mode == 2) {
