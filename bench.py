@@ -106,48 +106,62 @@ def single_switch_doc(world, p):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled DURING the timed region: an NVML thread polls every
+    ~2 ms between start() and stop() (the timed region of a 256 MiB step lasts only ~10-15 ms,
+    shorter than nvidia-smi's 100 ms period); nvidia-smi is the fallback."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
-        self.p = None
-        self.out = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+        self.rows = []
+        self.err = None
 
     def start(self):
+        import threading
         try:
-            self.f = open(self.out, "w")
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:   # no NVML: nvidia-smi one-shot queries in the thread
+            h, self.max_mhz, self.err = None, None, str(e)[:80]
+        self.stop_flag = False
+
+        def poll():
+            while not self.stop_flag:
+                try:
+                    if h is not None:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons",
+                                     getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons", None))(h)
+                        pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    else:
+                        out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                                              "--format=csv,noheader,nounits"], capture_output=True, text=True).stdout
+                        sm, mx = (int(x) for x in out.strip().split(","))
+                        self.max_mhz, rs, pw = mx, 0, 0.0
+                    self.rows.append((sm, rs, pw))
+                except Exception as e:
+                    self.err = str(e)[:80]
+                time.sleep(0.002)
+
+        self.t = threading.Thread(target=poll, daemon=True)
+        self.t.start()
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 3.0:   # sampling is live before timing starts
+            time.sleep(0.001)
+        self.rows.clear()
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.close()
-        rows = []
-        with open(self.out) as f:
-            for line in f:
-                parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9 and parts[1].isdigit():
-                    rows.append(parts)
+        self.stop_flag = True
+        self.t.join(timeout=5)
+        rows = self.rows
         if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = [int(r[1]) for r in rows]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][2]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3] not in ("[N/A]", ""))}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples: " + str(self.err)]}
+        reasons = sorted({k for _, rs, _ in rows for k, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(rows), "power_w_max": round(max(r[2] for r in rows), 1), "source": "nvml, 2 ms"}
 
 
 def busbw(bytes_per_rank, ranks, seconds):
