@@ -749,6 +749,87 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------ flat single-step path
+// Emulated ranks (all buffers on this GPU) and a CPS-shaped plan: the plan is one fused step
+// whose ops (one per owner block) touch disjoint regions, and every input was written before
+// the launch — so no flag is needed at all.  The ops' 16-byte vectors are concatenated and
+// split evenly over every SM (148 CTAs instead of floor(148/R)·R), each CTA running the same
+// bulk-copy pipeline and summation order as ar_exec_kernel; CTA 0 also does the unaligned
+// heads/tails.  Bits are the plan's.
+struct FlatArgs {
+  char *base;
+  long long stride, count;
+  int world, esize, avg_n;
+  int order[AR_MAX_RANKS];
+  int stages, stage_bytes;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_constant__ FlatArgs a) {
+  __shared__ OpShared sh;
+  __shared__ Pipe pp;
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  const bool bf16 = a.esize == 2;
+  const long long E = 16 / a.esize;
+  if (threadIdx.x == 0) {
+    pp.stages = a.stages;
+    pp.stage_bytes = a.stage_bytes;
+    for (int st = 0; st < a.stages; st++) {
+      mbar_init(&pp.full[st], 1);
+      mbar_init(&pp.empty[st], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // total whole vectors over all owner blocks
+  long long total = 0;
+  for (int r = 0; r < a.world; r++) {
+    const long long off = a.count / a.world * r + min((long long)r, a.count % a.world);
+    const long long len = a.count / a.world + (r < a.count % a.world ? 1 : 0);
+    const long long vb = (off * a.esize + 15) / 16, ve = (off + len) * a.esize / 16;
+    if (ve > vb) total += ve - vb;
+  }
+  const long long my0 = total * blockIdx.x / gridDim.x, my1 = total * (blockIdx.x + 1) / gridDim.x;
+  uint32_t g = 0;
+  long long acc = 0;
+  for (int r = 0; r < a.world; r++) {
+    const long long off = a.count / a.world * r + min((long long)r, a.count % a.world);
+    const long long len = a.count / a.world + (r < a.count % a.world ? 1 : 0);
+    const long long vb = (off * a.esize + 15) / 16, ve = (off + len) * a.esize / 16;
+    const long long nv = ve > vb ? ve - vb : 0;
+    const long long lo = max(my0, acc), hi = min(my1, acc + nv);
+    const bool mine_vec = lo < hi;
+    const bool mine_scalar = blockIdx.x == 0 && len > 0 && (nv == 0 || vb * 16 > off * a.esize ||
+                                                            ve * 16 < (off + len) * a.esize);
+    if (mine_vec || mine_scalar) {
+      __syncthreads();
+      if (threadIdx.x < a.world) {
+        sh.src[threadIdx.x] = (const uint4 *)(a.base + a.stride * a.order[threadIdx.x]);
+        sh.dst[threadIdx.x] = (uint4 *)(a.base + a.stride * threadIdx.x);
+      }
+      if (threadIdx.x == 0) {
+        sh.nsrc = a.world;
+        sh.ndst = a.world;
+        sh.div = a.avg_n;
+      }
+      __syncthreads();
+      if (mine_vec) {
+        const size_t v0 = (size_t)(vb + lo - acc), v1 = (size_t)(vb + hi - acc);
+        if (bf16) body_dispatch_bulk_st<true>(sh, v0, v1, g, dyn_smem, pp);
+        else body_dispatch_bulk_st<false>(sh, v0, v1, g, dyn_smem, pp);
+      }
+      if (mine_scalar) {
+        if (nv == 0) {
+          scalar_elems(sh, off, off + len, bf16);
+        } else {
+          if (vb * 16 > off * a.esize) scalar_elems(sh, off, vb * E, bf16);
+          if (ve * 16 < (off + len) * a.esize) scalar_elems(sh, ve * E, off + len, bf16);
+        }
+      }
+    }
+    acc += nv;
+  }
+}
+
 // ------------------------------------------------------------------ low-latency one-shot path
 // Small messages on one rank per GPU, CPS-shaped plans (one fan-in-N reduce per block, every
 // block with the same input order): every rank pushes its whole input to every peer's
@@ -997,6 +1078,7 @@ struct ar_comm {
   int stages = kDefStages, stage_bytes = kDefStageBytes;   // AR_STAGES, AR_STAGE_KB
   unsigned int jitter_ns = 0;                  // AR_JITTER_NS (stress testing)
   bool plain_launch = false;                   // AR_LAUNCH=plain (see launch_exec)
+  bool flat = true;                            // emulated single-step plans via ar_flat_kernel (AR_FLAT=0: off)
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
@@ -1378,6 +1460,7 @@ static int resident_ctas(int device) {
   int nsm = 0, per = 0;
   CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   CUDA_OK(cudaFuncSetAttribute(ar_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  CUDA_OK(cudaFuncSetAttribute(ar_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, kMaxDynSmem));
   return nsm * std::max(per, 1);
 }
@@ -1462,6 +1545,7 @@ static void init_comm(ar_comm *c) {
   while (dyn_smem_bytes(c->stages, c->stage_bytes) > kMaxDynSmem) c->stage_bytes -= 1024;
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
   if (const char *v = std::getenv("AR_LAUNCH")) c->plain_launch = std::string(v) == "plain";
+  if (const char *v = std::getenv("AR_FLAT")) c->flat = std::string(v) != "0";
   if (!c->local && c->rpp == 1) {
     c->push_max_bytes = kPushDefaultMaxBytes;
     if (const char *v = std::getenv("AR_PUSH_MAX_MB")) c->push_max_bytes = std::strtoll(v, nullptr, 10) << 20;
@@ -1901,6 +1985,27 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       const long long lines = (la.bytes + 7) / 8;
       const int ctas = (int)std::max(1LL, std::min<long long>(c->ll_ctas, (lines + kThreads - 1) / kThreads));
       ar_ll_kernel<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      CUDA_OK(cudaGetLastError());
+      c->last_launches = 1;
+      return AR_OK;
+    }
+  }
+  if (c->local && c->flat && c->bulk && c->store_tma && c->trace == nullptr) {
+    // emulated ranks, CPS-shaped plan: one flag-free launch over every SM (ar_flat_kernel)
+    auto lit = c->ll_shape.find(plan->uid);
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+    if (!lit->second.empty()) {
+      FlatArgs fa{};
+      fa.base = (char *)dptr;
+      fa.stride = (long long)ar_rank_stride_bytes(count, dtype);
+      fa.count = (long long)count;
+      fa.world = c->world;
+      fa.esize = plan->esize;
+      fa.avg_n = avg_n;
+      for (int k = 0; k < c->world; k++) fa.order[k] = lit->second[k];
+      fa.stages = c->stages;
+      fa.stage_bytes = c->stage_bytes;
+      ar_flat_kernel<<<c->max_ctas, kThreads, dyn_smem_bytes(c->stages, c->stage_bytes), (cudaStream_t)stream>>>(fa);
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
       return AR_OK;

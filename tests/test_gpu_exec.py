@@ -294,3 +294,14 @@ def test_rearrangement_and_acps(shape):
     from tests.topologies import cross_dc
     world = shape[0] * shape[1] + shape[2] * shape[3]
     run_emulated(cross_dc(*shape), world, 123457, "bf16")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_emulated_cps_flag_protocol(dtype, monkeypatch):
+    """Emulated CPS plans normally run flag-free (ar_flat_kernel); AR_FLAT=0 keeps them on the
+    step-table kernel and its flag protocol — both must give the plan's bits."""
+    monkeypatch.setenv("AR_FLAT", "0")
+    for world in (3, 8):
+        for count in (world * 4096 + 7, 300001):
+            run_emulated(single_switch(world), world, count, dtype, force="cps", calls=2)
+            run_emulated(single_switch(world), world, count, dtype, force="cps", red="avg")
