@@ -343,14 +343,15 @@ def main():
         hbm_peak, hbm_src = load_peaks()
         alg_bytes = 2 * world * nbytes          # every rank buffer read once + written once
         achieved = alg_bytes / kern_t / 1e9
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+        roof = {"kernel": comm.last_kernel(), "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
+                "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": alg_bytes, "peak_source": hbm_src}
         # DRAM traffic per launch from the committed ncu --set full capture of this config
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
                 tr = json.load(f).get(f"emulated:r{world}:{args.dtype}:{nbytes}:{chosen}")
-            if tr and not args.ctas:
+            if tr and not args.ctas and tr.get("kernel", "ar_exec_kernel") == comm.last_kernel():
                 roof["traffic"] = tr["traffic_bytes_per_launch"]
                 roof["traffic_source"] = tr["source"]
         except (OSError, ValueError):
@@ -358,7 +359,8 @@ def main():
     else:
         wire = 2 * (n - 1) * nbytes / n          # Eq. 2: bytes per direction per GPU
         achieved = wire / kern_t / 1e9
-        roof = {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+        roof = {"kernel": comm.last_kernel(), "bound": "nvlink", "achieved": round(achieved, 1),
+                "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                 "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": int(wire),
                 "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
@@ -460,7 +462,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
-        "gpu_launches_note": "one cooperative launch of ar_exec_kernel per step (per process)",
+        "gpu_launches_note": f"one launch of {comm.last_kernel()} per step (per process)",
         "clocks": clk,
         "genmodel": {"predicted_ms": round(pred * 1e3, 4), "measured_ms": round(t_step * 1e3, 4),
                      "pred_err": round(abs(pred - t_step) / t_step, 4), "params": pred_src,

@@ -253,6 +253,10 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *comm, void *dptr, void *ho
 
 /* Device kernels launched by the last allreduce_exec of this comm (per rank, per call). */
 int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
+/* Name of the kernel the last allreduce_exec of this comm launched: "ar_exec_kernel" (the
+ * step-table kernel and its flag protocol), "ar_ll_kernel" (one-shot small-message path) or
+ * "ar_flat_kernel" (emulated single-step plans); "" before the first call.  Static storage. */
+const char *ar_comm_last_kernel(ar_comm *comm);
 
 /* Tracing: when enabled, thread 0 of every CTA writes %globaltimer (ns) at kernel
  * start, after each step's waits, after its ops, after its notifies, and at exit, into

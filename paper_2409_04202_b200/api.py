@@ -260,6 +260,9 @@ class Comm:
     def async_error(self):
         check(lib.ar_comm_get_async_error(self._h))
 
+    def last_kernel(self) -> str:
+        return lib.ar_comm_last_kernel(self._h).decode()
+
     def last_launch_count(self) -> int:
         k = ctypes.c_int32()
         check(lib.ar_comm_last_launch_count(self._h, ctypes.byref(k)))

@@ -1066,6 +1066,7 @@ struct ar_comm {
   unsigned long long *err = nullptr;
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
   int last_launches = 0;
+  const char *last_kernel = "";                // kernel of the last allreduce_exec (ar_comm_last_kernel)
   bool bulk = true;                            // cp.async.bulk-staged body (AR_EXEC_BODY=regs: register body)
   // launch-argument cache for back-to-back calls with the same plan and buffer
   bool fast_valid = false;
@@ -1780,6 +1781,8 @@ int ar_comm_destroy(ar_comm *c) {
   return AR_OK;
 }
 
+const char *ar_comm_last_kernel(ar_comm *c) { return c ? c->last_kernel : ""; }
+
 int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
   if (!c || !kernels) { set_error("null argument"); return AR_EINVAL; }
   *kernels = c->last_launches;
@@ -1987,6 +1990,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       ar_ll_kernel<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
+      c->last_kernel = "ar_ll_kernel";
       return AR_OK;
     }
   }
@@ -2008,6 +2012,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       ar_flat_kernel<<<c->max_ctas, kThreads, dyn_smem_bytes(c->stages, c->stage_bytes), (cudaStream_t)stream>>>(fa);
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
+      c->last_kernel = "ar_flat_kernel";
       return AR_OK;
     }
   }
@@ -2018,6 +2023,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     void *args[] = {&c->fast_args};
     launch_exec(c, grid, args, (cudaStream_t)stream);
     c->last_launches = 1;
+    c->last_kernel = "ar_exec_kernel";
     return AR_OK;
   }
   const size_t bytes = count * (size_t)plan->esize;
@@ -2110,6 +2116,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   void *args[] = {&a};
   launch_exec(c, grid, args, (cudaStream_t)stream);
   c->last_launches = 1;
+  c->last_kernel = "ar_exec_kernel";
   return AR_OK;
 }
 
