@@ -2,7 +2,7 @@
 GenModel's plan-vs-NVLS choice against the measured winner.
 
     python tools/fit_nvls.py profiles/round1/c2/sweep_n4_f32_nvls16.jsonl \
-        profiles/round1/c2/sweep_n2_f32_nvls16.jsonl [--timing graph] [--min-bytes 1048576] [--install]
+        profiles/round1/c2/sweep_n2_f32_nvls16.jsonl [--timing graph] [--min-bytes 2097152] [--install]
 
 Writes profiles/genmodel_fit_nvls_<timing>.json (fit, per-row prediction errors, choice
 accuracy); --install also writes profiles/genmodel_params_nvls.json for bench.py."""
@@ -45,7 +45,7 @@ def main():
     choices = []
     for r in nv:
         key = (r["n"], r["bytes"])
-        if key not in gt:
+        if key not in gt or r["bytes"] < a.min_bytes:   # below: the plan side runs the one-shot path
             continue
         dtype = r.get("dtype", "f32")
         es = 4 if dtype == "f32" else 2

@@ -71,7 +71,9 @@ def main():
                "points": [{"x": int(x), "t_per_add_s": float(y)} for x, y in zip(xs, ys)],
                "strictly_decreasing": bool(np.all(np.diff(ys) < 0))}
     cps = [r for r in load(a.cps, a.timing) if r["plan"] == "cps"]
-    rows = [(r["n"], r["bytes"], r["t_mean"]) for r in cps]
+    # rows at or below the one-shot cut-off (1.5 MiB/(N-1)) run ar_ll_kernel, whose step
+    # structure GenModel's executed-plan view does not describe: --min-bytes excludes them
+    rows = [(r["n"], r["bytes"], r["t_mean"]) for r in cps if r["bytes"] >= a.min_bytes]
     nmax = max(n for n, _, _ in rows)
     # w_t: from the x-to-x fan-in test when given ("no incast for 2 <= x <= w_t"),
     # else scanned by the fit
