@@ -73,8 +73,10 @@ def ncu_section(out):
         out.append(f"* `{k}`: DRAM traffic {v['traffic_bytes_per_launch'] / 1e9:.4f} GB per launch "
                    f"(read {v['dram_read'] / 1e9:.4f}, write {v['dram_write'] / 1e9:.4f}), "
                    f"{v['duration_us']} µs cold; source {v['source']}.")
-    out.append("* Summary with stall reasons: `round1/ncu_exec_emulated8_bf16_256MiB.md`; launch list:\n"
-               "  `round1/ncu_launches_bench_n1.csv` (`ar_exec_kernel` is the only kernel in the timed\n"
+    kern = next(iter(tr.values())).get("kernel", "ar_exec_kernel")
+    summ = next(iter(tr.values())).get("summary", "round1/ncu_exec_emulated8_bf16_256MiB.md")
+    out.append(f"* Summary with stall reasons: `{summ}`; launch list:\n"
+               f"  `round1/ncu_launches_bench_n1.csv` (`{kern}` is the only kernel in the timed\n"
                "  region; `fill_kernel` launches are input set-up).  Algorithmic bytes per launch =\n"
                "  2·8·256 MiB = 4.295 GB, so traffic/algorithmic ≈ 0.99: no re-reads.\n")
 
