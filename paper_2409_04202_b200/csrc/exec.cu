@@ -1248,6 +1248,10 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
   // the producer op intersects its own slice of the consumer op (both sliced by the kernel's
   // rule), so dependent steps pipeline CTA by CTA.  Entry waits (t's input ready) are paired.
   using WaitKey = std::tuple<int, int, int, long long, long long, long long, long long>;
+  // AR_WAITS=full: every inter-step dependency waits for all producer CTAs (no CTA-level
+  // pipelining of dependent steps) — the A/B baseline for the range waits
+  const char *wenv = std::getenv("AR_WAITS");
+  const bool full_waits = wenv && std::string(wenv) == "full";
   std::vector<std::vector<std::set<WaitKey>>> wl(n, std::vector<std::set<WaitKey>>(S));
   std::vector<std::map<int, int>> exitdeps(n);
   for (int s = 0; s < S; s++)
@@ -1260,7 +1264,8 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
             if (x.step >= s) continue;
             if (!write && !x.write) continue;
             if (!overlap(o.off, o.len, x.off, x.len)) continue;
-            d.insert(WaitKey{x.rank, x.step + 1, kWaitRange, x.off, x.len, o.off, o.len});
+            if (full_waits) d.insert(WaitKey{x.rank, x.step + 1, kWaitFull, 0, 0, 0, 0});
+            else d.insert(WaitKey{x.rank, x.step + 1, kWaitRange, x.off, x.len, o.off, o.len});
           }
         };
         for (int q : o.src) visit(q, false);
