@@ -169,3 +169,23 @@ def test_lowered_avg_divides_once_at_the_final_reduce(doc, world, force):
         got = interpret(low, xs, ctas=rnd.choice([1, 2, 3]), calls=2, rnd=rnd, avg=True)
         for r in range(world):
             assert np.array_equal(got[r].view(np.uint32), want[r].view(np.uint32)), (force, trial, r)
+
+
+def test_full_waits_variant_is_also_correct(monkeypatch):
+    """AR_WAITS=full (the A/B baseline of the range waits) replaces every inter-step range wait
+    by a wait on all producer CTAs; the protocol stays correct under random schedules."""
+    monkeypatch.setenv("AR_WAITS", "full")
+    doc, world = single_switch(8), 8
+    for force in ("ring", "hcps:4,2", "rhd"):
+        count = 37 * world + 5
+        plan = G.Plan.from_topology(doc, count, "f32", None, force)
+        low = plan.lowering()
+        kinds = {w[2] for r in low["ranks"] for st in r["steps"] for w in st["waits"]}
+        assert 2 not in kinds and 1 in kinds
+        oplan, _ = GT.gentree(T.parse_topology(doc), count, 4, force=force)
+        xs = [GEN.generate(3, r, count, "f32", "integer") for r in range(world)]
+        want = SM.simulate(oplan, SM.simulate(oplan, xs, "f32"), "f32")
+        rnd = random.Random(5)
+        got = interpret(low, xs, ctas=3, calls=2, rnd=rnd)
+        for r in range(world):
+            assert np.array_equal(got[r], want[r])
