@@ -190,10 +190,13 @@ int ar_comm_create_multi(int32_t proc, int32_t nproc, int32_t ranks_per_proc, in
 
 /* Emulated communicator: all `world` ranks live in this process on one device (each rank's
  * buffer is a separate region of device memory; "8 ranks/GPU" of config C5).  The executor
- * runs all ranks in one cooperative launch, with the same step tables and flag protocol. */
+ * runs all ranks in one cooperative launch, with the same step tables and flag protocol;
+ * single-step (CPS-shaped) plans run flag-free over every SM instead (ar_flat_kernel, same
+ * bits; AR_FLAT=0 disables). */
 int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out);
 
-/* Number of CTAs per rank used by allreduce_exec (0 = automatic).  Same value on all ranks. */
+/* Number of CTAs per rank used by the step-table kernel (0 = automatic).  Same value on all
+ * ranks.  The flat and one-shot paths size their own grids and ignore it. */
 int ar_comm_set_ctas(ar_comm *comm, int32_t ctas);
 
 /* Export `bytes` of device memory at `dptr` (16-byte aligned; may be an interior pointer of
