@@ -1092,6 +1092,10 @@ struct ar_comm {
   bool ll_opened = false;
   int ll_ctas = 32;
   std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
+  // chunked end-to-end path (exec_host_chunked)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> evs;
+  std::map<std::pair<uint64_t, uint64_t>, gt_plan *> sub_plans;
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
 };
@@ -1777,6 +1781,10 @@ int ar_comm_destroy(ar_comm *c) {
   cudaDeviceSynchronize();
   for (auto &kv : c->lowered) free_lowered(kv.second);
   for (auto &kv : c->lowered_push) free_lowered(kv.second);
+  for (auto &kv : c->sub_plans) delete kv.second;
+  for (cudaEvent_t e : c->evs) cudaEventDestroy(e);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   for (auto &kv : c->ipc_opened) cudaIpcCloseMemHandle(kv.second);
   cudaFree(c->sig_local);
   cudaFree(c->ll_scratch);
@@ -1957,8 +1965,10 @@ static void launch_exec(ar_comm *c, dim3 grid, void **args, cudaStream_t stream)
   }
 }
 
+// stride_override: bytes between consecutive hosted ranks' buffers when dptr points into the
+// middle of larger rank buffers (the chunked end-to-end path); 0 = derived from count.
 static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream,
-                     int op = AR_OP_SUM) {
+                     int op = AR_OP_SUM, uint64_t stride_override = 0) {
   if (!plan || !c || !dptr) throw InvalidArg("null argument");
   if (op != AR_OP_SUM && op != AR_OP_AVG) throw InvalidArg("unknown reduction op");
   const int avg_n = op == AR_OP_AVG ? plan->plan.n : 0;
@@ -2006,7 +2016,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     if (!lit->second.empty()) {
       FlatArgs fa{};
       fa.base = (char *)dptr;
-      fa.stride = (long long)ar_rank_stride_bytes(count, dtype);
+      fa.stride = (long long)(stride_override ? stride_override : ar_rank_stride_bytes(count, dtype));
       fa.count = (long long)count;
       fa.world = c->world;
       fa.esize = plan->esize;
@@ -2034,22 +2044,28 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   const size_t bytes = count * (size_t)plan->esize;
   ExecArgs a{};
   if (c->local) {
-    const uint64_t stride = ar_rank_stride_bytes(count, dtype);
+    const uint64_t stride = stride_override ? stride_override : ar_rank_stride_bytes(count, dtype);
     for (int r = 0; r < c->world; r++) {
       a.bufs[r] = (char *)dptr + stride * r;
       a.sigs[r] = c->sig[r];
     }
   } else {
     // several ranks per process: consecutive rank buffers at the emulated stride
-    const uint64_t stride = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) : 0;
-    const size_t need = c->rpp > 1 ? stride * c->rpp : bytes;
+    const uint64_t stride =
+        c->rpp > 1 ? (stride_override ? stride_override : ar_rank_stride_bytes(count, dtype)) : 0;
+    const size_t need = c->rpp > 1 ? stride * (c->rpp - 1) + bytes : bytes;
+    // dptr may point inside a registered buffer (same offset on every rank)
     Registration *reg = nullptr;
+    size_t inner = 0;
     for (auto &r : c->regs)
-      if (r.local == (char *)dptr && r.opened && r.bytes >= need) reg = &r;
+      if (r.opened && (char *)dptr >= r.local && (char *)dptr + need <= r.local + r.bytes) {
+        reg = &r;
+        inner = (size_t)((char *)dptr - r.local);
+      }
     if (!reg) throw InvalidArg("buffer is not registered and opened on this communicator (or too small)");
     for (int r = 0; r < c->world; r++) {
       char *base = reg->peer[r / c->rpp];
-      a.bufs[r] = base ? base + stride * (r % c->rpp) : nullptr;
+      a.bufs[r] = base ? base + inner + stride * (r % c->rpp) : nullptr;
       a.sigs[r] = c->sig[r];
       if (!a.bufs[r] || !a.sigs[r]) throw InvalidArg("peer buffer not opened");
     }
@@ -2134,15 +2150,85 @@ int allreduce_exec_op(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t coun
   SYS_TRY({ return exec_impl(plan, c, dptr, count, dtype, stream, op); })
 }
 
+// A plan whose every element is summed in ascending rank order by one reduce (natural CPS):
+// any element range can then run as its own CPS plan with the same bits.
+static bool ascending_cps(const Plan &p) {
+  std::vector<int> ord = ll_order_of(p);
+  if (ord.empty()) return false;
+  for (int i = 0; i < (int)ord.size(); i++)
+    if (ord[i] != i) return false;
+  return true;
+}
+
+// End to end with host buffers, pipelined: the element range is split into chunks run as
+// natural-CPS sub-plans (same bits, see ascending_cps); chunk k's H2D, AllReduce and D2H run
+// on three streams so the copies of neighbouring chunks overlap each other (PCIe is full
+// duplex) and the kernels.  Plans of other shapes copy, execute and copy back in sequence.
+static void exec_host_chunked(const gt_plan *plan, ar_comm *c, char *dptr, char *host, uint64_t count,
+                              int32_t dtype, cudaStream_t s, int chunks) {
+  const int es = plan->esize;
+  const size_t stride = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) : count * (size_t)es;
+  const uint64_t per = ((count + chunks - 1) / chunks + 127) / 128 * 128;
+  if (!c->h2d) {
+    CUDA_OK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  }
+  while ((int)c->evs.size() < 2 * chunks + 2) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->evs.push_back(e);
+  }
+  cudaEvent_t start = c->evs[0], done = c->evs[1];
+  CUDA_OK(cudaEventRecord(start, s));
+  CUDA_OK(cudaStreamWaitEvent(c->h2d, start, 0));
+  CUDA_OK(cudaStreamWaitEvent(c->d2h, start, 0));
+  for (int k = 0; k < chunks; k++) {
+    const uint64_t off = per * k;
+    if (off >= count) break;
+    const uint64_t n = std::min<uint64_t>(per, count - off);
+    auto key = std::make_pair(plan->uid, n);
+    auto it = c->sub_plans.find(key);
+    if (it == c->sub_plans.end()) {
+      gt_plan *g = new gt_plan();
+      g->plan = build_plan_natural("cps", plan->plan.n, (int64_t)n);
+      g->dtype = plan->dtype;
+      g->esize = plan->esize;
+      g->uid = next_plan_uid();
+      it = c->sub_plans.emplace(key, g).first;
+    }
+    cudaEvent_t eh = c->evs[2 + 2 * k], ec = c->evs[3 + 2 * k];
+    CUDA_OK(cudaMemcpy2DAsync(dptr + off * es, stride, host + off * es, stride, n * es, c->rpp,
+                              cudaMemcpyHostToDevice, c->h2d));
+    CUDA_OK(cudaEventRecord(eh, c->h2d));
+    CUDA_OK(cudaStreamWaitEvent(s, eh, 0));
+    int rc = exec_impl(it->second, c, dptr + off * es, n, dtype, s, AR_OP_SUM, c->rpp > 1 ? stride : 0);
+    if (rc != AR_OK) throw SysError("chunk execution failed");
+    CUDA_OK(cudaEventRecord(ec, s));
+    CUDA_OK(cudaStreamWaitEvent(c->d2h, ec, 0));
+    CUDA_OK(cudaMemcpy2DAsync(host + off * es, stride, dptr + off * es, stride, n * es, c->rpp,
+                              cudaMemcpyDeviceToHost, c->d2h));
+  }
+  CUDA_OK(cudaEventRecord(done, c->d2h));
+  CUDA_OK(cudaStreamWaitEvent(s, done, 0));
+}
+
 int allreduce_exec_host(const gt_plan *plan, ar_comm *c, void *dptr, void *host, uint64_t count, int32_t dtype,
                         void *stream) {
   SYS_TRY({
     if (!host) throw InvalidArg("null host buffer");
     if (!c) throw InvalidArg("null comm");
+    if (!plan) throw InvalidArg("null plan");
     CUDA_OK(cudaSetDevice(c->device));
     const size_t bytes = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) * c->rpp
                                     : count * (size_t)(dtype == AR_BF16 ? 2 : 4);
     cudaStream_t s = (cudaStream_t)stream;
+    int chunks = 8;
+    if (const char *v = std::getenv("AR_E2E_CHUNKS")) chunks = std::max(1, std::atoi(v));
+    if (chunks > 1 && count * (uint64_t)plan->esize >= (8u << 20) && (uint64_t)plan->plan.count == count &&
+        plan->dtype == dtype && ascending_cps(plan->plan)) {
+      exec_host_chunked(plan, c, (char *)dptr, (char *)host, count, dtype, s, chunks);
+      return AR_OK;
+    }
     CUDA_OK(cudaMemcpyAsync(dptr, host, bytes, cudaMemcpyHostToDevice, s));
     int rc = exec_impl(plan, c, dptr, count, dtype, stream);
     if (rc != AR_OK) return rc;

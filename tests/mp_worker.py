@@ -75,6 +75,32 @@ def main():
                     print(e, flush=True)
                     failures += 1
                 dist.barrier()
+    # end to end from pinned host memory (chunked natural-CPS sub-plans on interior pointers
+    # of the registered buffer; allreduce_exec_host)
+    for dtype in ("f32", "bf16"):
+        es = 4 if dtype == "f32" else 2
+        count = (9 << 20) // es + 333
+        buf = torch.zeros(count * es + 16, dtype=torch.uint8, device="cuda")
+        keep.append(buf)
+        comm.register(buf)
+        host = torch.zeros(count * es, dtype=torch.uint8, pin_memory=True)
+        xs = GEN.generate_all(seed + 2, world, count, dtype)
+        host.numpy()[:] = xs[rank].view(np.uint8)
+        plan = G.Plan.from_topology(doc, count, dtype, None, None)
+        oplan, _ = GT.gentree(T.parse_topology(doc), count, es)
+        dist.barrier()
+        G.allreduce_exec_host(plan, comm, buf, host.data_ptr(), count, dtype)
+        torch.cuda.synchronize()
+        comm.async_error()
+        want = SM.simulate(oplan, xs, dtype)[rank]
+        got = host.numpy().view(np.float32 if dtype == "f32" else np.uint16)
+        try:
+            assert_bits_equal(got, want, dtype, f"rank {rank} {dtype} host end-to-end")
+        except AssertionError as e:
+            print(e, flush=True)
+            failures += 1
+        dist.barrier()
+
     # back-to-back small calls without host syncs: the one-shot low-latency path (double-
     # buffered scratch, epoch-tagged lines) interleaved with the flag-protocol path
     # (3001 elements: one-shot path; 600_001: push protocol; ring: flag protocol)

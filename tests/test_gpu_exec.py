@@ -305,3 +305,32 @@ def test_emulated_cps_flag_protocol(dtype, monkeypatch):
         for count in (world * 4096 + 7, 300001):
             run_emulated(single_switch(world), world, count, dtype, force="cps", calls=2)
             run_emulated(single_switch(world), world, count, dtype, force="cps", red="avg")
+
+
+@pytest.mark.parametrize("force", [None, "ring"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_exec_host_end_to_end(force, dtype):
+    """allreduce_exec_host from pinned host memory: natural-CPS plans run chunked (sub-plans
+    per element range, H2D/AllReduce/D2H overlapped on three streams), other plans in one
+    piece — both must return the plan's bits in the host buffer."""
+    world = 4
+    count = (9 << 20) // (4 if dtype == "f32" else 2) + 333      # > 8 MiB per rank, ragged
+    es = 4 if dtype == "f32" else 2
+    stride = G.rank_stride_bytes(count, dtype)
+    plan = G.Plan.from_topology(single_switch(world), count, dtype, None, force)
+    comm = G.Comm.local(world, 0)
+    dbuf = torch.zeros(world * stride, dtype=torch.uint8, device="cuda")
+    host = torch.zeros(world * stride, dtype=torch.uint8, pin_memory=True)
+    xs = GEN.generate_all(SEED, world, count, dtype)
+    hv = host.numpy()
+    for r in range(world):
+        hv[r * stride: r * stride + count * es] = xs[r].view(np.uint8)
+    for _ in range(2):
+        G.allreduce_exec_host(plan, comm, dbuf, host.data_ptr(), count, dtype)
+    torch.cuda.synchronize()
+    comm.async_error()
+    oplan, _ = GT.gentree(T.parse_topology(single_switch(world)), count, es, force=force)
+    want = SM.simulate(oplan, SM.simulate(oplan, xs, dtype), dtype)
+    for r in range(world):
+        got = hv[r * stride: r * stride + count * es].view(np.float32 if dtype == "f32" else np.uint16)
+        assert_bits_equal(got, want[r], dtype, f"rank {r}")
