@@ -78,6 +78,26 @@ def fit_nvls(rows):
     return {"alpha": float(x[0]), "beta": float(x[1]), "sse": float(r @ r)}
 
 
+def fit_row(kind: str, rows):
+    """NNLS for (α, β) of a closed-form row's A and B coefficients (the "nvls" and "oneshot"
+    rows: their own fitted latency and per-byte link cost, C/D/I absorbed).  rows: (n, s, t)."""
+    from .genmodel import closed_form_terms
+    rows = average_rows(rows)
+    if len(rows) < 2 or len({s for _, s, _ in rows}) < 2:
+        raise ValueError("underdetermined: need >= 2 distinct sizes")
+    A = []
+    for n, s, _ in rows:
+        a_, bn, _, _, _, den = closed_form_terms(kind, n, int(s), 1 << 30)
+        A.append([float(a_), bn / den])
+    A = np.array(A)
+    t = np.array([r[2] for r in rows])
+    scale = np.maximum(np.abs(A).max(axis=0), 1e-300)
+    x, _ = nnls(A / scale, t)
+    x = x / scale
+    r = A @ x - t
+    return {"alpha": float(x[0]), "beta": float(x[1]), "sse": float(r @ r)}
+
+
 def split_combined(k: float, link_bytes_per_s: float):
     """β from the bandwidth, γ = k − 2β; error if that is negative."""
     beta = 1.0 / link_bytes_per_s

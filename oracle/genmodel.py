@@ -212,6 +212,12 @@ def closed_form_terms(kind: str, c: int, S: int, w_t: int, fanins: tuple = ()):
         # reduced block (S/N) plus N multicast blocks (S): B = (N+1)·S/N.  No GPU-side
         # reduce (C = D = 0) and no unicast many-to-one flows (I = 0).
         return 2, (c + 1) * S, 0, 0, 0, c
+    if kind == "oneshot":
+        # DESIGN.md reading OS1 (the executor's small-message path): one round; every rank
+        # sends its whole input to each of the N-1 others as 16-byte lines carrying 8 payload
+        # bytes (B = 2(N-1)S per direction), then reduces all N blocks itself in plan order
+        # (C = (N-1)S, D = (N+1)S); every rank receives from N-1 senders (w = N, as CPS).
+        return 1, 2 * (c - 1) * S, (c - 1) * S, (c + 1) * S, 2 * (c - 1) * S * max(c - w_t, 0), 1
     raise ValueError(f"no closed form for {kind!r}")
 
 

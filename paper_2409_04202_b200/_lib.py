@@ -68,6 +68,8 @@ _SIGS = {
                            ctypes.POINTER(GmParams), ctypes.POINTER(ctypes.c_double)]),
     "genmodel_fit_nvls": (I32, [ctypes.POINTER(GmMeasurement), SZ, ctypes.POINTER(GmParams),
                                 ctypes.POINTER(ctypes.c_double)]),
+    "genmodel_fit_row": (I32, [ctypes.c_char_p, ctypes.POINTER(GmMeasurement), SZ, ctypes.POINTER(GmParams),
+                               ctypes.POINTER(ctypes.c_double)]),
     "genmodel_choose_nvls": (I32, [P, ctypes.POINTER(GmParams), ctypes.POINTER(GmParams), ctypes.POINTER(I32),
                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "gt_plan_simulate": (I32, [P, ctypes.c_char_p, ctypes.POINTER(GmParams), ctypes.POINTER(GmBreakdown),

@@ -18,7 +18,7 @@ import json
 from . import _lib as L
 from ._lib import AR_BF16, AR_F32, GmBreakdown, GmMeasurement, GmParams, check, lib
 
-__all__ = ["GmParams", "params", "genmodel_fit", "genmodel_fit_nvls", "genmodel_closed_form", "Plan", "Comm",
+__all__ = ["GmParams", "params", "genmodel_fit", "genmodel_fit_nvls", "genmodel_fit_row", "genmodel_closed_form", "Plan", "Comm",
            "allreduce_exec", "allreduce_exec_host", "fill_synthetic", "local_reduce",
            "rank_stride_bytes", "dtype_code"]
 
@@ -68,6 +68,18 @@ def genmodel_fit_nvls(rows):
     out = GmParams()
     sse = ctypes.c_double()
     check(lib.genmodel_fit_nvls(arr, len(rows), ctypes.byref(out), ctypes.byref(sse)))
+    return out, sse.value
+
+
+def genmodel_fit_row(kind: str, rows):
+    """(α, β) of the "nvls" or "oneshot" row (genmodel_fit_row).  Returns (GmParams, sse)."""
+    rows = list(rows)
+    arr = (GmMeasurement * max(1, len(rows)))()
+    for i, (n, b, t) in enumerate(rows):
+        arr[i] = GmMeasurement(int(n), 0, int(b), float(t))
+    out = GmParams()
+    sse = ctypes.c_double()
+    check(lib.genmodel_fit_row(kind.encode(), arr, len(rows), ctypes.byref(out), ctypes.byref(sse)))
     return out, sse.value
 
 

@@ -94,14 +94,20 @@ int genmodel_fit(const gm_measurement *rows, size_t n_rows, int32_t wt_min, int3
 }
 
 int genmodel_fit_nvls(const gm_measurement *rows, size_t n_rows, gm_params *out, double *sse) {
+  return genmodel_fit_row("nvls", rows, n_rows, out, sse);
+}
+
+int genmodel_fit_row(const char *kind, const gm_measurement *rows, size_t n_rows, gm_params *out, double *sse) {
   AR_TRY({
-    if (!rows || !out) throw InvalidArg("null argument");
+    if (!kind || !rows || !out) throw InvalidArg("null argument");
+    const std::string k(kind);
+    if (k != "nvls" && k != "oneshot") throw InvalidArg("genmodel_fit_row: kind must be nvls or oneshot");
     std::vector<Measurement> m;
     for (size_t i = 0; i < n_rows; i++) {
       if (rows[i].n < 2 || rows[i].bytes < 1 || !(rows[i].seconds > 0)) throw InvalidArg("bad measurement row");
       m.push_back({rows[i].n, (double)rows[i].bytes, rows[i].seconds});
     }
-    NvlsFit f = fit_nvls(m);
+    NvlsFit f = fit_row(k, m);
     gm_params o{};
     o.alpha = f.alpha;
     o.beta = f.beta;

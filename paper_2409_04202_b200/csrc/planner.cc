@@ -710,6 +710,9 @@ static void closed_form_terms(const std::string &kind, int c, int64_t S, int w_t
   } else if (kind == "nvls") {
     // DESIGN.md reading NV1: in-switch fan-in-N reduce + multicast; (N+1)S/N per direction
     A = 2; Bn = (int64_t)(c + 1) * S; Cn = 0; Dn = 0; In = 0; den = c;
+  } else if (kind == "oneshot") {
+    // DESIGN.md reading OS1: the executor's one-shot small-message path
+    A = 1; Bn = 2 * cm1 * S; Cn = cm1 * S; Dn = (int64_t)(c + 1) * S; In = 2 * cm1 * S * over; den = 1;
   } else {
     throw InvalidArg("no closed form for " + kind);
   }
@@ -1314,7 +1317,9 @@ FitResult fit_params(const std::vector<Measurement> &rows_in, int wt_min, int wt
   throw InvalidArg("fit failed");
 }
 
-NvlsFit fit_nvls(const std::vector<Measurement> &rows_in) {
+NvlsFit fit_nvls(const std::vector<Measurement> &rows_in) { return fit_row("nvls", rows_in); }
+
+NvlsFit fit_row(const std::string &kind, const std::vector<Measurement> &rows_in) {
   std::map<std::pair<int, double>, std::vector<double>> acc;
   for (auto &r : rows_in) acc[{r.n, r.s}].push_back(r.t);
   std::vector<Measurement> rows;
@@ -1329,8 +1334,9 @@ NvlsFit fit_nvls(const std::vector<Measurement> &rows_in) {
   std::vector<std::vector<double>> A;
   std::vector<double> b;
   for (auto &r : rows) {
-    double n = r.n, s = r.s;
-    A.push_back({2.0, (n + 1) * s / n});
+    int64_t a_, bn, cn, dn, in, den;
+    closed_form_terms(kind, r.n, (int64_t)r.s, 1 << 30, {}, a_, bn, cn, dn, in, den);
+    A.push_back({(double)a_, (double)bn / (double)den});
     b.push_back(r.t);
   }
   double scale[2] = {1e-300, 1e-300};

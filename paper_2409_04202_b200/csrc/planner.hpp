@@ -133,5 +133,6 @@ struct FitResult {
 FitResult fit_params(const std::vector<Measurement> &rows, int wt_min, int wt_max);
 struct NvlsFit { double alpha = 0, beta = 0, sse = 0; };
 NvlsFit fit_nvls(const std::vector<Measurement> &rows);   // NVLS row (reading NV1)
+NvlsFit fit_row(const std::string &kind, const std::vector<Measurement> &rows);   // (α, β) of a row
 
 }  // namespace gtar

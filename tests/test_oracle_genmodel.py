@@ -249,3 +249,25 @@ def test_nvls_fit_recovers_parameters():
     f = F.fit_nvls(rows)
     assert f["alpha"] == pytest.approx(alpha, rel=1e-9)
     assert f["beta"] == pytest.approx(beta, rel=1e-9)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_oneshot_row_matches_line_count(n):
+    """Reading OS1: count the one-shot path's traffic line by line — every rank writes each
+    8-byte payload word of its S-byte input as one 16-byte line {d0, e, d1, e} into each of the
+    N-1 peers' scratch — and its local work (all N blocks reduced from N inputs)."""
+    S = 8 * 1000 * n
+    lines = S // 8
+    out = [0] * n
+    inn = [0] * n
+    for src in range(n):
+        for dst in range(n):
+            if dst != src:
+                out[src] += 16 * lines
+                inn[dst] += 16 * lines
+    A, Bn, Cn, Dn, In, den = G.closed_form_terms("oneshot", n, S, 1 << 20)
+    assert A == 1 and Fraction(Bn, den) == max(max(out), max(inn))
+    assert Fraction(Cn, den) == (n - 1) * S and Fraction(Dn, den) == (n + 1) * S and In == 0
+    # incast as CPS: every rank receives from N-1 senders (w = N, reading Q8)
+    _, _, _, _, In2, den2 = G.closed_form_terms("oneshot", n, S, 1)
+    assert Fraction(In2, den2) == max(n - 1, 0) * Fraction(Bn, den)

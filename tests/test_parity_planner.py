@@ -180,6 +180,24 @@ def test_nvls_row_and_fit_parity():
     assert sse == pytest.approx(o["sse"], rel=1e-6)
 
 
+def test_oneshot_row_and_fit_parity():
+    p = OG.Params(4e-6, 1.0e-12, 2e-13, 3e-13, 1e-14, 3)
+    for n in (2, 4, 8):
+        for S in (16, 1 << 16, 1234567):
+            same_breakdown(G.genmodel_closed_form("oneshot", n, S, lib_params(p)),
+                           OG.closed_form_f64("oneshot", n, S, p))
+    rows = [(n, s, 4e-6 + 2 * (n - 1) * s * 3e-12 * (1 + 0.02 * ((n + s) % 5))) for n in (2, 4)
+            for s in (1 << 12, 1 << 16, 1 << 19)]
+    lp, sse = G.genmodel_fit_row("oneshot", rows)
+    o = OF.fit_row("oneshot", rows)
+    assert lp.alpha == pytest.approx(o["alpha"], rel=1e-9) and lp.beta == pytest.approx(o["beta"], rel=1e-9)
+    ln, _ = G.genmodel_fit_row("nvls", [(4, 1 << 20, 2e-5), (4, 1 << 24, 5e-5), (2, 1 << 22, 3e-5)])
+    on = OF.fit_nvls([(4, 1 << 20, 2e-5), (4, 1 << 24, 5e-5), (2, 1 << 22, 3e-5)])
+    assert ln.alpha == pytest.approx(on["alpha"], rel=1e-9) and ln.beta == pytest.approx(on["beta"], rel=1e-9)
+    with pytest.raises(G.ArInvalid):
+        G.genmodel_fit_row("cps", rows)
+
+
 def test_choose_nvls():
     """genmodel_choose_nvls = (executed-plan prediction) vs (NVLS closed form)."""
     pp = G.params(alpha=9.4e-6, combined=2.93e-12, w_t=4)

@@ -226,6 +226,17 @@ def pipelining_section(out):
                "is neutral (the steps are bandwidth-bound on the same memory).\n")
 
 
+def oneshot_section(out):
+    path = os.path.join(P, "genmodel_fit_oneshot_graph.json")
+    if not os.path.exists(path):
+        return
+    f = json.load(open(path))
+    out.append("**One-shot row (reading OS1)**, T = α + 2(N−1)S·β fitted on the calls the executor ran through\n"
+               f"its small-message path ({f['rows']} rows, N = 2 and 4): α = {f['alpha'] * 1e6:.2f} µs, "
+               f"β = {f['beta']:.4g} s/B\n({f['line_gbs']:.0f} GB/s of line bytes); prediction error median "
+               f"{f['pred_err_median'] * 100:.1f} %, max {f['pred_err_max'] * 100:.1f} %.\n")
+
+
 def p2p_section(out):
     out.append("## 5. Incast probe (x-to-x, S:449) on 4×B200\n")
     out.append("| pattern | bytes | GB/s per direction per GPU |")
@@ -246,6 +257,7 @@ def main():
     c2_section(out)
     fit_section(out)
     nvls_fit_section(out)
+    oneshot_section(out)
     p2p_section(out)
     hybrid_section(out)
     gentreesimu_section(out)
