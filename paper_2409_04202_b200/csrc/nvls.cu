@@ -278,9 +278,10 @@ int ar_nvls_create(int32_t rank, int32_t world, int32_t cuda_device, uint64_t by
     std::memcpy(blob_out, &b, sizeof b);
     int nsm = 148;
     RT_CALL(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, cuda_device));
-    // few CTAs: the switch serves multimem requests best with little contention (measured on
-    // 4 x B200, bf16 256 MiB: 16 CTAs 674 GB/s busbw vs 148 CTAs 591 GB/s)
-    n->nctas = std::min(16, std::min(nsm, kNvCtaCap));
+    // few CTAs: the switch serves multimem requests best with little contention (measured:
+    // 4 x B200 bf16 256 MiB, 16 CTAs 674 GB/s busbw vs 148 CTAs 591; 2 x B200 fp32 256 MiB,
+    // 32 CTAs 402 vs 16 CTAs 361 and 148 CTAs 352 — profiles/round1/nvls_ctas)
+    n->nctas = std::min(world == 2 ? 32 : 16, std::min(nsm, kNvCtaCap));
     if (const char *v = std::getenv("AR_NVLS_CTAS")) n->nctas = std::max(1, std::min(kNvCtaCap, std::atoi(v)));
     if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) n->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
     *out = n;
