@@ -267,6 +267,12 @@ int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
  * "ar_flat_kernel" (emulated single-step plans); "" before the first call.  Static storage. */
 const char *ar_comm_last_kernel(ar_comm *comm);
 
+/* Largest message (bytes per rank) run through the one-shot small-message path (default the
+ * measured cut-off 1.5 MiB/(N−1); e.g. set it to GenModel's crossover of the "oneshot" row and
+ * the executed-plan prediction).  0 disables the path.  AR_EINVAL above the scratch capacity
+ * allocated at creation or on a communicator without one (emulated / several ranks per GPU). */
+int ar_comm_set_oneshot_max(ar_comm *comm, uint64_t bytes);
+
 /* Tracing: when enabled, thread 0 of every CTA writes %globaltimer (ns) at kernel
  * start, after each step's waits, after its ops, after its notifies, and at exit, into
  * slots_per_cta stamps per CTA ([local rank][cta][slot]; slot 0 = start, 1+3i / 2+3i / 3+3i =

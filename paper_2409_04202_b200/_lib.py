@@ -111,6 +111,7 @@ _SIGS = {
     "allreduce_exec": (I32, [P, P, P, U64, I32, P]),
     "allreduce_exec_op": (I32, [P, P, P, U64, I32, I32, P]),
     "ar_comm_last_kernel": (ctypes.c_char_p, [P]),
+    "ar_comm_set_oneshot_max": (I32, [P, U64]),
     "allreduce_exec_host": (I32, [P, P, P, P, U64, I32, P]),
     "ar_fill_synthetic": (I32, [P, U64, I32, U64, I32, I32, U64, P]),
     "ar_local_reduce": (I32, [ctypes.POINTER(P), I32, P, U64, I32, P]),

@@ -272,6 +272,10 @@ class Comm:
     def async_error(self):
         check(lib.ar_comm_get_async_error(self._h))
 
+    def set_oneshot_max(self, nbytes: int):
+        """Cut-off of the one-shot small-message path (ar_comm_set_oneshot_max)."""
+        check(lib.ar_comm_set_oneshot_max(self._h, int(nbytes)))
+
     def last_kernel(self) -> str:
         return lib.ar_comm_last_kernel(self._h).decode()
 

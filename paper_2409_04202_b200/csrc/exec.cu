@@ -1796,6 +1796,16 @@ int ar_comm_destroy(ar_comm *c) {
 
 const char *ar_comm_last_kernel(ar_comm *c) { return c ? c->last_kernel : ""; }
 
+int ar_comm_set_oneshot_max(ar_comm *c, uint64_t bytes) {
+  SYS_TRY({
+    if (!c) throw InvalidArg("null comm");
+    if (!c->ll_scratch && bytes > 0) throw InvalidArg("this communicator has no one-shot scratch");
+    if ((long long)bytes > c->ll_cap_lines * 8) throw InvalidArg("above the scratch capacity (AR_LL_MAX_KB at creation)");
+    c->ll_max_bytes = (long long)bytes;
+    return AR_OK;
+  })
+}
+
 int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
   if (!c || !kernels) { set_error("null argument"); return AR_EINVAL; }
   *kernels = c->last_launches;
