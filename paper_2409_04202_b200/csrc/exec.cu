@@ -1567,7 +1567,7 @@ static void init_comm(ar_comm *c) {
     c->ll_max_bytes = std::max(0LL, c->ll_max_bytes);
     c->push_max_bytes = std::max(0LL, c->push_max_bytes);
     if (c->ll_max_bytes > 0 || c->push_max_bytes > 0) {
-      c->ll_cap_lines = (c->ll_max_bytes + 7) / 8;
+      c->ll_cap_lines = (2 * c->ll_max_bytes + 7) / 8;   // room to raise the cut-off 2x (ar_comm_set_oneshot_max)
       c->ll_region = ((long long)2 * c->world * c->ll_cap_lines * 16 + 255) / 256 * 256;
       // one block of the largest pushed message + 16 bytes of alignment phase
       c->push_slot = ((c->push_max_bytes + c->world - 1) / c->world + 16 + 255) / 256 * 256;
