@@ -159,6 +159,32 @@ def main():
             print(e, flush=True)
             failures += 1
         dist.barrier()
+    # the one-shot cut-off is settable (ar_comm_set_oneshot_max): off, then raised to 2x
+    default_cut = min(1536 * 1024, (3 << 19) // (world - 1)) // 256 * 256
+    for cut, count in ((0, 3001), (2 * default_cut, (2 * default_cut) // 4 - 100)):
+        comm.set_oneshot_max(cut)
+        buf = torch.zeros(count * 4 + 16, dtype=torch.uint8, device="cuda")
+        keep.append(buf)
+        comm.register(buf)
+        G.fill_synthetic(buf, count, "f32", seed + 4, rank, 0)
+        plan = G.Plan.from_topology(doc, count, "f32")
+        oplan, _ = GT.gentree(T.parse_topology(doc), count, 4)
+        torch.cuda.synchronize()
+        dist.barrier()
+        G.allreduce_exec(plan, comm, buf)
+        torch.cuda.synchronize()
+        comm.async_error()
+        expect = "ar_ll_kernel" if cut else "ar_exec_kernel"
+        want = SM.simulate(oplan, GEN.generate_all(seed + 4, world, count, "f32"), "f32")[rank]
+        got = buf.cpu().numpy()[: count * 4].view(np.float32)
+        try:
+            assert comm.last_kernel() == expect, comm.last_kernel()
+            assert_bits_equal(got, want, "f32", f"rank {rank} one-shot cut-off {cut}")
+        except AssertionError as e:
+            print(e, flush=True)
+            failures += 1
+        dist.barrier()
+    comm.set_oneshot_max(default_cut)
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
