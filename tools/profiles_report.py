@@ -33,8 +33,8 @@ def size(b):
 
 def bench_section(out):
     out.append("## 1. bench.py lines (metric: AllReduce busbw, bf16, 256 MiB per rank)\n")
-    out.append("| GPUs | ranks | plan | busbw GB/s | ms/step | roofline (GB/s) | NCCL busbw | NVLS busbw | GenModel pred. err |")
-    out.append("|---|---|---|---|---|---|---|---|---|")
+    out.append("| GPUs | ranks | plan | kernel | busbw GB/s | ms/step | roofline (GB/s) | NCCL busbw | NVLS busbw | GenModel pred. err |")
+    out.append("|---|---|---|---|---|---|---|---|---|---|")
     e2e = []
     cpu = None
     for n in (1, 2, 4, 8):
@@ -45,7 +45,7 @@ def bench_section(out):
         rf = d["roofline"]
         nc = d.get("nccl", {}).get("busbw", "-")
         nv = d.get("nvls", {}).get("busbw", "-")
-        out.append(f"| {d['n_gpus']} | {d['config']['ranks']} | {d['config']['plan']} | {d['value']} | "
+        out.append(f"| {d['n_gpus']} | {d['config']['ranks']} | {d['config']['plan']} | `{rf.get('kernel', 'ar_exec_kernel')}` | {d['value']} | "
                    f"{d['ms_per_step']} | {rf['bound']} {rf['achieved']} / {rf['peak']} = {rf['frac']} | "
                    f"{nc} | {nv} | {d.get('genmodel', {}).get('pred_err', '-')} |")
         e2e.append(f"N={n} {d['e2e']['value']} GB/s")
@@ -58,7 +58,7 @@ def bench_section(out):
                "* N > 1: one process per GPU, peer buffers IPC-mapped, the kernel pulls/pushes over NVLink 5;\n"
                "  roofline = 2(N−1)/N·S bytes per direction per GPU (Eq. 2) against the measured 770 GB/s\n"
                "  peer copy (B200_PROFILING.md).\n"
-               "* `NVLS` = the NEXT #1 plan kind (multimem.ld_reduce/st through the NVSwitch, 16 CTAs),\n"
+               "* `NVLS` = the NEXT #1 plan kind (multimem.ld_reduce/st through the NVSwitch, 16 CTAs; 32 at N = 2),\n"
                "  reported beside the GenTree value, not in it (its summation order is the switch's).")
     if cpu:
         out.append(f"* cpu_baseline (oracle, {cpu['cores']} core, {cpu['sample']}): {cpu['value']} GB/s.")
