@@ -22,3 +22,18 @@ def test_gentreesimu_tool_single_switch(tmp_path):
     assert out.returncode == 0, out.stderr
     d = json.load(open(dst))
     assert all(abs(r["rel_dev"]) < 0.05 for r in d["rows"])
+
+
+def test_nvlcounters_summary():
+    """Counter arithmetic used by bench.py's N > 1 roofline: exact byte counters preferred over
+    the GPM rate estimate, per-direction bytes per step, nothing claimed when nothing moved."""
+    sys.path.insert(0, ROOT)
+    from tools.nvlcounters import summarize
+    d = {"gpm_tx": 900, "gpm_rx": 800, "xmit_bytes": 2048, "rcv_bytes": 3072, "host_window_s": 1.0}
+    s = summarize(d, 2, 1024)
+    assert s["counters"] == "nvml xmit_bytes/rcv_bytes"
+    assert (s["tx_bytes_per_step"], s["rx_bytes_per_step"]) == (1024, 1536)
+    assert s["per_direction_vs_algorithmic"] == 1.5
+    s = summarize({"gpm_tx": 4000, "gpm_rx": 2000, "xmit_bytes": 0, "rcv_bytes": 0}, 4, 1000)
+    assert s["counters"] == "nvml gpm_tx/gpm_rx" and s["tx_bytes_per_step"] == 1000
+    assert summarize({"host_window_s": 1.0}, 1, 1)["counters"] == "none answered"
