@@ -3,6 +3,8 @@
     python tools/probe.py fanin            # local k-way reduce sweep, 150M-float vectors
     python tools/probe.py emu [--ctas ..]  # emulated R-rank AllReduce timing at one size
     python tools/probe.py copy             # torch copy bandwidth (sanity vs MEASURED_PEAKS)
+    python tools/probe.py nvpull           # k-way reduce body over NVLink, one process, 2 GPUs
+    python tools/probe.py nvflat           # the executor's bulk-copy body over NVLink (VMM split buffer)
 Prints one JSON object per measurement.
 """
 import argparse
@@ -165,6 +167,104 @@ def copy(args):
     print(json.dumps({"probe": "copy", "gbs": 2 * n * 2 / mn / 1e9, "gbs_med": 2 * n * 2 / med / 1e9}), flush=True)
 
 
+def nvpull(args):
+    """The k-way reduction body (local_reduce_kernel: 16-byte loads, fp32 accumulation, one
+    read / one write per element) launched on GPU0 with operands in GPU1's HBM through peer
+    access — one process and no flags, so ncu can replay it and read the NVLink counters
+    (nvlrx__bytes / nvltx__bytes) that the multi-rank kernel cannot be profiled for.
+    pull: out = local + remote (NVLink rx = S);  push: out(remote) = local + local (tx = S);
+    pullpush: out(remote) = local + remote (rx = tx = S: the fused CPS step's pattern at N = 2)."""
+    from cuda.bindings import runtime as rt
+    assert torch.cuda.device_count() >= 2, "nvpull needs 2 GPUs"
+    for d, p in ((0, 1), (1, 0)):
+        torch.cuda.set_device(d)
+        err, = rt.cudaDeviceEnablePeerAccess(p, 0)
+        assert err in (rt.cudaError_t.cudaSuccess, rt.cudaError_t.cudaErrorPeerAccessAlreadyEnabled), err
+    torch.cuda.set_device(0)
+    count, es = args.count, 4
+    S = count * es
+    l0 = torch.empty(S, dtype=torch.uint8, device="cuda:0")
+    l1 = torch.empty(S, dtype=torch.uint8, device="cuda:0")
+    lo = torch.empty(S, dtype=torch.uint8, device="cuda:0")
+    r0 = torch.empty(S, dtype=torch.uint8, device="cuda:1")
+    ro = torch.empty(S, dtype=torch.uint8, device="cuda:1")
+    for i, b in enumerate((l0, l1, r0)):
+        with torch.cuda.device(b.device):
+            G.fill_synthetic(b, count, "f32", 7, i, 0)
+    torch.cuda.synchronize(1)
+    cases = {"pull": ([l0, r0], lo, S, 0), "push": ([l0, l1], ro, 0, S), "pullpush": ([l0, r0], ro, S, S)}
+    for name in args.cases:
+        ins, out, rx, tx = cases[name]
+        med, mean, mn = timeit(lambda: G.local_reduce(ins, out, count, "f32"), reps=args.reps)
+        print(json.dumps({"probe": "nvpull", "case": name, "bytes_per_vector": S, "nvlink_rx_bytes": rx,
+                          "nvlink_tx_bytes": tx, "t_med": med, "t_min": mn,
+                          "nvlink_gbs_per_direction": max(rx, tx) / med / 1e9}), flush=True)
+
+
+def _split_buffer(ranks_on, stride):
+    """One contiguous virtual range of len(ranks_on) rank slots, slot r backed by physical HBM
+    on GPU ranks_on[r] (CUDA VMM), readable and writable from both GPUs."""
+    from cuda.bindings import driver as cu
+
+    def ok(r):
+        assert r[0] == cu.CUresult.CUDA_SUCCESS, r
+        return r[1] if len(r) == 2 else r[1:]
+    ok(cu.cuInit(0) + (None,))
+    props = []
+    for d in (0, 1):
+        pr = cu.CUmemAllocationProp()
+        pr.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        pr.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        pr.location.id = d
+        props.append(pr)
+    gran = ok(cu.cuMemGetAllocationGranularity(
+        props[0], cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED))
+    assert stride % gran == 0, (stride, gran)
+    total = stride * len(ranks_on)
+    va = ok(cu.cuMemAddressReserve(total, gran, 0, 0))
+    for r, d in enumerate(ranks_on):
+        h = ok(cu.cuMemCreate(stride, props[d], 0))
+        ok(cu.cuMemMap(int(va) + r * stride, stride, 0, h, 0) + (None,))
+    descs = []
+    for d in (0, 1):
+        ad = cu.CUmemAccessDesc()
+        ad.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        ad.location.id = d
+        ad.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        descs.append(ad)
+    ok(cu.cuMemSetAccess(va, total, descs, 2) + (None,))
+    return int(va)
+
+
+def nvflat(args):
+    """The executor's production body (bulk-copy pipeline, ar_flat_kernel) with rank slots split
+    across two GPUs: ranks 0..R/2-1 in GPU0's HBM, the rest in GPU1's, one VMM range, the kernel
+    on GPU0.  Every element of a GPU1 rank is read over NVLink and its result written back over
+    NVLink (rx = tx = R/2·S per call), the pull → add → push pattern of the fused CPS step; one
+    process and no flags, so ncu can read nvlrx/nvltx for the real body."""
+    assert torch.cuda.device_count() >= 2, "nvflat needs 2 GPUs"
+    torch.cuda.set_device(0)
+    world, count, dtype = args.ranks, args.count, args.dtype
+    stride = G.rank_stride_bytes(count, dtype)
+    on = [0] * (world // 2) + [1] * (world - world // 2)
+    base = _split_buffer(on, stride)
+    for r in range(world):
+        with torch.cuda.device(on[r]):
+            G.fill_synthetic(base + r * stride, count, dtype, 7, r, 0)
+        torch.cuda.synchronize(on[r])
+    params = G.params(3e-6, 1 / 900e9, 0.0, 1 / 6.54e12, 0.0, 9)
+    plan = G.Plan.single_switch(world, count, dtype, params, "cps")
+    comm = G.Comm.local(world, 0)
+    S = count * (2 if dtype == "bf16" else 4)
+    remote = sum(on) * S
+    med, mean, mn = timeit(lambda: G.allreduce_exec(plan, comm, base), reps=args.reps)
+    print(json.dumps({"probe": "nvflat", "kernel": comm.last_kernel(), "ranks": world, "ranks_on_gpu1": sum(on),
+                      "dtype": dtype, "bytes_per_rank": S, "nvlink_rx_bytes": remote, "nvlink_tx_bytes": remote,
+                      "t_med": med, "t_min": mn, "nvlink_gbs_per_direction": remote / med / 1e9,
+                      "busbw_equiv": S * 2 * (world - 1) / world / med / 1e9}), flush=True)
+    comm.destroy()
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("what")
@@ -175,6 +275,7 @@ if __name__ == "__main__":
     ap.add_argument("--ctas", type=int, nargs="*", default=[0])
     ap.add_argument("--force", default=None)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--cases", nargs="*", default=["pull", "push", "pullpush"])
     a = ap.parse_args()
     torch.cuda.set_device(0)
-    {"fanin": fanin, "emu": emu, "copy": copy, "trace": trace, "hunt": hunt}[a.what](a)
+    {"fanin": fanin, "emu": emu, "copy": copy, "trace": trace, "hunt": hunt, "nvpull": nvpull, "nvflat": nvflat}[a.what](a)

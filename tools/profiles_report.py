@@ -247,6 +247,62 @@ def p2p_section(out):
                "domain, hence w_t ≥ 4 in the fit and ε = 0.\n")
 
 
+def ncu_csv(path):
+    """{launch id: {metric: value}} from an ncu --csv --metrics launch list."""
+    import csv
+    with open(path) as f:
+        rows = list(csv.DictReader(l for l in f if not l.startswith("==")))
+    out = collections.OrderedDict()
+    for r in rows:
+        out.setdefault(r["ID"], {})[r["Metric Name"]] = float(r["Metric Value"].replace(",", ""))
+    return out
+
+
+def nvlink_section(out):
+    d = os.path.join(P, "round1", "nvlink")
+    if not os.path.isdir(d):
+        return
+    out.append("## 9. NVLink counters (ncu nvlrx/nvltx) for the reduction body\n")
+    out.append("NVML's link counters answer NOT_SUPPORTED on this pool (`nvlink/nvml_counters_probe.json`) and\n"
+               "ncu must not wrap the multi-rank kernel, so the bodies run in ONE process with operands in the\n"
+               "other GPU's HBM (`tools/probe.py nvflat|nvpull`, 2 GPUs, no flags) and ncu reads the link\n"
+               "counters per launch (`nvlink/*_ncu.csv`; median over the launches of each case).\n")
+    out.append("| body / case | kernel time µs | algorithmic bytes per direction | NVLink user bytes rx / tx "
+               "(× algorithmic) | NVLink wire bytes rx / tx (protocol incl.) | user GB/s per direction |")
+    out.append("|---|---|---|---|---|---|")
+    cases = []
+    fl = jl(os.path.join(d, "nvflat2.jsonl"))[0]
+    ids = list(ncu_csv(os.path.join(d, "nvflat2_ncu.csv")).values())
+    cases.append((f"bulk-copy body (`ar_flat_kernel`), CPS over 2 ranks, rank 1 in GPU1 (pull → add → push), "
+                  f"{size(fl['bytes_per_rank'])} {fl['dtype']}", ids, fl["nvlink_rx_bytes"]))
+    pull = jl(os.path.join(d, "nvpull.jsonl"))
+    ids = list(ncu_csv(os.path.join(d, "nvpull_ncu.csv")).values())
+    per = len(ids) // len(pull)
+    for i, r in enumerate(pull):
+        cases.append((f"register body (`local_reduce_kernel`), {r['case']}, {size(r['bytes_per_vector'])} f32",
+                      ids[i * per:(i + 1) * per], max(r["nvlink_rx_bytes"], r["nvlink_tx_bytes"])))
+    for name, launches, alg in cases:
+        def med(m):
+            v = sorted(x[m] for x in launches)
+            return v[len(v) // 2]
+        t = med("gpu__time_duration.sum")
+        ur, ut = med("nvlrx__bytes_data_user.sum"), med("nvltx__bytes_data_user.sum")
+        wr, wt = med("nvlrx__bytes.sum"), med("nvltx__bytes.sum")
+        out.append(f"| {name} | {t / 1e3:.1f} | {alg / 1e6:.1f} MB | {ur / 1e6:.1f} / {ut / 1e6:.1f} MB "
+                   f"({max(ur, ut) / alg:.4f}) | {wr / 1e6:.1f} / {wt / 1e6:.1f} MB | {max(ur, ut) / t:.1f} |")
+    out.append("\n* The production (bulk-copy) body moves exactly the algorithmic bytes over NVLink (user bytes\n"
+               "  1.0006× per direction): every remote element crosses the link once each way — one read, one\n"
+               "  write — with no re-reads.  The register body (Eq. 6 microbenchmark kernel) carries 3 % more\n"
+               "  user bytes than it needs, one more reason the executor stages through shared memory.\n"
+               "* Protocol overhead is what the user-byte rate cannot recover: 13 % on responses, and on the\n"
+               "  issuing side read requests share tx with the write data (wire tx 1.38× user bytes in the\n"
+               "  pull → push case).  Link bandwidth is counted in wire bytes, which is why the measured\n"
+               "  busbw of the symmetric N-GPU kernel (655–690 GB/s user data per direction, §1) sits at\n"
+               "  0.85–0.90 of the 770 GB/s peer-copy figure.\n"
+               "* In these probes ONE GPU's SMs issue all traffic (the other GPU is passive), so their user\n"
+               "  GB/s is below the symmetric kernel's; the evidence here is the byte accounting.\n")
+
+
 def main():
     out = ["# profiles/ — measured evidence (round 1)\n",
            "Generated by `tools/profiles_report.py` from the files in this directory.  All numbers were\n"
@@ -262,6 +318,7 @@ def main():
     hybrid_section(out)
     gentreesimu_section(out)
     pipelining_section(out)
+    nvlink_section(out)
     sys.stdout.write("\n".join(out) + "\n")
 
 
