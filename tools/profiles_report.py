@@ -303,6 +303,37 @@ def nvlink_section(out):
                "  GB/s is below the symmetric kernel's; the evidence here is the byte accounting.\n")
 
 
+def nvls_order_section(out):
+    d = os.path.join(P, "round1", "nvls_order")
+    if not os.path.isdir(d):
+        return
+    out.append("## 10. What the NVSwitch computes for multimem.ld_reduce (NVLS summation semantics)\n")
+    out.append("`tools/nvls_order.py` (torchrun, N GPUs): the NVLS AllReduce's result bits against host\n"
+               "candidates — sequential fp32 sums in every rotation, the pairwise trees (N = 4), and the\n"
+               "correctly rounded sum (exact sum, one RNE rounding) — on gradient-shaped inputs and on\n"
+               "adversarial inputs built on rounding boundaries.  Three calls per case.\n")
+    out.append("| N | dtype | data | elements | where candidates disagree | stable over calls | best candidate (match) |")
+    out.append("|---|---|---|---|---|---|---|")
+    for n in (2, 3, 4):
+        path = os.path.join(d, f"order{n}.jsonl")
+        if not os.path.exists(path):
+            continue
+        for r in jl(path):
+            k, v = max(r["match_fraction"].items(), key=lambda kv: (kv[1], kv[0] == "correctly_rounded"))
+            out.append(f"| {n} | {r['dtype']} | {r['data']} | {r['count']} | {r['elements_where_candidates_disagree']} | "
+                       f"{r['stable_across_calls']} | {k} ({v:.4f}) |")
+    out.append("\n* fp32: the switch returns the **correctly rounded** sum (one rounding of the exact sum) on\n"
+               "  every element, N = 2–4, including the 1.8 M elements at N = 4 where every fixed association\n"
+               "  order gives a different bit pattern somewhere; −0 + −0 comes back +0 (the candidate sums\n"
+               "  from +0).  No plan order reproduces it, so NVLS is not bit-exact to any GenTree plan, but it\n"
+               "  is deterministic and has a plain definition an oracle can compute (a candidate bit-exact\n"
+               "  plan kind for a later round).\n"
+               "* bf16 (`acc::f32`): no candidate explains every element; the mismatches against one RNE\n"
+               "  rounding of the exact sum are ties (and near-ties after fp32 accumulation) resolved to the\n"
+               "  odd neighbour — the switch's bf16 conversion is not round-to-nearest-even.  NVLS bf16 is\n"
+               "  therefore checked against the north star's 1e-2 bound, never bit-exact.\n")
+
+
 def main():
     out = ["# profiles/ — measured evidence (round 1)\n",
            "Generated by `tools/profiles_report.py` from the files in this directory.  All numbers were\n"
@@ -319,6 +350,7 @@ def main():
     gentreesimu_section(out)
     pipelining_section(out)
     nvlink_section(out)
+    nvls_order_section(out)
     sys.stdout.write("\n".join(out) + "\n")
 
 
