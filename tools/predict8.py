@@ -1,0 +1,67 @@
+"""GenModel's prediction for configuration C2 at 8 x B200 (the box size this pool cannot lease).
+
+    python tools/predict8.py [--world 8] > profiles/genmodel_predict_n8.json
+
+For every size of the C2 sweep (fp32, 64 KiB - 1 GiB) it asks the library's GenTree for the
+plan (fitted NVLink parameters, profiles/genmodel_params.json), predicts the executed plan's time
+(`genmodel_predict_executed`, reading A6x) — or the one-shot row (reading OS1) below the
+executor's one-shot cut-off 1.5 MiB/(N-1) — and the NVLS row (reading NV1, fitted
+profiles/genmodel_params_nvls.json), and converts both to busbw.  The parameters were fitted
+on N = 2..4 (median executed-plan error 1.7 %); at N = 8 the numbers are a model prediction,
+not a measurement, and say so in the output.  CPU only.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2409_04202_b200 as G  # noqa: E402
+
+P = os.path.join(ROOT, "profiles")
+
+
+def busbw(nbytes, n, t):
+    return nbytes * 2 * (n - 1) / n / t / 1e9
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--world", type=int, default=8)
+    a = ap.parse_args()
+    n = a.world
+    pj = json.load(open(os.path.join(P, "genmodel_params.json")))
+    nj = json.load(open(os.path.join(P, "genmodel_params_nvls.json")))
+    oj = json.load(open(os.path.join(P, "genmodel_fit_oneshot_graph.json")))
+    gp = G.params(pj["alpha"], pj["beta"], pj["gamma"], pj["delta"], pj["epsilon"], pj["w_t"])
+    npar = G.params(alpha=nj["alpha"], beta=nj["beta"])
+    ll_max = min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256   # executor default (exec.cu, init_comm)
+    rows = []
+    for k in range(16, 31):
+        nbytes = 1 << k
+        count = nbytes // 4
+        plan = G.Plan.single_switch(n, count, "f32", gp)
+        kind = plan.report()[-1]["chosen"]
+        if nbytes <= ll_max:
+            t_plan = oj["alpha"] + 2 * (n - 1) * nbytes * oj["beta"]
+            path = "one-shot"
+        else:
+            t_plan = plan.predict_executed(gp)["total"]
+            path = f"{kind} (executed steps)"
+        c = plan.choose_nvls(gp, npar)
+        rows.append({"bytes": nbytes, "gentree_plan": kind, "path": path, "t_pred_s": t_plan,
+                     "busbw_pred": round(busbw(nbytes, n, t_plan), 1), "t_nvls_pred_s": c["t_nvls"],
+                     "nvls_busbw_pred": round(busbw(nbytes, n, c["t_nvls"]), 1)})
+    out = {"tool": "predict8", "world": n, "dtype": "f32", "kind": "GenModel prediction, not a measurement",
+           "params": pj["source"], "nvls_params": nj["source"], "oneshot_params": "genmodel_fit_oneshot_graph.json",
+           "oneshot_max_bytes": ll_max,
+           "fit_range": "parameters fitted on N = 2..4 (w_t >= 4, eps = 0: no incast seen up to the whole box)",
+           "context": "NCCL 8-rank all-reduce busbw 725 GB/s at 1 GiB on B200 (B200_PROFILING.md)",
+           "rows": rows}
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -334,6 +334,25 @@ def nvls_order_section(out):
                "  therefore checked against the north star's 1e-2 bound, never bit-exact.\n")
 
 
+def predict8_section(out):
+    path = os.path.join(P, "genmodel_predict_n8.json")
+    if not os.path.exists(path):
+        return
+    d = json.load(open(path))
+    out.append(f"## 11. GenModel prediction for C2 at {d['world']} x B200 (not measured: no 8-GPU lease here)\n")
+    out.append(f"`tools/predict8.py`: GenTree's plan and the fitted executed-plan model ({d['params']}; one-shot row\n"
+               f"below {d['oneshot_max_bytes'] >> 10} KiB), and the fitted NVLS row ({d['nvls_params']}).  "
+               f"{d['fit_range']}.\n")
+    out.append("| size | GenTree plan | path | predicted busbw GB/s | NVLS row predicted busbw GB/s |")
+    out.append("|---|---|---|---|---|")
+    for r in d["rows"]:
+        out.append(f"| {size(r['bytes'])} | {r['gentree_plan']} | {r['path']} | {r['busbw_pred']} | {r['nvls_busbw_pred']} |")
+    out.append(f"\nContext: {d['context']}.  At 8 GPUs the P2P plans' wire volume per GPU, 2(N−1)/N·S = 1.75·S,\n"
+               "is 1.56× NVLS's (1 + 1/N)·S = 1.125·S, so the model expects the bit-exact GenTree plan to\n"
+               "stay near 670-680 GB/s at large sizes — below NCCL's published 725 — while the NVLS kind\n"
+               "(§10: fp32 = correctly rounded sum) would pass it.\n")
+
+
 def main():
     out = ["# profiles/ — measured evidence (round 1)\n",
            "Generated by `tools/profiles_report.py` from the files in this directory.  All numbers were\n"
@@ -351,6 +370,7 @@ def main():
     pipelining_section(out)
     nvlink_section(out)
     nvls_order_section(out)
+    predict8_section(out)
     sys.stdout.write("\n".join(out) + "\n")
 
 
