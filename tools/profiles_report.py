@@ -81,7 +81,24 @@ def ncu_section(out):
                "  2·8·256 MiB = 4.295 GB, so traffic/algorithmic ≈ 0.99: no re-reads.\n")
 
 
-def sweep_table(out, path, title):
+def genmodel_pick(n, nbytes):
+    """GenModel's choice between the GenTree plan (the one-shot row below the executor's cut-off,
+    else the executed-plan model) and the NVLS row (reading NV1), with the fitted parameters."""
+    sys.path.insert(0, ROOT)
+    import paper_2409_04202_b200 as G
+    pj = json.load(open(os.path.join(P, "genmodel_params.json")))
+    nj = json.load(open(os.path.join(P, "genmodel_params_nvls.json")))
+    oj = json.load(open(os.path.join(P, "genmodel_fit_oneshot_graph.json")))
+    gp = G.params(pj["alpha"], pj["beta"], pj["gamma"], pj["delta"], pj["epsilon"], pj["w_t"])
+    plan = G.Plan.single_switch(n, nbytes // 4, "f32", gp)
+    c = plan.choose_nvls(gp, G.params(alpha=nj["alpha"], beta=nj["beta"]))
+    t_plan = c["t_plan"]
+    if nbytes <= min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256:
+        t_plan = oj["alpha"] + 2 * (n - 1) * nbytes * oj["beta"]
+    return "nvls" if c["t_nvls"] < t_plan else "gentree"
+
+
+def sweep_table(out, path, title, pick=False):
     rows = jl(path)
     t = collections.defaultdict(dict)
     for r in rows:
@@ -90,29 +107,39 @@ def sweep_table(out, path, title):
     name = {"gentree": "GenTree", "nvls": "NVLS", "default": "NCCL"}
     out.append(f"**{title}** (busbw GB/s, median; eager = per-call events incl. host launch, graph = CUDA-graph replay)\n")
     hdr = "| size | " + " | ".join(f"{name[p]} eager | {name[p]} graph" for p in plans) + " | GenTree/NCCL (graph) |"
+    if pick:
+        hdr += " GenModel pick (GenTree plan or NVLS) | pick/NCCL (graph) |"
     out.append(hdr)
-    out.append("|" + "---|" * (2 + 2 * len(plans)))
+    out.append("|" + "---|" * (2 + 2 * len(plans) + (2 if pick else 0)))
+    n = rows[0]["n"]
     for b in sorted(t):
         d = t[b]
         cells = []
         for p in plans:
             cells += [f"{d.get((p, 'eager'), float('nan')):.1f}", f"{d.get((p, 'graph'), float('nan')):.1f}"]
         ratio = d.get(("gentree", "graph"), 0) / max(d.get(("default", "graph"), 1e-9), 1e-9)
-        out.append(f"| {size(b)} | " + " | ".join(cells) + f" | {ratio:.2f} |")
+        line = f"| {size(b)} | " + " | ".join(cells) + f" | {ratio:.2f} |"
+        if pick:
+            k = genmodel_pick(n, b)
+            line += f" {name[k]} | {d.get((k, 'graph'), 0) / max(d.get(('default', 'graph'), 1e-9), 1e-9):.2f} |"
+        out.append(line)
     out.append("")
 
 
 def c2_section(out):
     out.append("## 3. C2 sweep: busbw vs size — GenTree plan, NVLS, NCCL on the same box\n")
     c2 = os.path.join(P, "round1", "c2")
-    sweep_table(out, os.path.join(c2, "sweep_n4_f32_ll.jsonl"), "C2, 4×B200, fp32 (GenTree chose CPS at every size; ≤ 512 KiB via the one-shot path)")
-    sweep_table(out, os.path.join(c2, "sweep_n2_f32_ll.jsonl"), "C2, 2×B200, fp32 (GenTree chose CPS at every size; ≤ 1 MiB via the one-shot path)")
+    sweep_table(out, os.path.join(c2, "sweep_n4_f32_ll.jsonl"), "C2, 4×B200, fp32 (GenTree chose CPS at every size; ≤ 512 KiB via the one-shot path)", pick=True)
+    sweep_table(out, os.path.join(c2, "sweep_n2_f32_ll.jsonl"), "C2, 2×B200, fp32 (GenTree chose CPS at every size; ≤ 1 MiB via the one-shot path)", pick=True)
     bf = os.path.join(c2, "sweep_n4_bf16.jsonl")
     if os.path.exists(bf):
         sweep_table(out, bf, "4×B200, bf16")
     out.append("NVLS wire volume per GPU and direction is (1 + 1/N)·S against the P2P plans'\n"
                "2(N−1)/N·S: at N = 2 that is 1.5·S vs 1·S, so NVLS loses at large sizes on 2 GPUs and\n"
-               "wins on 4 (1.25·S vs 1.5·S); at small sizes its single switch round trip wins on both.\n")
+               "wins on 4 (1.25·S vs 1.5·S); at small sizes its single switch round trip wins on both.\n"
+               "\"GenModel pick\" = the fitted model's choice between the GenTree plan and the NVLS row (reading NV1;\n"
+               "fp32 NVLS is bit-exact against the oracle's correctly rounded sum, reading NV2), and the measured\n"
+               "busbw of the picked path over NCCL's.\n")
 
 
 def fit_section(out):
