@@ -1541,11 +1541,12 @@ static void init_comm(ar_comm *c) {
   if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
   if (const char *f = std::getenv("AR_FENCE_MODE")) c->fence_mode = std::atoi(f);
   if (const char *st = std::getenv("AR_EXEC_STORE")) c->store_tma = std::string(st) != "regs";
-  // measured defaults (profiles/README.md): HBM-bound emulated ranks prefer a short ring of
-  // large tiles (2 x 48 KB: 91 % of the copy peak vs 85 % at 4 x 40 KB); NVLink 3 x 40 KB
+  // measured defaults (profiles/README.md): HBM-bound emulated ranks prefer a short ring
+  // (2 x 40 KB: 658.8 GB/s busbw at 8 ranks x 256 MiB bf16, vs 648.5 at 2 x 48 KB, 654-656 at
+  // 2 x 36/44 KB, 609-632 at 3-4 stages; profiles/round1/stages); NVLink 3 x 40 KB
   if (c->local) {
     c->stages = 2;
-    c->stage_bytes = 48 * 1024;
+    c->stage_bytes = 40 * 1024;
   } else {
     c->stages = 3;
     c->stage_bytes = 40 * 1024;
