@@ -89,6 +89,10 @@ struct ExecArgs {
   // push protocol (lower_push): rank -> its push scratch as seen here; [parity][src][slot]
   char *scr[AR_MAX_RANKS];
   long long scr_plane, scr_slot;
+  // dynamic tile scheduling (CPS-shaped plans, one rank per process): op i's tiles are handed
+  // out by atomicAdd on dyn_ctr[i]; the last CTA of the launch zeroes the dyn_nops counters
+  unsigned int *dyn_ctr;     // nullptr = static per-CTA slices
+  int dyn_nops;
 };
 
 // Buffer references in op rank lists: r < kScrRef is rank r's data buffer; kScrRef + o·64 + s
@@ -329,7 +333,9 @@ struct Pipe {
   unsigned long long full[kMaxStages];
   unsigned long long empty[kMaxStages];
   int stages, stage_bytes;   // runtime ring geometry (AR_STAGES, AR_STAGE_KB)
+  uint32_t tile[kMaxStages]; // dynamic scheduling: the op tile in each stage (kNoTile = op done)
 };
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
 
 template <int NSRC, bool BF16>
 __device__ __noinline__ void body_bulk(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
@@ -474,6 +480,106 @@ __device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v
     }
   }
   g += ntiles;
+}
+
+// Dynamic-tile variant of body_bulk_st for NSRC > 1 (CPS-shaped plans).  [v0, v1) is the WHOLE
+// op; the producer thread takes tile indices from the op's global counter (atomicAdd), so CTAs
+// that get more NVLink/HBM bandwidth take more tiles and all CTAs finish together (static
+// slices finished between 0.67x and 1.0x of the slowest CTA's time: harness mtrace, 256 MiB,
+// 2 x B200).  The tile index travels to the consumers through the stage's smem slot, released
+// by the full barrier; when the counter runs out the producer publishes kNoTile with a plain
+// arrive.  Per element the reduction is unchanged (same sources, same order): same bits.
+template <int NSRC, bool BF16>
+__device__ __noinline__ void body_bulk_st_dyn(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
+                                              Pipe &pp, unsigned int *ctr) {
+  const int kStages = pp.stages, kStageBytes = pp.stage_bytes, kOutTile = pp.stage_bytes / 2;
+  const int T = (kStageBytes / NSRC) / 16 * 16;
+  const int TV = T / 16;
+  const uint32_t ntiles = (uint32_t)((v1 - v0 + TV - 1) / TV);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t used = 0;   // stage uses of this op (tiles + the closing kNoTile), identical in every thread
+  if (warp == 0) {
+    if (lane == 0) {
+      for (;; used++) {
+        const uint32_t gi = g + used, st = gi % kStages, use = gi / kStages;
+        if (use > 0) mbar_wait(&pp.empty[st], (use - 1) & 1);
+        const uint32_t tile = atomicAdd(ctr, 1u);
+        if (tile >= ntiles) {
+          pp.tile[st] = kNoTile;
+          mbar_arrive(&pp.full[st]);
+          used++;
+          break;
+        }
+        pp.tile[st] = tile;
+        const size_t t0 = v0 + (size_t)tile * TV;
+        const uint32_t bytes = (uint32_t)min((size_t)TV, v1 - t0) * 16;
+        mbar_expect_tx(&pp.full[st], bytes * NSRC);
+        uint8_t *base = smem + st * kStageBytes;
+#pragma unroll
+        for (int k = 0; k < NSRC; k++) bulk_g2s(base + k * T, s.src[k] + t0, bytes, &pp.full[st]);
+      }
+    }
+    used = __shfl_sync(0xffffffffu, used, 0);
+  } else {
+    const int ndst = s.ndst;
+    const int nthr = blockDim.x - 32;
+    const bool storer = threadIdx.x == 32;
+    uint4 *outb = (uint4 *)(smem + kStages * kStageBytes);
+    for (;; used++) {
+      const uint32_t gi = g + used, st = gi % kStages, use = gi / kStages;
+      mbar_wait(&pp.full[st], use & 1);
+      const uint32_t tile = pp.tile[st];
+      if (tile == kNoTile) {
+        consumer_bar(nthr);   // every consumer has read the slot before the stage is released
+        if (storer) mbar_arrive(&pp.empty[st]);
+        used++;
+        break;
+      }
+      const size_t t0 = v0 + (size_t)tile * TV;
+      const int nvt = (int)min((size_t)TV, v1 - t0);
+      const uint4 *base = (const uint4 *)(smem + st * kStageBytes);
+      uint4 *o = outb + (gi & 1) * (kOutTile / 16);
+      consumer_bar(nthr);     // the storer has drained reads of this output tile (use i-2)
+      for (int v = threadIdx.x - 32; v < nvt; v += nthr) {
+        uint4 x[NSRC];
+#pragma unroll
+        for (int k = 0; k < NSRC; k++) x[k] = base[k * TV + v];
+        float acc[8];
+        acc_first<BF16>(acc, x[0]);
+#pragma unroll
+        for (int k = 1; k < NSRC; k++) acc_add<BF16>(acc, x[k]);
+        if (s.div) acc_div(acc, (float)s.div);
+        o[v] = acc_pack<BF16>(acc);
+      }
+      consumer_bar(nthr);     // output tile complete, input stage fully read
+      if (storer) {
+        mbar_arrive(&pp.empty[st]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int d = 0; d < ndst; d++) bulk_s2g(s.dst[d] + t0, o, (uint32_t)nvt * 16);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      }
+    }
+    if (storer) {
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+  }
+  g += used;
+}
+
+template <bool BF16>
+__device__ void body_dispatch_bulk_st_dyn(const OpShared &s, size_t v0, size_t v1, uint32_t &g, uint8_t *smem,
+                                          Pipe &pp, unsigned int *ctr) {
+  switch (s.nsrc) {
+    case 2: body_bulk_st_dyn<2, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+    case 3: body_bulk_st_dyn<3, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+    case 4: body_bulk_st_dyn<4, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+    case 5: body_bulk_st_dyn<5, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+    case 6: body_bulk_st_dyn<6, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+    case 7: body_bulk_st_dyn<7, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+    case 8: body_bulk_st_dyn<8, BF16>(s, v0, v1, g, smem, pp, ctr); break;
+  }
 }
 
 template <bool BF16>
@@ -662,7 +768,11 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       }
       const long long nv = ve - vb;
       const size_t v0 = (size_t)(vb + nv * cta / nctas), v1 = (size_t)(vb + nv * (cta + 1) / nctas);
-      if (a.bulk) {
+      if (a.dyn_ctr && op.nsrc >= 2 && op.nsrc <= 8) {
+        unsigned int *ctr = a.dyn_ctr + st.op_begin + oi;
+        if (bf16) body_dispatch_bulk_st_dyn<true>(sh, (size_t)vb, (size_t)ve, g, dyn_smem, pp, ctr);
+        else body_dispatch_bulk_st_dyn<false>(sh, (size_t)vb, (size_t)ve, g, dyn_smem, pp, ctr);
+      } else if (a.bulk) {
         if (a.store_tma) {
           if (bf16) body_dispatch_bulk_st<true>(sh, v0, v1, g, dyn_smem, pp);
           else body_dispatch_bulk_st<false>(sh, v0, v1, g, dyn_smem, pp);
@@ -743,6 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
     const unsigned int total = gridDim.x * gridDim.y;
     if (atomicAdd(a.done_ctr, 1u) == total - 1) {
       *(volatile unsigned int *)a.done_ctr = 0;
+      for (int i = 0; i < a.dyn_nops; i++) a.dyn_ctr[i] = 0u;   // every CTA is past its ops
       *(volatile unsigned long long *)a.epoch_dev = epoch;
       __threadfence();
     }
@@ -1045,6 +1156,8 @@ struct Lowered {
   int nctas = 0;
   bool ll_shape = false;     // CPS-shaped: one all-rank reduce per block, identical input order
   std::vector<int> ll_order;
+  unsigned int *dyn_ctr = nullptr;   // per-op tile counters (dynamic scheduling), nullptr = static
+  int nops = 0;
 };
 
 }  // namespace
@@ -1080,6 +1193,7 @@ struct ar_comm {
   unsigned int jitter_ns = 0;                  // AR_JITTER_NS (stress testing)
   bool plain_launch = false;                   // AR_LAUNCH=plain (see launch_exec)
   bool flat = true;                            // emulated single-step plans via ar_flat_kernel (AR_FLAT=0: off)
+  bool dyn = true;                             // dynamic tile scheduling of CPS-shaped plans (AR_DYN=0: off)
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
@@ -1464,6 +1578,7 @@ static void free_lowered(Lowered &L) {
   cudaFree(L.ranks);
   cudaFree(L.prog_begin);
   cudaFree(L.prog_len);
+  if (L.dyn_ctr) cudaFree(L.dyn_ctr);
 }
 
 static int resident_ctas(int device) {
@@ -1557,6 +1672,7 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
   if (const char *v = std::getenv("AR_LAUNCH")) c->plain_launch = std::string(v) == "plain";
   if (const char *v = std::getenv("AR_FLAT")) c->flat = std::string(v) != "0";
+  if (const char *v = std::getenv("AR_DYN")) c->dyn = std::string(v) != "0";
   if (!c->local && c->rpp == 1) {
     c->push_max_bytes = kPushDefaultMaxBytes;
     if (const char *v = std::getenv("AR_PUSH_MAX_MB")) c->push_max_bytes = std::strtoll(v, nullptr, 10) << 20;
@@ -2106,6 +2222,18 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     }
     L.steps = upload(st);
     L.ops = upload(ops);
+    if (c->dyn && !c->local && c->rpp == 1 && !use_push) {
+      // CPS-shaped plans only: their one data step sits between paired entry and exit waits,
+      // and any CTA of a peer having posted implies the whole peer buffer is ready / done, so
+      // tiles need not belong to fixed CTAs (range waits of multi-step plans do need that)
+      auto lit = c->ll_shape.find(plan->uid);
+      if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+      if (!lit->second.empty() && !ops.empty()) {
+        L.nops = (int)ops.size();
+        CUDA_OK(cudaMalloc(&L.dyn_ctr, ops.size() * sizeof(unsigned int)));
+        CUDA_OK(cudaMemset(L.dyn_ctr, 0, ops.size() * sizeof(unsigned int)));
+      }
+    }
     L.waits = upload(w);
     L.ranks = upload(rk);
     L.prog_begin = upload(pb);
@@ -2140,6 +2268,8 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.stage_bytes = c->stage_bytes;
   a.jitter_ns = c->jitter_ns;
   a.avg_n = avg_n;
+  a.dyn_ctr = (a.bulk && a.store_tma) ? L.dyn_ctr : nullptr;
+  a.dyn_nops = a.dyn_ctr ? L.nops : 0;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;

@@ -326,9 +326,15 @@ def mtrace(args):
                         u = [c for c in range(a_.shape[0]) if a_[c, -1] > 0]
                         med = lambda j: round(float(np.median([(a_[c, j] - g0) / 1e3 for c in u])), 2)
                         nst2 = len(plan.lowering()["ranks"][q]["steps"])
+                        spread = lambda j: [round(float(f([(a_[c, j] - g0) / 1e3 for c in u])), 2)
+                                            for f in (np.min, np.median, np.max)]
                         print(json.dumps({"mode": "mtrace-steady", "rank": q, "bytes": nbytes, "start": med(0),
                                           "steps": [[med(1 + 3 * i), med(2 + 3 * i), med(3 + 3 * i)]
-                                                    for i in range(nst2)], "end": med(-1)}), flush=True)
+                                                    for i in range(nst2)], "end": med(-1),
+                                          "cta_spread_min_med_max": {
+                                              "start": spread(0), "end": spread(-1),
+                                              "steps": [[spread(1 + 3 * i), spread(2 + 3 * i), spread(3 + 3 * i)]
+                                                        for i in range(nst2)]}}), flush=True)
             nst = len(plan.lowering()["ranks"][rank]["steps"])
             t0 = tr[:, 0].min()
             C = comm_ctas = tr.shape[0]
