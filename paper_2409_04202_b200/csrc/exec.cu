@@ -873,6 +873,9 @@ struct FlatArgs {
   int world, esize, avg_n;
   int order[AR_MAX_RANKS];
   int stages, stage_bytes;
+  // dynamic tile scheduling (world <= 8): [0, world) per-owner-block tile counters, [world] the
+  // launch's finished-CTA count; nullptr = static equal slices of the concatenated blocks
+  unsigned int *ctr;
 };
 
 __global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_constant__ FlatArgs a) {
@@ -901,6 +904,45 @@ __global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_const
   }
   const long long my0 = total * blockIdx.x / gridDim.x, my1 = total * (blockIdx.x + 1) / gridDim.x;
   uint32_t g = 0;
+  if (a.ctr) {
+    // every CTA works on every owner block, taking tiles from the block's counter (same
+    // pipeline and per-element order as the static split; body_bulk_st_dyn)
+    for (int r = 0; r < a.world; r++) {
+      const long long off = a.count / a.world * r + min((long long)r, a.count % a.world);
+      const long long len = a.count / a.world + (r < a.count % a.world ? 1 : 0);
+      const long long vb = (off * a.esize + 15) / 16, ve = (off + len) * a.esize / 16;
+      const bool mine_scalar = blockIdx.x == 0 && len > 0 && (ve <= vb || vb * 16 > off * a.esize ||
+                                                              ve * 16 < (off + len) * a.esize);
+      if (ve <= vb && !mine_scalar) continue;
+      __syncthreads();
+      if (threadIdx.x < a.world) {
+        sh.src[threadIdx.x] = (const uint4 *)(a.base + a.stride * a.order[threadIdx.x]);
+        sh.dst[threadIdx.x] = (uint4 *)(a.base + a.stride * threadIdx.x);
+      }
+      if (threadIdx.x == 0) {
+        sh.nsrc = a.world;
+        sh.ndst = a.world;
+        sh.div = a.avg_n;
+      }
+      __syncthreads();
+      if (ve > vb) {
+        if (bf16) body_dispatch_bulk_st_dyn<true>(sh, (size_t)vb, (size_t)ve, g, dyn_smem, pp, a.ctr + r);
+        else body_dispatch_bulk_st_dyn<false>(sh, (size_t)vb, (size_t)ve, g, dyn_smem, pp, a.ctr + r);
+      }
+      if (mine_scalar) {
+        if (ve <= vb) {
+          scalar_elems(sh, off, off + len, bf16);
+        } else {
+          if (vb * 16 > off * a.esize) scalar_elems(sh, off, vb * E, bf16);
+          if (ve * 16 < (off + len) * a.esize) scalar_elems(sh, ve * E, off + len, bf16);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(a.ctr + a.world, 1u) == gridDim.x - 1)
+      for (int i = 0; i <= a.world; i++) a.ctr[i] = 0u;   // every CTA is past every block
+    return;
+  }
   long long acc = 0;
   for (int r = 0; r < a.world; r++) {
     const long long off = a.count / a.world * r + min((long long)r, a.count % a.world);
@@ -1194,6 +1236,7 @@ struct ar_comm {
   bool plain_launch = false;                   // AR_LAUNCH=plain (see launch_exec)
   bool flat = true;                            // emulated single-step plans via ar_flat_kernel (AR_FLAT=0: off)
   bool dyn = true;                             // dynamic tile scheduling of CPS-shaped plans (AR_DYN=0: off)
+  unsigned int *flat_ctr = nullptr;            // ar_flat_kernel tile counters (local comms)
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
@@ -1649,6 +1692,10 @@ static void init_comm(ar_comm *c) {
   // [3] last completed LL epoch, [4] LL finished-CTA counter
   CUDA_OK(cudaMalloc(&c->err, 6 * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->err, 0, 6 * sizeof(unsigned long long)));
+  if (c->local) {   // ar_flat_kernel's tile counters (dynamic scheduling)
+    CUDA_OK(cudaMalloc(&c->flat_ctr, (AR_MAX_RANKS + 1) * sizeof(unsigned int)));
+    CUDA_OK(cudaMemset(c->flat_ctr, 0, (AR_MAX_RANKS + 1) * sizeof(unsigned int)));
+  }
   c->sig.assign(c->world, nullptr);
   for (int i = 0; i < c->rpp; i++) c->sig[c->rank + i] = c->sig_local + (size_t)i * c->page_elems;
   if (c->local) c->sig_opened = true;
@@ -1906,6 +1953,7 @@ int ar_comm_destroy(ar_comm *c) {
   cudaFree(c->sig_local);
   cudaFree(c->ll_scratch);
   cudaFree(c->err);
+  if (c->flat_ctr) cudaFree(c->flat_ctr);
   cudaFree(c->trace);
   delete c;
   return AR_OK;
@@ -2151,6 +2199,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       for (int k = 0; k < c->world; k++) fa.order[k] = lit->second[k];
       fa.stages = c->stages;
       fa.stage_bytes = c->stage_bytes;
+      fa.ctr = (c->dyn && c->world <= 8) ? c->flat_ctr : nullptr;
       ar_flat_kernel<<<c->max_ctas, kThreads, dyn_smem_bytes(c->stages, c->stage_bytes), (cudaStream_t)stream>>>(fa);
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
