@@ -115,6 +115,7 @@ struct NvArgs {
   long long off, len;             // this rank's block (elements)
   int world, esize;
   unsigned long long timeout_ns;
+  int dyn;                        // 1 = chunks handed out by atomicAdd on epoch_dev[3] (AR_NVLS_DYN)
 };
 
 __device__ __forceinline__ unsigned long long nv_ld_acquire(const unsigned long long *p) {
@@ -188,6 +189,37 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
   const long long vb = a.off * a.esize / 16, nv = a.len * a.esize / 16;
   const long long v0 = vb + nv * blockIdx.x / gridDim.x, v1 = vb + nv * (blockIdx.x + 1) / gridDim.x;
   constexpr int U = 4;   // vectors in flight per thread
+  if (a.dyn) {
+    // dynamic chunks of 8 x (blockDim x U) vectors: CTAs that get more switch bandwidth take
+    // more chunks (the same scheme as the P2P executor's tiles).  A/B option, off by default:
+    // measured equal at 256 MiB - 1 GiB and 1-3 % slower at 16 MiB on 2 and 4 B200s
+    // (profiles/round1/dyn/nvls_dyn_ab.txt) — the 16 NVLS CTAs are not imbalanced
+    __shared__ long long s_chunk;
+    unsigned int *ctr = (unsigned int *)(a.epoch_dev + 3);
+    const long long CH = (long long)blockDim.x * U * 8;
+    const long long nch = (nv + CH - 1) / CH;
+    for (;;) {
+      if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(ctr, 1u);
+      __syncthreads();
+      const long long c = s_chunk;
+      __syncthreads();
+      if (c >= nch) break;
+      const long long c0 = vb + c * CH, c1 = min(vb + nv, c0 + CH);
+      for (long long base = c0 + threadIdx.x; base < c1; base += (long long)blockDim.x * U) {
+        uint4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const long long v = base + (long long)u * blockDim.x;
+          if (v < c1) x[u] = ld_reduce<BF16>(a.mc + v * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+          const long long v = base + (long long)u * blockDim.x;
+          if (v < c1) mc_store<BF16>(a.mc + v * 16, x[u]);
+        }
+      }
+    }
+  } else
   for (long long base = v0 + threadIdx.x; base < v1; base += (long long)blockDim.x * U) {
     uint4 x[U];
 #pragma unroll
@@ -205,6 +237,7 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
   if (threadIdx.x == 0) {
     if (atomicAdd((unsigned int *)(a.epoch_dev + 1), 1u) == gridDim.x - 1) {
       *(volatile unsigned int *)(a.epoch_dev + 1) = 0;
+      *(volatile unsigned int *)(a.epoch_dev + 3) = 0;   // dynamic chunk counter
       *(volatile unsigned long long *)a.epoch_dev = epoch;
       __threadfence();
     }
@@ -223,6 +256,7 @@ struct ar_nvls {
   unsigned long long *dev_words = nullptr;
   int nctas = 0;
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
+  bool dyn = false;
 };
 
 #define NV_TRY(...)                                         \
@@ -284,6 +318,7 @@ int ar_nvls_create(int32_t rank, int32_t world, int32_t cuda_device, uint64_t by
     n->nctas = std::min(world == 2 ? 32 : 16, std::min(nsm, kNvCtaCap));
     if (const char *v = std::getenv("AR_NVLS_CTAS")) n->nctas = std::max(1, std::min(kNvCtaCap, std::atoi(v)));
     if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) n->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
+    if (const char *v = std::getenv("AR_NVLS_DYN")) n->dyn = std::string(v) != "0";
     *out = n;
     return AR_OK;
   })
@@ -368,6 +403,7 @@ int allreduce_exec_nvls(ar_nvls *n, uint64_t count, int32_t dtype, void *stream)
     a.world = n->world;
     a.esize = es;
     a.timeout_ns = n->timeout_ns;
+    a.dyn = n->dyn ? 1 : 0;
     if (dtype == AR_BF16) nvls_kernel<true><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
     else nvls_kernel<false><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
     RT_CALL(cudaGetLastError());
