@@ -128,6 +128,8 @@ def sweep_table(out, path, title, pick=False):
 
 def c2_section(out):
     out.append("## 3. C2 sweep: busbw vs size — GenTree plan, NVLS, NCCL on the same box\n")
+    out.append("Measured before dynamic tile scheduling (DESIGN §6); on the final build the GenTree plan is\n"
+               "1.5–2 % faster at 256 MiB (§1 and `round1/dyn/`), so its columns here are conservative.\n")
     c2 = os.path.join(P, "round1", "c2")
     sweep_table(out, os.path.join(c2, "sweep_n4_f32_ll.jsonl"), "C2, 4×B200, fp32 (GenTree chose CPS at every size; ≤ 512 KiB via the one-shot path)", pick=True)
     sweep_table(out, os.path.join(c2, "sweep_n2_f32_ll.jsonl"), "C2, 2×B200, fp32 (GenTree chose CPS at every size; ≤ 1 MiB via the one-shot path)", pick=True)
