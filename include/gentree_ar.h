@@ -234,7 +234,10 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
  * rank's registered buffer (ar_comm_register + ar_comm_open_peers).  Emulated comm: dptr
  * is the base of world consecutive rank buffers, rank r's at dptr + r *
  * ar_rank_stride_bytes(count, dtype).  Asynchronous and ordered on `stream` (a
- * cudaStream_t; NULL = legacy default stream).  Every element of every rank's buffer ends
+ * cudaStream_t; NULL = legacy default stream).  Calls on one communicator must be ordered
+ * with respect to each other (one stream, or explicit events): a launch reads the flag epoch
+ * and the tile counters (dynamic tile scheduling of CPS-shaped plans) that the
+ * previous launch left.  Every element of every rank's buffer ends
  * equal to the plan's left-to-right fp32 sum of the ranks' inputs (bit-exact to the CPU
  * oracle).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
  * plan's, unregistered or misaligned buffer; AR_ESYS on launch failure. */
