@@ -307,6 +307,19 @@ def test_emulated_cps_flag_protocol(dtype, monkeypatch):
             run_emulated(single_switch(world), world, count, dtype, force="cps", red="avg")
 
 
+@pytest.mark.parametrize("dyn", ["0", "1"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_flat_kernel_static_and_dynamic_tiles(dyn, dtype, monkeypatch):
+    """ar_flat_kernel with static slices (AR_DYN=0) and with tiles handed out by the per-block
+    atomic counters (default): same plan bits, over back-to-back calls (the counters must be
+    back at zero for the next launch), ragged sizes, SUM and AVG, R = 2..8 (dynamic) and 9."""
+    monkeypatch.setenv("AR_DYN", dyn)
+    for world in (2, 5, 8, 9):
+        for count in (world * 4096 + 7, 1000003):
+            run_emulated(single_switch(world), world, count, dtype, force="cps", calls=3)
+            run_emulated(single_switch(world), world, count, dtype, force="cps", red="avg")
+
+
 @pytest.mark.parametrize("force", [None, "ring"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_exec_host_end_to_end(force, dtype):

@@ -79,3 +79,19 @@ def test_push_protocol_bit_exact(world):
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert f"mp_worker world={world}: OK" in r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_static_tiles_bit_exact(world):
+    """AR_DYN=0 (static per-CTA slices instead of the default dynamic tiles for CPS-shaped
+    plans) keeps the plan's bits."""
+    if ngpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT, AR_DYN="0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29621", os.path.join(ROOT, "tests", "mp_worker.py")]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert f"mp_worker world={world}: OK" in r.stdout
+
