@@ -1703,12 +1703,12 @@ static void init_comm(ar_comm *c) {
   if (const char *b = std::getenv("AR_EXEC_BODY")) c->bulk = std::string(b) != "regs";
   if (const char *f = std::getenv("AR_FENCE_MODE")) c->fence_mode = std::atoi(f);
   if (const char *st = std::getenv("AR_EXEC_STORE")) c->store_tma = std::string(st) != "regs";
-  // measured defaults (profiles/README.md): HBM-bound emulated ranks prefer a short ring
-  // (2 x 40 KB: 658.8 GB/s busbw at 8 ranks x 256 MiB bf16, vs 648.5 at 2 x 48 KB, 654-656 at
-  // 2 x 36/44 KB, 609-632 at 3-4 stages; profiles/round1/stages); NVLink 3 x 40 KB
+  // measured defaults (profiles/round1/stages): HBM-bound emulated ranks, dynamic tiles: 3 x 48
+  // KB (713-718 GB/s busbw at 8 ranks x 256 MiB bf16; 2 x 40 KB 695, 2 x 64 / 3 x 56 KB 716,
+  // 5-6 stages 700-703); with static slices a short 2 x 40 KB ring had been best; NVLink 3 x 40 KB
   if (c->local) {
-    c->stages = 2;
-    c->stage_bytes = 40 * 1024;
+    c->stages = 3;
+    c->stage_bytes = 48 * 1024;
   } else {
     c->stages = 3;
     c->stage_bytes = 40 * 1024;
