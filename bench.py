@@ -289,11 +289,13 @@ def main():
         dbytes = world * stride
     else:
         comm = G.Comm.create(rank, n, dev)
+        if args.ctas:   # agreed at registration (ar_comm_open_peers checks it)
+            comm.set_ctas(args.ctas)
         buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
         G.fill_synthetic(buf, count, args.dtype, seed, rank, 0)
         comm.register(buf)
         dbytes = nbytes
-    if args.ctas:
+    if args.ctas and n == 1:
         comm.set_ctas(args.ctas)
     torch.cuda.synchronize()
 

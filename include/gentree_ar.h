@@ -38,7 +38,7 @@ extern "C" {
 #define AR_BF16 1 /* bfloat16 data, fp32 accumulation, one RNE rounding per stored partial (Q2) */
 
 #define AR_MAX_RANKS 64     /* ranks of one communicator (2..64) */
-#define AR_BLOB_BYTES 256   /* size of one exported registration blob */
+#define AR_BLOB_BYTES 512   /* size of one exported registration blob */
 
 const char *ar_last_error(void);
 const char *ar_version(void);
@@ -202,7 +202,8 @@ int ar_comm_create_multi(int32_t proc, int32_t nproc, int32_t ranks_per_proc, in
 int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out);
 
 /* Number of CTAs per rank used by the step-table kernel (0 = automatic).  Same value on all
- * ranks.  The flat and one-shot paths size their own grids and ignore it. */
+ * ranks (checked by ar_comm_open_peers); multi-process comms: call before ar_comm_register —
+ * AR_EINVAL once peers are open.  The flat and one-shot paths size their own grids and ignore it. */
 int ar_comm_set_ctas(ar_comm *comm, int32_t ctas);
 
 /* Export `bytes` of device memory at `dptr` (16-byte aligned; may be an interior pointer of
@@ -216,7 +217,16 @@ int ar_comm_register(ar_comm *comm, void *dptr, size_t bytes, void *blob_out);
  * blobs = nproc * AR_BLOB_BYTES (= world * AR_BLOB_BYTES for ar_comm_create), process
  * order, from ar_comm_register on every process for the
  * same logical buffer (same size).  Collective: call on all ranks before the first
- * allreduce_exec on that buffer. */
+ * allreduce_exec on that buffer.  This process's own blob selects the local registration
+ * (same allocation handle, offset and size).  The blobs carry the settings every rank must
+ * share — CTA count (ar_comm_set_ctas), flag-page geometry, one-shot scratch size and path
+ * cut-offs — and AR_EINVAL is returned if any rank differs; after this call
+ * ar_comm_set_ctas may no longer change the CTA count.  Peers in the SAME process (several
+ * communicators in one process, e.g. one per rank on one GPU for single-GPU testing of this
+ * path) are mapped by their raw device pointers, since CUDA IPC handles cannot be opened by
+ * the exporting process; each such communicator's kernels must then run on their own stream
+ * with ar_comm_set_ctas(...) * world <= the SM count, so that all ranks' persistent kernels
+ * are resident together. */
 int ar_comm_open_peers(ar_comm *comm, const void *blobs);
 /* Asynchronous device error of earlier executions (flag wait timeout = AR_ESYS), cleared on
  * read.  Synchronises the communicator's device. */
@@ -256,6 +266,14 @@ int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t coun
  * errors; AR_EINVAL for an unknown op. */
 int allreduce_exec_op(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype, int32_t op,
                       void *stream);
+
+/* Data-movement plans (measurement probes, e.g. the C3-ii fan-in tests: plans loaded with
+ * gt_plan_from_json that are not AllReduces).  allreduce_exec and allreduce_exec_op reject
+ * a plan that failed symbolic verification with AR_EINVAL; this entry runs it through the same
+ * executor (copies and reduces of the plan's steps, same flag protocol).  Plans whose ops
+ * exceed AR_MAX_RANKS sources or destinations are rejected (AR_EINVAL) in either entry. */
+int ar_exec_movement_plan(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
+                          void *stream);
 
 /* The same, end to end from host memory: copies `host` (pinned recommended; for an emulated
  * comm world consecutive rank buffers at the same stride) into dptr, executes, copies the

@@ -14,7 +14,7 @@ LIB_PATH = os.path.join(HERE, "libgentree_ar.so")
 AR_OK, AR_EINVAL, AR_ESYS = 0, 1, 2
 AR_F32, AR_BF16 = 0, 1
 AR_MAX_RANKS = 64
-AR_BLOB_BYTES = 256
+AR_BLOB_BYTES = 512
 DTYPES = {"f32": AR_F32, "bf16": AR_BF16}
 ESIZE = {AR_F32: 4, AR_BF16: 2}
 
@@ -110,6 +110,7 @@ _SIGS = {
     "ar_rank_stride_bytes": (U64, [U64, I32]),
     "allreduce_exec": (I32, [P, P, P, U64, I32, P]),
     "allreduce_exec_op": (I32, [P, P, P, U64, I32, I32, P]),
+    "ar_exec_movement_plan": (I32, [P, P, P, U64, I32, P]),
     "ar_comm_last_kernel": (ctypes.c_char_p, [P]),
     "ar_comm_set_oneshot_max": (I32, [P, U64]),
     "allreduce_exec_host": (I32, [P, P, P, P, U64, I32, P]),

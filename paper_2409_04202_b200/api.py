@@ -366,9 +366,14 @@ class Executor:
     (e.g. every training step, or inside torch.cuda.graph capture: the kernel launch carries no
     per-call host state, the call epoch lives on the device)."""
 
-    def __init__(self, plan: Plan, comm: Comm, buf, stream=None, op: str = "sum"):
+    def __init__(self, plan: Plan, comm: Comm, buf, stream=None, op: str = "sum", movement: bool = False):
         info = plan.info()
         self._keep = (plan, comm, buf)
+        if movement:   # data-movement probe plan (ar_exec_movement_plan)
+            self._args = (plan.handle, comm.handle, ctypes.c_void_p(_ptr(buf)), info["count"], info["dtype"],
+                          ctypes.c_void_p(_stream(stream)))
+            self._f = lib.ar_exec_movement_plan
+            return
         self._args = (plan.handle, comm.handle, ctypes.c_void_p(_ptr(buf)), info["count"], info["dtype"],
                       OPS[op], ctypes.c_void_p(_stream(stream)))
         self._f = lib.allreduce_exec_op
@@ -390,6 +395,11 @@ def allreduce_exec(plan: Plan, comm: Comm, buf, count: int | None = None, dtype=
         info = plan.info()
     count = info["count"] if count is None else count
     dt = info["dtype"] if dtype is None else dtype_code(dtype)
+    if comm.local and not isinstance(buf, int):   # world rank buffers at the emulated stride
+        need = rank_stride_bytes(count, dt) * (comm.world - 1) + count * (2 if dt == AR_BF16 else 4)
+        if buf.numel() * buf.element_size() < need:
+            raise ValueError(f"buffer holds {buf.numel() * buf.element_size()} bytes; an emulated "
+                             f"communicator of {comm.world} ranks needs {need}")
     if op == "sum":
         check(lib.allreduce_exec(plan.handle, comm.handle, _ptr(buf), count, dt, _stream(stream)))
     else:

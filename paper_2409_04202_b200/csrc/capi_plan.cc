@@ -306,6 +306,7 @@ int gt_plan_from_json(const char *plan_json, gt_plan **out, int32_t *is_allreduc
     g->json = plan_to_json(g->plan, dtype.c_str());
     g->report = "[]";
     g->uid = next_plan_uid();
+    g->is_allreduce = ar;
     if (is_allreduce) *is_allreduce = ar ? 1 : 0;
     *out = g;
     return AR_OK;

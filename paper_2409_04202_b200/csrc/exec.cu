@@ -16,6 +16,7 @@
 // launch with blockIdx.y = rank.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -93,6 +94,7 @@ struct ExecArgs {
   // out by atomicAdd on dyn_ctr[i]; the last CTA of the launch zeroes the dyn_nops counters
   unsigned int *dyn_ctr;     // nullptr = static per-CTA slices
   int dyn_nops;
+  int entry_fence;           // 1 = fence.acq_rel.sys before the relaxed entry flags (AR_ENTRY_FENCE)
 };
 
 // Buffer references in op rank lists: r < kScrRef is rank r's data buffer; kScrRef + o·64 + s
@@ -809,6 +811,10 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
         // there is nothing for a release to order — a relaxed system-scope store suffices
         // (st.release.sys costs ~5 us on B200 even with no prior writes: measured with
         // `harness.py mtrace --steady`)
+        if (a.entry_fence) {   // AR_ENTRY_FENCE=1: order earlier work at system scope first
+          if (threadIdx.x == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+          __syncthreads();
+        }
         for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
           const int consumer = a.ranks[st.notify_begin + i];
           asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(flag_ptr(a, consumer, st.slot, me, cta)),
@@ -1186,6 +1192,8 @@ struct Registration {
   size_t bytes = 0;
   std::vector<char *> peer;   // process -> mapped pointer (own = local)
   bool opened = false;
+  cudaIpcMemHandle_t handle;  // of the allocation (ar_comm_open_peers matches its own blob by it)
+  uint64_t offset = 0;
 };
 
 struct Lowered {
@@ -1255,6 +1263,10 @@ struct ar_comm {
   std::map<std::pair<uint64_t, uint64_t>, gt_plan *> sub_plans;
   unsigned long long *trace = nullptr;         // in-kernel globaltimer stamps (ar_comm_set_trace)
   size_t trace_elems = 0;
+  bool settings_fixed = false;                 // peers opened: the CTA count is agreed (Blob)
+  char *checked_base = nullptr;                // local comms: last buffer extent validated
+  size_t checked_need = 0;
+  bool entry_fence = false;                    // AR_ENTRY_FENCE=1: fence.acq_rel.sys before relaxed entry flags
 };
 
 namespace {
@@ -1266,6 +1278,16 @@ struct Blob {
   cudaIpcMemHandle_t data, sig;
   cudaIpcMemHandle_t ll;      // low-latency scratch (valid iff has_ll)
   int32_t has_ll, pad;
+  // settings every rank must share (checked by ar_comm_open_peers): the flag-page geometry,
+  // the CTA count the range/paired waits are computed for, the one-shot scratch plane size and
+  // the path cut-offs
+  int32_t nctas, cta_cap, rpp, pad2;
+  int64_t ll_cap_lines, ll_max_bytes, push_max_bytes;
+  // same-process peers (several communicators in one process, e.g. one per rank on one GPU):
+  // CUDA IPC handles cannot be opened by the exporting process, so the raw pointers are used
+  int64_t pid;
+  int32_t device, pad3;
+  uint64_t raw_base, raw_sig, raw_ll;
 };
 static_assert(sizeof(Blob) <= AR_BLOB_BYTES, "blob too large");
 
@@ -1396,6 +1418,12 @@ static void lower_plan(const Plan &p, int world, std::vector<DevStep> &steps, st
       H[s] = saveB;
     }
   }
+  // the kernel stages an op's source and destination lists in fixed arrays (OpShared)
+  for (int s = 0; s < S; s++)
+    for (int r = 0; r < n; r++)
+      for (auto &o : H[s][r])
+        if (o.src.empty() || (int)o.src.size() > AR_MAX_RANKS || (int)o.dst.size() > AR_MAX_RANKS)
+          throw InvalidArg("plan op has more than AR_MAX_RANKS sources or destinations");
   // accesses per buffer rank
   std::vector<std::vector<Access>> acc(n);
   for (int s = 0; s < S; s++)
@@ -1720,6 +1748,7 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_LAUNCH")) c->plain_launch = std::string(v) == "plain";
   if (const char *v = std::getenv("AR_FLAT")) c->flat = std::string(v) != "0";
   if (const char *v = std::getenv("AR_DYN")) c->dyn = std::string(v) != "0";
+  if (const char *v = std::getenv("AR_ENTRY_FENCE")) c->entry_fence = std::string(v) == "1";
   if (!c->local && c->rpp == 1) {
     c->push_max_bytes = kPushDefaultMaxBytes;
     if (const char *v = std::getenv("AR_PUSH_MAX_MB")) c->push_max_bytes = std::strtoll(v, nullptr, 10) << 20;
@@ -1824,6 +1853,9 @@ int ar_comm_set_ctas(ar_comm *c, int32_t ctas) {
       CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->device));
       want = std::min(nsm, kCtaCapMulti);
     }
+    if (c->settings_fixed && want != c->nctas)
+      throw InvalidArg("ar_comm_set_ctas after ar_comm_open_peers: the peers' waits are computed for the agreed "
+                       "CTA count; set it before ar_comm_register on every rank");
     c->nctas = want;
     return AR_OK;
   })
@@ -1839,9 +1871,10 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     size_t size;
     base_of(dptr, &base, &size);
     if ((char *)dptr + bytes > base + size) throw InvalidArg("buffer extends past its allocation");
-    Blob b{};
+    Blob b;
+    std::memset(&b, 0, sizeof b);
     b.magic = kBlobMagic;
-    b.version = 1;
+    b.version = 2;
     b.rank = c->proc;
     b.world = c->world;
     b.bytes = bytes;
@@ -1852,6 +1885,17 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
       CUDA_OK(cudaIpcGetMemHandle(&b.ll, c->ll_scratch));
       b.has_ll = 1;
     }
+    b.nctas = c->nctas;
+    b.cta_cap = c->cta_cap;
+    b.rpp = c->rpp;
+    b.ll_cap_lines = c->ll_cap_lines;
+    b.ll_max_bytes = c->ll_max_bytes;
+    b.push_max_bytes = c->push_max_bytes;
+    b.pid = (int64_t)getpid();
+    b.device = c->device;
+    b.raw_base = (uint64_t)(uintptr_t)base;
+    b.raw_sig = (uint64_t)(uintptr_t)c->sig_local;
+    b.raw_ll = (uint64_t)(uintptr_t)c->ll_scratch;
     std::memset(blob_out, 0, AR_BLOB_BYTES);
     std::memcpy(blob_out, &b, sizeof b);
     Registration reg;
@@ -1859,6 +1903,8 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     reg.bytes = bytes;
     reg.peer.assign(c->nproc, nullptr);
     reg.peer[c->proc] = (char *)dptr;
+    reg.handle = b.data;
+    reg.offset = b.offset;
     for (auto it = c->regs.begin(); it != c->regs.end(); ++it)
       if (it->local == reg.local) { c->regs.erase(it); break; }
     c->regs.push_back(reg);
@@ -1874,19 +1920,36 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
     CUDA_OK(cudaSetDevice(c->device));
     const char *bb = (const char *)blobs;
     const Blob *mine = (const Blob *)(bb + (size_t)c->proc * AR_BLOB_BYTES);
+    if (mine->magic != kBlobMagic || mine->version != 2 || mine->rank != c->proc) throw InvalidArg("corrupt or misordered blob");
+    // this process's registration of the buffer the blobs describe: same allocation, offset, size
     Registration *reg = nullptr;
-    for (auto &r : c->regs)
-      if ((uint64_t)r.bytes == mine->bytes) reg = &r;
-    // the most recently registered buffer with this size is the one being opened
     for (auto it = c->regs.rbegin(); it != c->regs.rend(); ++it)
-      if ((uint64_t)it->bytes == mine->bytes) { reg = &*it; break; }
-    if (!reg) throw InvalidArg("no local registration matches the blobs");
+      if ((uint64_t)it->bytes == mine->bytes && it->offset == mine->offset &&
+          std::memcmp(&it->handle, &mine->data, sizeof(cudaIpcMemHandle_t)) == 0) {
+        reg = &*it;
+        break;
+      }
+    if (!reg) throw InvalidArg("no local registration matches this process's blob");
+    const int64_t me_pid = (int64_t)getpid();
     for (int t = 0; t < c->nproc; t++) {   // one blob per process
       const Blob *b = (const Blob *)(bb + (size_t)t * AR_BLOB_BYTES);
-      if (b->magic != kBlobMagic || b->world != c->world || b->rank != t) throw InvalidArg("corrupt or misordered blob");
+      if (b->magic != kBlobMagic || b->version != 2 || b->world != c->world || b->rank != t)
+        throw InvalidArg("corrupt or misordered blob");
       if (b->bytes != mine->bytes) throw InvalidArg("ranks registered buffers of different sizes");
+      if (b->nctas != c->nctas || b->cta_cap != c->cta_cap || b->rpp != c->rpp || b->ll_cap_lines != c->ll_cap_lines ||
+          b->ll_max_bytes != mine->ll_max_bytes || b->push_max_bytes != c->push_max_bytes)
+        throw InvalidArg("ranks disagree on communicator settings (ar_comm_set_ctas, AR_LL_MAX_KB, "
+                         "AR_PUSH_MAX_MB or the one-shot cut-off must be identical on every rank)");
       if (t == c->proc) continue;
-      auto open = [&](const cudaIpcMemHandle_t &h) -> char * {
+      const bool same_proc = b->pid == me_pid;
+      if (same_proc && b->device != c->device) {
+        // a communicator of this process on another GPU: direct peer access instead of IPC
+        cudaError_t e = cudaDeviceEnablePeerAccess(b->device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CUDA_OK(e);
+      }
+      auto open = [&](const cudaIpcMemHandle_t &h, uint64_t raw) -> char * {
+        if (same_proc) return (char *)(uintptr_t)raw;   // IPC handles cannot be opened by their exporter
         std::string key((const char *)&h, sizeof h);
         key += std::to_string(t);
         auto it = c->ipc_opened.find(key);
@@ -1896,15 +1959,16 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
         c->ipc_opened[key] = (char *)p;
         return (char *)p;
       };
-      reg->peer[t] = open(b->data) + b->offset;
-      if (c->ll_scratch && b->has_ll && !c->ll_peer[t]) c->ll_peer[t] = open(b->ll);
+      reg->peer[t] = open(b->data, b->raw_base) + b->offset;
+      if (c->ll_scratch && b->has_ll && !c->ll_peer[t]) c->ll_peer[t] = open(b->ll, b->raw_ll);
       unsigned long long *pages = nullptr;
       for (int i = 0; i < c->rpp; i++)
         if (!c->sig[t * c->rpp + i]) {
-          if (!pages) pages = (unsigned long long *)open(b->sig);
+          if (!pages) pages = (unsigned long long *)open(b->sig, b->raw_sig);
           c->sig[t * c->rpp + i] = pages + (size_t)i * c->page_elems;
         }
     }
+    c->settings_fixed = true;
     reg->opened = true;
     c->fast_valid = false;
     c->sig_opened = true;
@@ -2142,9 +2206,24 @@ static void launch_exec(ar_comm *c, dim3 grid, void **args, cudaStream_t stream)
 
 // stride_override: bytes between consecutive hosted ranks' buffers when dptr points into the
 // middle of larger rank buffers (the chunked end-to-end path); 0 = derived from count.
+static void check_local_extent(ar_comm *c, void *dptr, size_t need) {
+  // emulated comm: dptr is the base of world rank buffers; the whole extent must be one allocation
+  if ((char *)dptr == c->checked_base && need <= c->checked_need) return;
+  char *base;
+  size_t size;
+  base_of(dptr, &base, &size);
+  if ((char *)dptr + need > base + size)
+    throw InvalidArg("buffer too small: an emulated communicator needs world rank buffers at ar_rank_stride_bytes");
+  c->checked_base = (char *)dptr;
+  c->checked_need = need;
+}
+
 static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream,
-                     int op = AR_OP_SUM, uint64_t stride_override = 0) {
+                     int op = AR_OP_SUM, uint64_t stride_override = 0, bool movement = false) {
   if (!plan || !c || !dptr) throw InvalidArg("null argument");
+  if (!plan->is_allreduce && !movement)
+    throw InvalidArg("plan is not an AllReduce (failed symbolic verification); data-movement plans run through "
+                     "ar_exec_movement_plan");
   if (op != AR_OP_SUM && op != AR_OP_AVG) throw InvalidArg("unknown reduction op");
   const int avg_n = op == AR_OP_AVG ? plan->plan.n : 0;
   if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");
@@ -2155,6 +2234,10 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   if (cur != c->device) CUDA_OK(cudaSetDevice(c->device));
   dim3 grid(c->nctas, c->rpp);
   const size_t nbytes_call = count * (size_t)plan->esize;
+  if (c->local)
+    check_local_extent(c, dptr,
+                       (stride_override ? stride_override : ar_rank_stride_bytes(count, dtype)) * (c->world - 1) +
+                           nbytes_call);
   if (c->ll_opened && (long long)nbytes_call <= c->ll_max_bytes) {
     // low-latency one-shot path for CPS-shaped plans (see ar_ll_kernel)
     auto lit = c->ll_shape.find(plan->uid);
@@ -2319,6 +2402,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.avg_n = avg_n;
   a.dyn_ctr = (a.bulk && a.store_tma) ? L.dyn_ctr : nullptr;
   a.dyn_nops = a.dyn_ctr ? L.nops : 0;
+  a.entry_fence = c->entry_fence ? 1 : 0;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;
@@ -2338,6 +2422,10 @@ int allreduce_exec(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, 
 int allreduce_exec_op(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, int32_t op,
                       void *stream) {
   SYS_TRY({ return exec_impl(plan, c, dptr, count, dtype, stream, op); })
+}
+
+int ar_exec_movement_plan(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count, int32_t dtype, void *stream) {
+  SYS_TRY({ return exec_impl(plan, c, dptr, count, dtype, stream, AR_OP_SUM, 0, true); })
 }
 
 // A plan whose every element is summed in ascending rank order by one reduce (natural CPS):
@@ -2408,6 +2496,7 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *c, void *dptr, void *host,
     if (!host) throw InvalidArg("null host buffer");
     if (!c) throw InvalidArg("null comm");
     if (!plan) throw InvalidArg("null plan");
+    if (!plan->is_allreduce) throw InvalidArg("plan is not an AllReduce (failed symbolic verification)");
     CUDA_OK(cudaSetDevice(c->device));
     const size_t bytes = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) * c->rpp
                                     : count * (size_t)(dtype == AR_BF16 ? 2 : 4);

@@ -17,6 +17,7 @@ struct gt_plan {
   std::string json;            // canonical plan JSON
   std::string report;          // GenTree report JSON
   uint64_t uid = 0;            // unique id (lowering cache key)
+  bool is_allreduce = true;    // passed symbolic verification (gt_plan_from_json may load other plans)
 };
 
 namespace gtar {

@@ -216,29 +216,70 @@ def test_cta_counts(ctas):
     run_emulated(single_switch(8), 8, 123457, "bf16", force="hcps:4,2", ctas=ctas)
 
 
-def test_full_size_bench_config_sampled():
-    """bench.py's N=1 workload (8 emulated ranks, bf16, 256 MiB per rank, GenTree plan) in the
-    launch configuration bench.py times; outputs checked at sampled indices one by one."""
+@pytest.mark.parametrize("mode", ["gradient", "specials"])
+def test_full_size_bench_config_full_buffer(mode):
+    """bench.py's N=1 workload in the launch configuration bench.py times: 8 emulated ranks,
+    bf16, 256 MiB per rank, GenTree plan (CPS) on ar_flat_kernel with dynamic tiles, bench's
+    seed — EVERY element of EVERY rank compared with the oracle's step-by-step simulation (a
+    single wrong tile anywhere fails), for gradient-shaped and special-value inputs."""
     world, count, dtype = 8, 128 * 1024 * 1024, "bf16"
+    seed = 0x240904202 ^ 4
     doc = single_switch(world)
     plan = G.Plan.from_topology(doc, count, dtype)
     comm = G.Comm.local(world, 0)
-    buf, stride = emulated_buffer(world, count, dtype, SEED)
+    stride = G.rank_stride_bytes(count, dtype)
+    buf = torch.empty(world * stride, dtype=torch.uint8, device="cuda")
+    for r in range(world):
+        G.fill_synthetic(buf.data_ptr() + r * stride, count, dtype, seed, r, MODES[mode])
     G.allreduce_exec(plan, comm, buf)
     torch.cuda.synchronize()
     comm.async_error()
-    rng = np.random.default_rng(0)
-    idx = np.unique(np.concatenate([rng.integers(0, count, 4000), np.arange(0, 64),
-                                    np.arange(count - 64, count),
-                                    [OP.block_offset(count, world, b) + d for b in range(1, world) for d in (-1, 0)]]))
-    vals = [np.concatenate([GEN.generate(SEED, r, 1, dtype, start=int(i)) for i in idx]) for r in range(world)]
-    t = T.parse_topology(doc)
-    oplan, _ = GT.gentree(t, count, 2)
-    want = SM.simulate_at(oplan, idx, vals, dtype)
-    host = buf.view(torch.int16)
-    for r in (0, 3, world - 1):
-        got = host[r * stride // 2 + torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint16)
+    assert comm.last_kernel() == "ar_flat_kernel"
+    oplan, _ = GT.gentree(T.parse_topology(doc), count, 2)
+    assert OP.plan_to_json(oplan, dtype) == plan.to_json()
+    want = SM.simulate(oplan, GEN.generate_all(seed, world, count, dtype, mode), dtype)
+    host = buf.cpu().numpy()
+    for r in range(world):
+        got = host[r * stride: r * stride + 2 * count].view(np.uint16)
         assert_bits_equal(got, want[r], dtype, f"rank {r}")
+    del host, want
+
+
+@pytest.mark.parametrize("force", [None, "ring", "rhd", "rb", "hcps:4,2", "hcps:2,2,2"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_large_all_kinds_full_buffer(force, dtype):
+    """Every plan kind at 32 MiB per rank (8 emulated ranks, thousands of tiles per op,
+    ragged count), every element of every rank vs the oracle."""
+    world = 8
+    count = (32 << 20) // (4 if dtype == "f32" else 2) + 13
+    run_emulated(single_switch(world), world, count, dtype, force=force)
+
+
+@pytest.mark.parametrize("mode", ["integer", "specials"])
+@pytest.mark.parametrize("force", [None, "ring", "rhd", "rb", "hcps:4,2", "hcps:2,4", "hcps:2,2,2"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_modes_every_kind(mode, force, dtype):
+    """±0, subnormals, ±max-finite (overflow -> inf), ±inf, NaN, and integer-valued inputs
+    through every plan kind — CPS on the flat kernel (dynamic tiles) and on the step-table
+    kernel's flag protocol, Ring, RHD, RB, HCPS — SUM and AVG (reading AV1).  Integer inputs
+    must give the exact int64 sum (every partial exact)."""
+    world, count = 8, 300007
+    got = run_emulated(single_switch(world), world, count, dtype, force=force, mode=mode)
+    if mode == "integer":
+        xs = GEN.generate_all(SEED, world, count, dtype, "integer")
+        ref = sum(GEN.as_f64(x, dtype).astype(np.int64) for x in xs)
+        for r in (0, world - 1):
+            assert np.array_equal(GEN.as_f64(got[r], dtype).astype(np.int64), ref)
+    run_emulated(single_switch(world), world, count, dtype, force=force, mode=mode, red="avg")
+
+
+@pytest.mark.parametrize("mode", ["integer", "specials"])
+def test_modes_cps_flag_protocol(mode, monkeypatch):
+    """The same edge-case inputs through CPS on the step-table kernel (AR_FLAT=0)."""
+    monkeypatch.setenv("AR_FLAT", "0")
+    for dtype in ("f32", "bf16"):
+        run_emulated(single_switch(8), 8, 300007, dtype, force="cps", mode=mode)
+        run_emulated(single_switch(8), 8, 300007, dtype, force="cps", mode=mode, red="avg")
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])

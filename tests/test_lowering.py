@@ -189,3 +189,19 @@ def test_full_waits_variant_is_also_correct(monkeypatch):
         got = interpret(low, xs, ctas=3, calls=2, rnd=rnd)
         for r in range(world):
             assert np.array_equal(got[r], want[r])
+
+
+def test_lowering_rejects_oversized_ops():
+    """A plan that fails verification with duplicated inputs (fan-in 100 at N = 2) loads as a
+    data-movement plan but cannot be lowered: the kernel's per-op source table holds
+    AR_MAX_RANKS entries (ADVICE r1: such a plan used to overrun OpShared::src)."""
+    import json
+    world, count = 2, 1024
+    bad = {"count": count, "dtype": "f32", "n": world, "steps": [
+        {"label": "rs", "phase": "rs", "transfers": [],
+         "reduces": [{"block": b, "fan_in": 100, "inputs": [0] * 50 + [1] * 50, "server": b}
+                     for b in range(world)]}]}
+    plan = G.Plan.from_json(json.dumps(bad))
+    assert not plan.is_allreduce
+    with pytest.raises(Exception, match="AR_MAX_RANKS"):
+        plan.lowering()

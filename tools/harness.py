@@ -273,7 +273,7 @@ def p2p(args):
         cases = [("pull", None), ("push", None)] + [("push", x) for x in range(2, world)]
         for kind, x in cases:
             plan = G.Plan.from_json(probe_plan(kind, world, count, args.dtype, x))
-            r = timer.run(lambda: G.Executor(plan, comm, view), 10, lambda: None, "graph")
+            r = timer.run(lambda: G.Executor(plan, comm, view, movement=True), 10, lambda: None, "graph")
             m = x or world
             per_dir = (m - 1) * (nbytes // world) / r["t_mean"] / 1e9
             emit(rank, {"mode": "p2p", "kind": kind if x is None else f"x-to-x push (x={x})", "n": world,
