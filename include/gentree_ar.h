@@ -155,15 +155,24 @@ int gt_plan_simulate(const gt_plan *plan, const char *topology_json, const gm_pa
  * another op of the step reads or writes (AR_EINVAL otherwise).  *is_allreduce (optional)
  * is set to 1 iff the plan also passes the AllReduce conservation check;
  * data-movement plans that are not AllReduces (e.g. the x-to-x fan-in probe of P:418) are
- * accepted and run by allreduce_exec all the same.  genmodel_predict needs explicit params. */
+ * accepted, and run through ar_exec_movement_plan (allreduce_exec refuses them).
+ * genmodel_predict needs explicit params. */
 int gt_plan_from_json(const char *plan_json, gt_plan **out, int32_t *is_allreduce);
 
 /* GenModel of the plan as the B200 executor runs it (reading A6x): the same
  * per-step formula applied to the lowered steps — after the last RS level is fused
  * with the first AG level — with one α per flag round (entry + one per executed step) and
  * B = max over ranks of max(bytes in, bytes out) per step, since NVLink is full duplex and a
- * fused step moves RS and AG traffic at the same time.  `params` is required (uniform). */
+ * fused step moves RS and AG traffic at the same time.  `params` is required (uniform).
+ * Bit-identical to oracle/genmodel.py predict_executed (which derives the executed steps from
+ * the plan and the stated fusion rule, not from these tables; tests/test_parity_planner.py). */
 int genmodel_predict_executed(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
+
+/* The same for a plan whose ranks ALL share one GPU (emulated communicator; config C5's
+ * "8 ranks per GPU" on one device; reading A6e): the ranks' data movement goes through one
+ * HBM, so each executed step costs α + C·γ + D·δ with D = Σ over ranks and ops of
+ * (sources + destinations)·bytes and C = Σ (k − 1)·bytes (no link term). */
+int genmodel_predict_executed_shared(const gt_plan *plan, const gm_params *params, gm_breakdown *out);
 
 /* Plan-vs-NVLS selection by GenModel: *t_plan = the executed-plan
  * prediction of `plan` under plan_params (genmodel_predict_executed), *t_nvls = the "nvls"

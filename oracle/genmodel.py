@@ -300,3 +300,124 @@ def enumerate_hcps_factorizations(n: int, max_steps: int) -> list:
     for m in range(1, max_steps + 1):
         out.extend(sorted((f for f in found if len(f) == m), reverse=True))
     return out
+
+
+# ---------------------------------------------------------------- the executed plan (reading A6x)
+
+def executed_steps(plan: Plan) -> list:
+    """The plan as the executor runs it (reading A6x), as a list of steps, each a
+    list of ops (rank, block, inputs, dests): rank computes block from `inputs` (summed in
+    order; one input = a copy) and writes it to every rank in `dests`.
+
+    A Reduce(r, b, I) of an RS step is the op (r, b, I, (r,)); the Transfers (r -> d, b) of an
+    AG step with the same source and block form one op (r, b, (r,), (d1, d2, ...)) — the
+    sender reads its block once and writes it to each peer ("each processor sends the block
+    that it reduced to others").  Fusion rule ("one read / one write per element", SURVEY
+    §8(a) row a4; the δ saving of P:402): when AG step s+1 directly follows RS step s, every
+    transfer (r -> d, b) of step s+1 whose source r reduced block b in step s with fan-in >= 2
+    is executed by that reduce — the reduced value goes from the reducer straight to d —
+    and leaves step s+1.  If the fused step s would contain a hazard (an op writing a
+    (rank, block) that another op of the step reads or writes; the concurrency rule of S:212),
+    nothing of step s+1 is fused.  Ops on blocks of zero elements (N > count, reading Q3)
+    move nothing and are not executed; steps left without ops vanish."""
+    ops = []
+    live = [block_size(plan.count, plan.n, b) > 0 for b in range(plan.n)]
+    for st in plan.steps:
+        if st.phase == "rs":
+            ops.append([[rd.server, rd.block, tuple(rd.inputs), (rd.server,)] for rd in st.reduces if live[rd.block]])
+        else:
+            by = {}
+            for t in st.transfers:
+                if live[t.block]:
+                    by.setdefault((t.src, t.block), []).append(t.dst)
+            ops.append([[r, b, (r,), tuple(sorted(d))] for (r, b), d in sorted(by.items())])
+    for s in range(len(plan.steps) - 1):
+        if plan.steps[s].phase != "rs" or plan.steps[s + 1].phase != "ag":
+            continue
+        fused = [list(o) for o in ops[s]]
+        rest = []
+        for o in ops[s + 1]:
+            r, b, _, dsts = o
+            tgt = [f for f in fused if f[0] == r and f[1] == b and len(f[2]) >= 2]
+            if tgt:
+                tgt[0][3] = tgt[0][3] + dsts
+            else:
+                rest.append(o)
+        if len(rest) == len(ops[s + 1]) or not _hazard_free(fused):
+            continue
+        ops[s], ops[s + 1] = fused, rest
+    return [st for st in ops if st]
+
+
+def _hazard_free(step_ops) -> bool:
+    for i, (_, b, _, dsts) in enumerate(step_ops):
+        for j, (_, b2, ins2, dsts2) in enumerate(step_ops):
+            if i == j or b != b2:
+                continue
+            if set(dsts) & (set(ins2) | set(dsts2)):
+                return False
+    return True
+
+
+def executed_step_coeffs(plan: Plan, esize: int) -> list:
+    """Per-step GenModel coefficients of the executed plan (reading A6x; P:441-444 applied
+    to executed_steps): the entry flag round first (A = 1, nothing moved: its α is the
+    round trip that makes the inputs visible), then per executed step
+
+      B = max over ranks of max(bytes into the rank, bytes out of it) — every input read from
+          another rank moves bytes from it to the reader, every destination on another rank
+          moves bytes from the writer to it; NVLink is full duplex, so a fused step's RS and
+          AG traffic overlap (P:178 "data through a link");
+      C = max over ranks of Σ (k − 1)·|block| over its ops with k >= 2 inputs  (P:178);
+      D = max over ranks of Σ (k + 1)·|block| over the same ops (P:229-238, P:402; copies 0);
+      w = 1 + the most distinct ranks sending into one rank (reading Q8)."""
+    n = plan.n
+    out = [StepCoeffs(1, 0, 0, 0, 1)]
+    for st in executed_steps(plan):
+        inb, outb, cc, dd = [0] * n, [0] * n, [0] * n, [0] * n
+        senders = [set() for _ in range(n)]
+        for r, b, ins, dsts in st:
+            L = block_size(plan.count, n, b) * esize
+            for q in ins:
+                if q != r:
+                    inb[r] += L
+                    outb[q] += L
+                    senders[r].add(q)
+            for d in dsts:
+                if d != r:
+                    outb[r] += L
+                    inb[d] += L
+                    senders[d].add(r)
+            if len(ins) >= 2:
+                cc[r] += (len(ins) - 1) * L
+                dd[r] += (len(ins) + 1) * L
+        out.append(StepCoeffs(1, max(max(inb), max(outb)), max(cc), max(dd),
+                              1 + max(len(x) for x in senders)))
+    return out
+
+
+def executed_step_coeffs_shared(plan: Plan, esize: int) -> list:
+    """The executed plan when ALL ranks share one GPU (emulated ranks, config C5's "8 ranks
+    per GPU" on one device; reading A6e).  Every rank's data movement then goes through the
+    same HBM, so a step costs its total memory traffic: D = Σ over ranks and ops of
+    (k reads + one write per destination)·|block| (the memory-access term of P:402 summed
+    over the ranks sharing the memory), C = Σ (k − 1)·|block| (the SMs are shared too), and
+    no link term (B = 0, w = 1).  The entry round comes first, as in executed_step_coeffs."""
+    n = plan.n
+    out = [StepCoeffs(1, 0, 0, 0, 1)]
+    for st in executed_steps(plan):
+        cc = dd = 0
+        for r, b, ins, dsts in st:
+            L = block_size(plan.count, n, b) * esize
+            dd += (len(ins) + len(dsts)) * L
+            if len(ins) >= 2:
+                cc += (len(ins) - 1) * L
+        out.append(StepCoeffs(1, 0, cc, dd, 1))
+    return out
+
+
+def predict_executed(plan: Plan, esize: int, p: Params, shared: bool = False) -> dict:
+    """GenModel of the executed plan, fixed-order float64 (the library's contract, bit for
+    bit: genmodel_predict_executed / genmodel_predict_executed_shared)."""
+    co = executed_step_coeffs_shared(plan, esize) if shared else executed_step_coeffs(plan, esize)
+    return predict_f64(co, uniform_step_params(p, len(co)))

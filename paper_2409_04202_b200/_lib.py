@@ -88,6 +88,7 @@ _SIGS = {
     "gt_plan_free": (None, [P]),
     "gt_plan_from_json": (I32, [ctypes.c_char_p, ctypes.POINTER(P), ctypes.POINTER(I32)]),
     "genmodel_predict_executed": (I32, [P, ctypes.POINTER(GmParams), ctypes.POINTER(GmBreakdown)]),
+    "genmodel_predict_executed_shared": (I32, [P, ctypes.POINTER(GmParams), ctypes.POINTER(GmBreakdown)]),
     "ar_comm_create": (I32, [I32, I32, I32, ctypes.POINTER(P)]),
     "ar_comm_create_multi": (I32, [I32, I32, I32, I32, ctypes.POINTER(P)]),
     "ar_comm_create_local": (I32, [I32, I32, ctypes.POINTER(P)]),

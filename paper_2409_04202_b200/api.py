@@ -157,6 +157,12 @@ class Plan:
         check(lib.genmodel_predict_executed(self._h, ctypes.byref(params), ctypes.byref(out)))
         return out.as_dict()
 
+    def predict_executed_shared(self, params: GmParams) -> dict:
+        """Executed-plan GenModel with all ranks on one GPU (reading A6e)."""
+        out = GmBreakdown()
+        check(lib.genmodel_predict_executed_shared(self._h, ctypes.byref(params), ctypes.byref(out)))
+        return out.as_dict()
+
     def simulate(self, params: GmParams | None = None, topology_json: str | None = None) -> dict:
         """Incast-aware flow-level simulation (gt_plan_simulate; NEXT #2), on the plan's own
         topology or on `topology_json`.  Adds "steps"."""

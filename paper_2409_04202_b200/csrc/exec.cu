@@ -2041,71 +2041,94 @@ int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
   return AR_OK;
 }
 
+// GenModel of the executed plan (reading A6x): the per-step formula
+// applied to the lowered programs — the entry flag round, then every slot in which some rank
+// runs ops.  shared = all ranks on one GPU (reading A6e): a slot costs the memory traffic of
+// all ranks together (D = Σ (sources + destinations)·len, C = Σ (k − 1)·len), no link term.
+static Breakdown predict_executed_impl(const gt_plan *plan, const gm_params *params, bool shared) {
+  std::vector<DevStep> st;
+  std::vector<DevOp> ops;
+  std::vector<DevWait> w;
+  std::vector<int> rk, pb, pl;
+  const int n = plan->plan.n;
+  lower_plan(plan->plan, n, st, ops, w, rk, pb, pl);
+  const int64_t es = plan->esize;
+  // per executed slot: in/out bytes per rank (full duplex), reduce work, distinct peers
+  std::map<int, std::vector<int64_t>> in, outb, cc, dd;
+  std::map<int, std::vector<std::set<int>>> peers;
+  for (int r = 0; r < n; r++)
+    for (int i = 0; i < pl[r]; i++) {
+      const DevStep &d = st[pb[r] + i];
+      if (d.op_count == 0) continue;
+      const int s = d.slot;
+      if (!in.count(s)) {
+        in[s].assign(n, 0); outb[s].assign(n, 0); cc[s].assign(n, 0); dd[s].assign(n, 0);
+        peers[s].assign(n, std::set<int>());
+      }
+      for (int k = 0; k < d.op_count; k++) {
+        const DevOp &x = ops[d.op_begin + k];
+        const int64_t L = x.len * es;
+        for (int j = 0; j < x.nsrc; j++) {
+          const int q = rk[x.src_begin + j];
+          if (q == r) continue;
+          in[s][r] += L;
+          outb[s][q] += L;
+          peers[s][r].insert(q);
+        }
+        for (int j = 0; j < x.ndst; j++) {
+          const int q = rk[x.dst_begin + j];
+          if (q == r) continue;
+          outb[s][r] += L;
+          in[s][q] += L;
+          peers[s][q].insert(r);
+        }
+        if (x.nsrc >= 2) cc[s][r] += (x.nsrc - 1) * L;
+        if (shared) dd[s][r] += (x.nsrc + x.ndst) * L;
+        else if (x.nsrc >= 2) dd[s][r] += (x.nsrc + 1) * L;
+      }
+    }
+  std::vector<StepCoeffs> co;
+  co.push_back(StepCoeffs{1, 0, 0, 0, 1});   // the entry flag round (one alpha)
+  for (auto &kv : in) {
+    const int s = kv.first;
+    StepCoeffs c{1, 0, 0, 0, 1};
+    for (int r = 0; r < n; r++) {
+      if (shared) {
+        c.C += cc[s][r];
+        c.D += dd[s][r];
+        continue;
+      }
+      c.B = std::max(c.B, std::max(in[s][r], outb[s][r]));
+      c.C = std::max(c.C, cc[s][r]);
+      c.D = std::max(c.D, dd[s][r]);
+      c.w = std::max(c.w, 1 + (int)peers[s][r].size());
+    }
+    co.push_back(c);
+  }
+  Params p;
+  p.alpha = params->alpha; p.beta = params->beta; p.gamma = params->gamma; p.delta = params->delta;
+  p.epsilon = params->epsilon; p.w_t = params->w_t; p.has_combined = params->has_combined != 0;
+  p.combined = params->combined;
+  return predict_f64(co, uniform_step_params(p, co.size()));
+}
+
+static void fill_breakdown(gm_breakdown *out, const Breakdown &b) {
+  out->latency = b.latency; out->bandwidth = b.bandwidth; out->compute = b.compute;
+  out->memory = b.memory; out->incast = b.incast; out->total = b.total;
+}
+
 int genmodel_predict_executed(const gt_plan *plan, const gm_params *params, gm_breakdown *out) {
   SYS_TRY({
     if (!plan || !params || !out) throw InvalidArg("null argument");
-    std::vector<DevStep> st;
-    std::vector<DevOp> ops;
-    std::vector<DevWait> w;
-    std::vector<int> rk, pb, pl;
-    const int n = plan->plan.n;
-    lower_plan(plan->plan, n, st, ops, w, rk, pb, pl);
-    const int64_t es = plan->esize;
-    // per executed slot: in/out bytes per rank (full duplex), reduce work, distinct peers
-    std::map<int, std::vector<int64_t>> in, outb, cc, dd;
-    std::map<int, std::vector<std::set<int>>> peers;
-    for (int r = 0; r < n; r++)
-      for (int i = 0; i < pl[r]; i++) {
-        const DevStep &d = st[pb[r] + i];
-        if (d.op_count == 0) continue;
-        const int s = d.slot;
-        if (!in.count(s)) {
-          in[s].assign(n, 0); outb[s].assign(n, 0); cc[s].assign(n, 0); dd[s].assign(n, 0);
-          peers[s].assign(n, std::set<int>());
-        }
-        for (int k = 0; k < d.op_count; k++) {
-          const DevOp &x = ops[d.op_begin + k];
-          const int64_t L = x.len * es;
-          for (int j = 0; j < x.nsrc; j++) {
-            const int q = rk[x.src_begin + j];
-            if (q == r) continue;
-            in[s][r] += L;
-            outb[s][q] += L;
-            peers[s][r].insert(q);
-          }
-          for (int j = 0; j < x.ndst; j++) {
-            const int q = rk[x.dst_begin + j];
-            if (q == r) continue;
-            outb[s][r] += L;
-            in[s][q] += L;
-            peers[s][q].insert(r);
-          }
-          if (x.nsrc >= 2) {
-            cc[s][r] += (x.nsrc - 1) * L;
-            dd[s][r] += (x.nsrc + 1) * L;
-          }
-        }
-      }
-    std::vector<StepCoeffs> co;
-    co.push_back(StepCoeffs{1, 0, 0, 0, 1});   // the entry flag round (one alpha)
-    for (auto &kv : in) {
-      const int s = kv.first;
-      StepCoeffs c{1, 0, 0, 0, 1};
-      for (int r = 0; r < n; r++) {
-        c.B = std::max(c.B, std::max(in[s][r], outb[s][r]));
-        c.C = std::max(c.C, cc[s][r]);
-        c.D = std::max(c.D, dd[s][r]);
-        c.w = std::max(c.w, 1 + (int)peers[s][r].size());
-      }
-      co.push_back(c);
-    }
-    Params p;
-    p.alpha = params->alpha; p.beta = params->beta; p.gamma = params->gamma; p.delta = params->delta;
-    p.epsilon = params->epsilon; p.w_t = params->w_t; p.has_combined = params->has_combined != 0;
-    p.combined = params->combined;
-    Breakdown b = predict_f64(co, uniform_step_params(p, co.size()));
-    out->latency = b.latency; out->bandwidth = b.bandwidth; out->compute = b.compute;
-    out->memory = b.memory; out->incast = b.incast; out->total = b.total;
+    fill_breakdown(out, predict_executed_impl(plan, params, false));
+    return AR_OK;
+  })
+}
+
+int genmodel_predict_executed_shared(const gt_plan *plan, const gm_params *params, gm_breakdown *out) {
+  SYS_TRY({
+    if (!plan || !params || !out) throw InvalidArg("null argument");
+    fill_breakdown(out, predict_executed_impl(plan, params, true));
     return AR_OK;
   })
 }

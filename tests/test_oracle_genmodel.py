@@ -271,3 +271,123 @@ def test_oneshot_row_matches_line_count(n):
     # incast as CPS: every rank receives from N-1 senders (w = N, reading Q8)
     _, _, _, _, In2, den2 = G.closed_form_terms("oneshot", n, S, 1)
     assert Fraction(In2, den2) == max(n - 1, 0) * Fraction(Bn, den)
+
+
+# ---------------------------------------------------------------- executed plan (reading A6x/A6e)
+
+def _exact_executed(plan, p, shared=False):
+    co = G.executed_step_coeffs_shared(plan, 4) if shared else G.executed_step_coeffs(plan, 4)
+    return co, G.predict_exact(co, G.uniform_step_params(p, len(co)))
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8, 12, 16])
+@pytest.mark.parametrize("wt", [2, 5, 64])
+def test_executed_cps_is_table2_row(n, wt):
+    """CPS fuses its one RS step with its AG step, and the entry round takes the AG step's α:
+    A = 2 and the full-duplex B of the fused step = 2(N−1)S/N — Table 2's CPS row
+    term for term, incast included (w = N), exact rationals."""
+    S = n * 96
+    p = G.Params(1e-6, 1e-9, 3e-10, 2e-10, 5e-11, wt)
+    _, got = _exact_executed(P.build_plan("cps", n, S // 4), p)
+    ref = G.closed_form_exact("cps", n, S, p)
+    for key in ref:
+        assert got[key] == ref[key], key
+
+
+@pytest.mark.parametrize("kind", ["ring", "rhd", "hcps:4,2", "hcps:2,4", "hcps:2,2,2", "hcps:3,2",
+                                  "hcps:2,3", "hcps:2,2,3", "hcps:6,2"])
+def test_executed_multistep_equals_table2_below_threshold(kind):
+    """Ring / RHD / HCPS: the fused step moves RS and AG bytes at once, but since every rank
+    sends and receives equally, max(in, out) summed over the executed steps equals Table 2's B
+    (Eq. 2: 2(N−1)S/N); A (entry + executed steps) equals 2(N−1), 2·log N, 2m; C and D
+    unchanged.  Exact when no step reaches the incast threshold."""
+    name, f = P.parse_kind(kind)
+    n = 8
+    if name == "hcps":
+        n = 1
+        for x in f:
+            n *= x
+    S = n * 96
+    p = G.Params(1e-6, 1e-9, 3e-10, 2e-10, 5e-11, 64)
+    _, got = _exact_executed(P.build_plan(kind, n, S // 4), p)
+    ref = G.closed_form_exact(name, n, S, p, f)
+    for key in ref:
+        assert got[key] == ref[key], key
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8, 12])
+def test_executed_rb_halves_bandwidth_and_incast(n):
+    """RB fused: the root pulls (N−1)S and pushes (N−1)S in the same step; full duplex makes
+    B = (N−1)S, half of Table 2's 2(N−1)S, and the incast charged on it (w = N, the
+    root's N−1 senders) half of the printed value; A, C, D as printed (γ = (N−1)S, Q7)."""
+    S = n * 96
+    p = G.Params(1e-6, 1e-9, 3e-10, 2e-10, 5e-11, 1)
+    co, got = _exact_executed(P.build_plan("rb", n, S // 4), p)
+    ref = G.closed_form_exact("rb", n, S, p)
+    assert [c.A for c in co] == [1, 1]
+    assert got["bandwidth"] * 2 == ref["bandwidth"]
+    assert got["incast"] * 2 == ref["incast"]
+    for key in ("latency", "compute", "memory"):
+        assert got[key] == ref[key], key
+
+
+def test_executed_ring4_hand_count():
+    """Ring at N = 4, S bytes, hand-counted (reading Q10b: the AG runs the other way
+    round the ring).  Entry; RS steps 0 and 1: each rank pulls S/4 from its left neighbour
+    (B = S/4, C = S/4, D = 3S/4, w = 2); RS step 2 fused with AG step 0: it pulls S/4 and pushes
+    its result S/4 to its right... neighbour in the reversed ring, receiving from both sides
+    (B = S/2, w = 3); AG steps 1 and 2: copies of S/4 (B = S/4, C = D = 0, w = 2)."""
+    S = 4 * 1000
+    co = G.executed_step_coeffs(P.build_plan("ring", 4, S // 4), 4)
+    q = S // 4
+    assert [(c.A, c.B, c.C, c.D, c.w) for c in co] == [
+        (1, 0, 0, 0, 1), (1, q, q, 3 * q, 2), (1, q, q, 3 * q, 2), (1, 2 * q, q, 3 * q, 3),
+        (1, q, 0, 0, 2), (1, q, 0, 0, 2)]
+
+
+def test_executed_rhd4_is_hcps22():
+    """N = 4: RHD and HCPS[2,2] execute the same steps (SURVEY §8(c) degenerate identity),
+    hand count: entry; S/2 pairwise reduce (B = S/2, C = S/2, D = 3S/2); fused S/4 reduce +
+    S/4 send to the same partner (B = S/2, C = S/4, D = 3S/4); S/2 copy; all w = 2."""
+    S = 4 * 1000
+    h = S // 2
+    want = [(1, 0, 0, 0, 1), (1, h, h, 3 * h, 2), (1, h, h // 2, 3 * h // 2, 2), (1, h, 0, 0, 2)]
+    for kind in ("rhd", "hcps:2,2"):
+        co = G.executed_step_coeffs(P.build_plan(kind, 4, S // 4), 4)
+        assert [(c.A, c.B, c.C, c.D, c.w) for c in co] == want, kind
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8, 16])
+def test_executed_shared_hbm_bytes(n):
+    """Reading A6e (all ranks on one GPU): the memory term counts every byte any rank reads or
+    writes.  CPS: each rank buffer is read once and written once, D = 2·N·S (bench.py's
+    algorithmic bytes); Ring: per rank (N−1) two-input reduces (3 block accesses each), one
+    extra fused write and N−2 copies (2 accesses each): D = (5N − 6)·S; RB: the root reads N
+    buffers and writes N: D = 2·N·S.  C = Σ (k − 1)|b| = (N−1)·S for all three."""
+    S = n * 96
+    for kind, dmul in (("cps", 2 * n), ("ring", 5 * n - 6), ("rb", 2 * n)):
+        co = G.executed_step_coeffs_shared(P.build_plan(kind, n, S // 4), 4)
+        assert sum(c.D for c in co) == dmul * S, kind
+        assert sum(c.C for c in co) == (n - 1) * S, kind
+        assert all(c.B == 0 and c.w == 1 for c in co)
+
+
+def test_executed_fusion_refused_on_hazard():
+    """The fusion rule's hazard clause: an AG step whose transfer would make the fused RS
+    step write a (rank, block) another op of that step reads is left unfused."""
+    n, count = 2, 8
+    rs = P.Step("rs", "x", [P.Reduce(0, 0, (0, 1)), P.Reduce(1, 1, (0, 1))])
+    P.add_implied_transfers(rs, count, n)
+    # rank 0 sends block 0 to rank 1 — but rank 1's reduce of step 0 reads only block 1, so
+    # this one fuses; a transfer of block 1 from rank 0 (who did not reduce it) cannot
+    ag = P.Step("ag", "y", [], [P.Transfer(0, 1, 0, 4), P.Transfer(1, 0, 1, 4)])
+    ex = G.executed_steps(P.Plan(n, count, [rs, ag]))
+    assert len(ex) == 1 and sorted(tuple(o) for o in ex[0]) == [(0, 0, (0, 1), (0, 1)), (1, 1, (0, 1), (1, 0))]
+    # N = 3: rank 2's reduce of block 0 reads (1, 0); fusing rank 0's send of block 0 to rank 1
+    # would write (1, 0) in the same step -> no fusion at all (both RS steps are hazard-free)
+    n3, c3 = 3, 9
+    rs2 = P.Step("rs", "x", [P.Reduce(0, 0, (0, 1)), P.Reduce(2, 0, (1, 2))])
+    P.check_step_hazards(rs2)
+    P.add_implied_transfers(rs2, c3, n3)
+    ag2 = P.Step("ag", "y", [], [P.Transfer(0, 1, 0, 3)])
+    assert len(G.executed_steps(P.Plan(n3, c3, [rs2, ag2]))) == 2

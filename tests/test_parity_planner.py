@@ -245,3 +245,40 @@ def test_flow_simulator_parity(which):
     lib = G.Plan.from_topology(doc, 99999, "bf16")
     oplan, _ = GT.gentree(t, 99999, 2)
     _sim_close(lib.simulate(lib_params(p)), FS.simulate_flows(t, oplan, 2, p))
+
+
+@pytest.mark.parametrize("shared", [False, True])
+def test_predict_executed_parity(shared):
+    """genmodel_predict_executed[_shared] (the library derives the executed steps from its
+    lowered device tables) vs oracle.genmodel.predict_executed (executed steps derived from
+    the plan and the stated fusion rule, reading A6x / A6e): bit-identical doubles over every
+    plan kind, single-switch N = 2..16, the C1/C5/asymmetric trees and rearrangement trees,
+    degenerate (count < N), ragged and divisible counts, f32 and bf16."""
+    from tests.topologies import cross_dc
+    p = OG.Params(3e-6, 1 / 900e9, 1e-13, 1 / 6.54e12, 2e-13, 3)
+    lp = lib_params(p)
+
+    def ss(n):
+        return T.single_switch_doc(n, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
+                                   {"gamma": 0.0, "delta": 4 / 6.54e12})
+    docs = [(n, ss(n)) for n in (2, 3, 4, 5, 6, 8, 12, 16)]
+    docs += [(4, T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])),
+             (7, T.two_level_doc([3, 4], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])),
+             (64, T.two_level_doc([8] * 8, T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"]))]
+    docs += [(sh[0] * sh[1] + sh[2] * sh[3], cross_dc(*sh)) for sh in [(2, 2, 2, 2), (2, 4, 2, 2)]]
+    checked = 0
+    for n, doc in docs:
+        t = T.parse_topology(doc)
+        for kind in (None, "cps", "ring", "rb", "rhd", "hcps:2,2", "hcps:4,2", "hcps:2,2,2", "hcps:2,4", "hcps:3,2"):
+            for count in (1, n - 1, 1000003, 1000000, 7777):
+                for dtype in ("f32", "bf16"):
+                    try:
+                        gplan = G.Plan.from_topology(doc, count, dtype, None, kind)
+                    except G.ArInvalid:
+                        continue
+                    oplan, _ = GT.gentree(t, count, ES[dtype], force=kind)
+                    want = OG.predict_executed(oplan, ES[dtype], p, shared)
+                    got = (gplan.predict_executed_shared if shared else gplan.predict_executed)(lp)
+                    same_breakdown(got, want)
+                    checked += 1
+    assert checked > 500
