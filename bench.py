@@ -399,26 +399,41 @@ def main():
         except Exception as e:   # multicast unavailable: report, do not fail the bench
             nvls = {"unavailable": str(e)[:200]}
 
-    # NCCL on the same buffer (N > 1)
+    # NCCL on the same data size (N > 1), three variants (the config's Ring
+    # comparator, NCCL's default choice, and NVLS disabled).  NCCL reads NCCL_ALGO when a
+    # communicator is initialised, so each variant is its own process group, created and
+    # initialised (first collective) while NCCL_ALGO is set; "^NVLS,NVLSTree" excludes the
+    # NVSwitch algorithms without touching the process-wide NCCL_NVLS_ENABLE parameter.
     nccl = None
     if dist is not None and not args.no_nccl:
         t = torch.empty(count, dtype=torch.bfloat16 if args.dtype == "bf16" else torch.float32, device="cuda")
         t.normal_()
-        for _ in range(args.warmup):
-            dist.all_reduce(t)
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            dist.all_reduce(t)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        tt = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        nccl = {"busbw": round(busbw(nbytes, n, float(tt.item())), 2), "ms_per_step": round(float(tt.item()) * 1e3, 4),
-                "version": ".".join(map(str, torch.cuda.nccl.version())),
-                "algo_env": os.environ.get("NCCL_ALGO", "default")}
+        nccl = {"version": ".".join(map(str, torch.cuda.nccl.version()))}
+        for key, algo in (("default", None), ("ring", "Ring"), ("nvls_off", "^NVLS,NVLSTree")):
+            old = os.environ.get("NCCL_ALGO")
+            try:
+                if algo is not None:
+                    os.environ["NCCL_ALGO"] = algo
+                grp = dist.new_group(list(range(n)), backend="nccl") if algo is not None else None
+                for _ in range(max(1, args.warmup)):
+                    dist.all_reduce(t, group=grp)
+                torch.cuda.synchronize()
+            finally:
+                if old is None:
+                    os.environ.pop("NCCL_ALGO", None)
+                else:
+                    os.environ["NCCL_ALGO"] = old
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                dist.all_reduce(t, group=grp)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tt = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            nccl[key] = {"busbw": round(busbw(nbytes, n, float(tt.item())), 2),
+                         "ms_per_step": round(float(tt.item()) * 1e3, 4), "NCCL_ALGO": algo or "unset"}
         del t
 
     # end to end through the C-ABI from pinned host memory
@@ -475,6 +490,7 @@ def main():
     }
     if nccl:
         line["nccl"] = nccl
+        line["vs_nccl"] = {k: round(value / v["busbw"], 3) for k, v in nccl.items() if isinstance(v, dict)}
     if nvls:
         line["nvls"] = nvls
     print(json.dumps(line), flush=True)

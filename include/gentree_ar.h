@@ -115,6 +115,18 @@ typedef struct gt_plan gt_plan; /* opaque, immutable, library-owned, thread-shar
 int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
                  const char *force_kind, gt_plan **out);
 
+/* GenTree with the NVLS plan kind as an extra candidate (reading NV1;
+ * the paper's min-GenModel selection): builds gentree_plan's plan, and on a
+ * single-switch topology with dtype AR_F32 replaces it by the NVLS plan when
+ * genmodel_choose_nvls(plan, params, nvls_params) prefers NVLS.  NVLS plans (also
+ * force_kind "nvls" in gentree_plan; fp32 only, single switch) have the CPS data movement
+ * and "switch_reduce": true in their JSON; every element ends as the correctly rounded fp32
+ * sum of the ranks' inputs (reading NV2, measured) — the oracle's exactsum, bit for bit.
+ * They run through allreduce_exec on a communicator with an attached NVLS buffer
+ * (ar_comm_attach_nvls; dptr = that buffer).  params and nvls_params are required. */
+int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
+                      const gm_params *nvls_params, gt_plan **out);
+
 /* Convenience: single switch with `world` ranks and uniform `params` (required). */
 int gentree_plan_single_switch(int32_t world, uint64_t count, int32_t dtype, const gm_params *params,
                                const char *force_kind, gt_plan **out);
@@ -340,8 +352,9 @@ int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *ne
  *   3. ar_nvls_bind on every rank (allocate, bind, map unicast + multicast) -> the unicast
  *      device pointer of this rank's `bytes`-byte buffer (library-owned; freed by destroy),
  *      then a host barrier before the first allreduce_exec_nvls.
- * allreduce_exec_nvls: in-place SUM of the first `count` elements (count a multiple of
- * world * 16 / element size), stream-ordered, graph-capturable.  Errors: AR_EINVAL for bad
+ * allreduce_exec_nvls: in-place SUM of the first `count` elements (fp32 any count, bf16 even
+ * counts; whole 16-byte vectors split evenly over the ranks, the tail on the last rank),
+ * stream-ordered, graph-capturable.  Errors: AR_EINVAL for bad
  * arguments, AR_ESYS for CUDA/driver failures (e.g. multicast unsupported). */
 typedef struct ar_nvls ar_nvls;
 int ar_nvls_create(int32_t rank, int32_t world, int32_t cuda_device, uint64_t bytes, ar_nvls **out,
@@ -351,6 +364,11 @@ int ar_nvls_bind(ar_nvls *nvls, void **uc_ptr_out);
 int allreduce_exec_nvls(ar_nvls *nvls, uint64_t count, int32_t dtype, void *stream);
 int ar_nvls_get_async_error(ar_nvls *nvls);
 int ar_nvls_destroy(ar_nvls *nvls);
+/* Attach this rank's NVLS buffer to a one-rank-per-GPU communicator: allreduce_exec then runs
+ * NVLS plans (gentree_plan_nvls / force_kind "nvls") on it, dptr = the buffer's unicast
+ * pointer from ar_nvls_bind, any count up to its size (fp32; bf16 even counts).  The comm does
+ * not own it.  AR_EINVAL for emulated / several-ranks-per-GPU comms. */
+int ar_comm_attach_nvls(ar_comm *comm, ar_nvls *nvls);
 
 /* ------------------------------------------------------------------ inputs and harness */
 

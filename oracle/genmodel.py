@@ -419,5 +419,9 @@ def executed_step_coeffs_shared(plan: Plan, esize: int) -> list:
 def predict_executed(plan: Plan, esize: int, p: Params, shared: bool = False) -> dict:
     """GenModel of the executed plan, fixed-order float64 (the library's contract, bit for
     bit: genmodel_predict_executed / genmodel_predict_executed_shared)."""
+    if plan.switch_reduce:   # NVLS plan: the NV1 row
+        if shared:
+            raise ValueError("an NVLS plan cannot run on ranks sharing one GPU")
+        return closed_form_f64("nvls", plan.n, plan.count * esize, p)
     co = executed_step_coeffs_shared(plan, esize) if shared else executed_step_coeffs(plan, esize)
     return predict_f64(co, uniform_step_params(p, len(co)))

@@ -153,6 +153,18 @@ def gentree(topo, count: int, esize: int, params: Params | None = None,
     if count < 1:
         raise PlanError("count must be >= 1")
     S = count * esize
+    if force == "nvls":
+        # NVLS plan kind (readings NV1/NV2): CPS's data movement on one
+        # NVSwitch, the reduce done in the switch; fp32 only (its bf16 rounding is not RNE)
+        if esize != 4:
+            raise PlanError("NVLS plans are fp32 only (reading NV2)")
+        if sum(1 for nd in topo.nodes.values() if nd.kind != "server") != 1:
+            raise PlanError("NVLS plans need a single-switch topology")
+        plan, reps = gentree(topo, count, esize, params, "cps")
+        plan.switch_reduce = True
+        for rp in reps:
+            rp.chosen = "nvls"
+        return plan, reps
     if force is not None:
         fname, ff = parse_kind(force)
         if fname == "rb":
@@ -380,3 +392,19 @@ def predict_plan(topo, plan: Plan, esize: int, params: Params | None = None) -> 
     sp = (uniform_step_params(params, len(coeffs)) if params is not None
           else topo_step_params(topo, plan))
     return predict_f64(coeffs, sp)
+
+
+def gentree_nvls(topo, count: int, esize: int, params: Params, nvls_params: Params):
+    """GenTree with the NVLS plan kind as one more candidate (reading NV1; the paper's
+    minimum-GenModel choice): on a single-switch topology in fp32, the NVLS plan
+    replaces GenTree's plan iff the NVLS row's closed form (P:441-444 with its own α, β) is
+    strictly below the executed-plan prediction of GenTree's plan (ties keep the plan)."""
+    from .genmodel import predict_executed
+    plan, reps = gentree(topo, count, esize, params)
+    single = sum(1 for nd in topo.nodes.values() if nd.kind != "server") == 1
+    if esize == 4 and single:
+        t_plan = predict_executed(plan, esize, params)["total"]
+        t_nvls = closed_form_f64("nvls", len(topo.servers), count * esize, nvls_params)["total"]
+        if t_nvls < t_plan:
+            return gentree(topo, count, esize, params, "nvls")
+    return plan, reps

@@ -65,6 +65,10 @@ class Plan:
     n: int
     count: int
     steps: list
+    # NVLS plan kind (readings NV1/NV2): the CPS data movement
+    # with every fan-in-N reduce done in the NVSwitch — each element becomes the correctly
+    # rounded fp32 sum of the ranks' inputs, not a plan-order sum
+    switch_reduce: bool = False
 
     @property
     def nsteps(self) -> int:
@@ -399,7 +403,10 @@ def plan_to_obj(plan: Plan, dtype: str) -> dict:
             "transfers": [{"block": t.block, "dst": t.dst, "size": t.size, "src": t.src}
                           for t in sorted(st.transfers, key=lambda t: (t.dst, t.block, t.src))],
         })
-    return {"count": plan.count, "dtype": dtype, "n": plan.n, "steps": steps}
+    obj = {"count": plan.count, "dtype": dtype, "n": plan.n, "steps": steps}
+    if plan.switch_reduce:
+        obj["switch_reduce"] = True
+    return obj
 
 
 def plan_to_json(plan: Plan, dtype: str) -> str:

@@ -105,6 +105,20 @@ class Plan:
         return cls(h)
 
     @classmethod
+    def from_topology_nvls(cls, topology_json: str, count: int, dtype, params: GmParams,
+                           nvls_params: GmParams) -> "Plan":
+        """GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1)."""
+        h = ctypes.c_void_p()
+        check(lib.gentree_plan_nvls(topology_json.encode(), count, dtype_code(dtype), ctypes.byref(params),
+                                    ctypes.byref(nvls_params), ctypes.byref(h)))
+        return cls(h)
+
+    @property
+    def switch_reduce(self) -> bool:
+        """True for an NVLS plan (the reduce happens in the NVSwitch)."""
+        return '"switch_reduce":true' in self.to_json()
+
+    @classmethod
     def single_switch(cls, world: int, count: int, dtype="f32", params: GmParams | None = None,
                       force: str | None = None) -> "Plan":
         h = ctypes.c_void_p()
@@ -261,6 +275,11 @@ class Comm:
         blobs = [None] * self.nproc
         dist.all_gather_object(blobs, blob, group=group)
         self.open_peers(blobs)
+
+    def attach_nvls(self, nvls: "Nvls"):
+        """Run NVLS plans on this comm with `nvls`'s buffer (ar_comm_attach_nvls)."""
+        check(lib.ar_comm_attach_nvls(self._h, nvls._h))
+        self._nvls = nvls
 
     def set_trace(self, enable: bool = True):
         check(lib.ar_comm_set_trace(self._h, 1 if enable else 0))

@@ -204,7 +204,23 @@ static int make_plan(const Topology &t, uint64_t count, int32_t dtype, const gm_
     p = to_params(params);
   }
   std::string force = force_kind ? force_kind : "";
+  const bool nvls = force == "nvls";
+  if (nvls) {
+    // NVLS plan kind: the single-switch CPS data movement with the
+    // reduce in the NVSwitch.  fp32 only: the switch returns the correctly rounded fp32 sum
+    // (reading NV2, measured), which has a plain definition to check against; its bf16
+    // rounding is not round-to-nearest-even, so bf16 stays on the plan-order kinds.
+    if (dtype != AR_F32) throw InvalidArg("NVLS plans are fp32 only (reading NV2: the switch's bf16 rounding is not RNE)");
+    int switches = 0;
+    for (auto &nd : t.nodes) switches += nd.server ? 0 : 1;
+    if (switches != 1) throw InvalidArg("NVLS plans need a single-switch topology (one NVSwitch domain)");
+    force = "cps";
+  }
   PlanResult r = gentree(t, (int64_t)count, esize_of(dtype), params ? &p : nullptr, force);
+  if (nvls) {
+    r.plan.switch_reduce = true;
+    for (auto &rep : r.reports) rep.chosen = "nvls";
+  }
   gt_plan *g = new gt_plan();
   g->plan = std::move(r.plan);
   g->reports = std::move(r.reports);
@@ -225,6 +241,37 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
     if (!topology_json) throw InvalidArg("null topology");
     Topology t = parse_topology(topology_json);
     return make_plan(t, count, dtype, params, force_kind, out);
+  })
+}
+
+int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
+                      const gm_params *nvls_params, gt_plan **out) {
+  AR_TRY({
+    if (!topology_json || !nvls_params || !params || !out) throw InvalidArg("null argument");
+    check_params(nvls_params);
+    Topology t = parse_topology(topology_json);
+    gt_plan *g = nullptr;
+    int rc = make_plan(t, count, dtype, params, nullptr, &g);
+    if (rc != AR_OK) return rc;
+    int switches = 0;
+    for (auto &nd : t.nodes) switches += nd.server ? 0 : 1;
+    if (dtype == AR_F32 && switches == 1) {
+      int32_t use = 0;
+      double tp = 0, tn = 0;
+      rc = genmodel_choose_nvls(g, params, nvls_params, &use, &tp, &tn);
+      if (rc != AR_OK) {
+        delete g;
+        return rc;
+      }
+      if (use) {
+        delete g;
+        g = nullptr;
+        rc = make_plan(t, count, dtype, params, "nvls", &g);
+        if (rc != AR_OK) return rc;
+      }
+    }
+    *out = g;
+    return AR_OK;
   })
 }
 
@@ -276,6 +323,12 @@ int gt_plan_info(const gt_plan *plan, int32_t *n_ranks, int32_t *n_steps, uint64
 int genmodel_predict(const gt_plan *plan, const gm_params *params, gm_breakdown *out) {
   AR_TRY({
     if (!plan || !out) throw InvalidArg("null argument");
+    if (plan->plan.switch_reduce) {   // NVLS: the NV1 row (no plan-order steps)
+      if (!params) throw InvalidArg("an NVLS plan is predicted with explicit (NVLS-row) params");
+      check_params(params);
+      fill(out, closed_form_f64("nvls", plan->plan.n, plan->plan.count * (int64_t)plan->esize, to_params(params), {}));
+      return AR_OK;
+    }
     auto co = step_coeffs(plan->plan, plan->esize);
     std::vector<StepParams> sp;
     if (params) {

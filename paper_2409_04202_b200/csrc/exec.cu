@@ -1267,6 +1267,7 @@ struct ar_comm {
   char *checked_base = nullptr;                // local comms: last buffer extent validated
   size_t checked_need = 0;
   bool entry_fence = false;                    // AR_ENTRY_FENCE=1: fence.acq_rel.sys before relaxed entry flags
+  ar_nvls *nvls = nullptr;                     // NVLS buffer for switch_reduce plans (ar_comm_attach_nvls)
 };
 
 namespace {
@@ -2025,6 +2026,15 @@ int ar_comm_destroy(ar_comm *c) {
 
 const char *ar_comm_last_kernel(ar_comm *c) { return c ? c->last_kernel : ""; }
 
+int ar_comm_attach_nvls(ar_comm *c, ar_nvls *nvls) {
+  SYS_TRY({
+    if (!c) throw InvalidArg("null comm");
+    if (c->local || c->rpp != 1) throw InvalidArg("NVLS needs one rank per GPU");
+    c->nvls = nvls;
+    return AR_OK;
+  })
+}
+
 int ar_comm_set_oneshot_max(ar_comm *c, uint64_t bytes) {
   SYS_TRY({
     if (!c) throw InvalidArg("null comm");
@@ -2046,6 +2056,14 @@ int ar_comm_last_launch_count(ar_comm *c, int32_t *kernels) {
 // runs ops.  shared = all ranks on one GPU (reading A6e): a slot costs the memory traffic of
 // all ranks together (D = Σ (sources + destinations)·len, C = Σ (k − 1)·len), no link term.
 static Breakdown predict_executed_impl(const gt_plan *plan, const gm_params *params, bool shared) {
+  if (plan->plan.switch_reduce) {   // NVLS: its closed-form row (reading NV1)
+    if (shared) throw InvalidArg("an NVLS plan cannot run on ranks sharing one GPU");
+    Params q;
+    q.alpha = params->alpha; q.beta = params->beta; q.gamma = params->gamma; q.delta = params->delta;
+    q.epsilon = params->epsilon; q.w_t = params->w_t; q.has_combined = params->has_combined != 0;
+    q.combined = params->combined;
+    return closed_form_f64("nvls", plan->plan.n, plan->plan.count * (int64_t)plan->esize, q, {});
+  }
   std::vector<DevStep> st;
   std::vector<DevOp> ops;
   std::vector<DevWait> w;
@@ -2173,6 +2191,7 @@ int ar_comm_read_trace(ar_comm *c, uint64_t *out, size_t cap, size_t *n, int32_t
 int ar_plan_lowering_json(const gt_plan *plan, char *buf, size_t cap, size_t *needed) {
   SYS_TRY({
     if (!plan) throw InvalidArg("null plan");
+    if (plan->plan.switch_reduce) throw InvalidArg("an NVLS plan has no step tables (the switch reduces)");
     std::vector<DevStep> st;
     std::vector<DevOp> ops;
     std::vector<DevWait> w;
@@ -2247,6 +2266,17 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   if (!plan->is_allreduce && !movement)
     throw InvalidArg("plan is not an AllReduce (failed symbolic verification); data-movement plans run through "
                      "ar_exec_movement_plan");
+  if (plan->plan.switch_reduce) {
+    // NVLS plan kind: the fan-in-N reduce and the broadcast happen in the NVSwitch
+    if (op != AR_OP_SUM) throw InvalidArg("NVLS plans support AR_OP_SUM only");
+    if (!c->nvls) throw InvalidArg("NVLS plan: attach the NVLS buffer first (ar_comm_attach_nvls)");
+    if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");
+    if ((uint64_t)plan->plan.count != count || plan->dtype != dtype) throw InvalidArg("count/dtype differ from the plan's");
+    nvls_launch(c->nvls, dptr, count, dtype, stream);
+    c->last_launches = 1;
+    c->last_kernel = "nvls_kernel";
+    return AR_OK;
+  }
   if (op != AR_OP_SUM && op != AR_OP_AVG) throw InvalidArg("unknown reduction op");
   const int avg_n = op == AR_OP_AVG ? plan->plan.n : 0;
   if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");

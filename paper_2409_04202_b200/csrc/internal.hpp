@@ -2,6 +2,7 @@
 #pragma once
 
 #include <atomic>
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -20,8 +21,12 @@ struct gt_plan {
   bool is_allreduce = true;    // passed symbolic verification (gt_plan_from_json may load other plans)
 };
 
+struct ar_nvls;
+
 namespace gtar {
 void set_error(const std::string &msg);
+// nvls.cu: in-switch AllReduce of `count` elements of the rank's NVLS buffer (throws)
+void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, void *stream);
 uint64_t next_plan_uid();
 inline int esize_of(int dtype) { return dtype == 0 ? 4 : 2; }
 inline const char *dtype_name(int dtype) { return dtype == 0 ? "f32" : "bf16"; }

@@ -112,7 +112,8 @@ struct NvArgs {
   unsigned long long *flags_uc;   // [2][cta_cap] counters (local copy)
   unsigned long long *flags_mc;
   unsigned long long *epoch_dev;  // [0] epoch, [1] finished-CTA counter, [2] error
-  long long off, len;             // this rank's block (elements)
+  long long off, len;             // this rank's whole 16-byte vectors (elements)
+  long long tail_off, tail_len;   // trailing elements past the last whole vector (rank world-1)
   int world, esize;
   unsigned long long timeout_ns;
   int dyn;                        // 1 = chunks handed out by atomicAdd on epoch_dev[3] (AR_NVLS_DYN)
@@ -178,6 +179,19 @@ __device__ __forceinline__ void mc_store(void *mc, const uint4 &v) {
                  : "memory");
 }
 
+// Scalar tail (count not a multiple of 16 bytes): fp32 one element, bf16 an element pair.
+template <bool BF16>
+__device__ __forceinline__ void tail_reduce_store(char *mc) {
+  uint32_t v;
+  if (BF16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.bf16x2 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.bf16x2 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+  } else {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
+    asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
+  }
+}
+
 template <bool BF16>
 __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant__ NvArgs a) {
   __shared__ unsigned long long s_epoch;
@@ -233,6 +247,12 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
       if (v < v1) mc_store<BF16>(a.mc + v * 16, x[u]);
     }
   }
+  if (a.tail_len > 0 && blockIdx.x == 0) {
+    const int step = BF16 ? 2 : 1;
+    for (long long e = a.tail_off + (long long)threadIdx.x * step; e < a.tail_off + a.tail_len;
+         e += (long long)blockDim.x * step)
+      tail_reduce_store<BF16>(a.mc + e * a.esize);
+  }
   nv_barrier(a, 1, epoch, t0);   // every rank's results have landed in every GPU's buffer
   if (threadIdx.x == 0) {
     if (atomicAdd((unsigned int *)(a.epoch_dev + 1), 1u) == gridDim.x - 1) {
@@ -258,6 +278,44 @@ struct ar_nvls {
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
   bool dyn = false;
 };
+
+namespace gtar {
+// Launch the in-switch AllReduce of `count` elements of this rank's NVLS buffer (dptr must be
+// its unicast base).  Whole 16-byte vectors are split evenly over the ranks (the result does
+// not depend on the split: the switch reduces every element once); the trailing elements past
+// the last whole vector go to the last rank (fp32: any count; bf16: even counts).
+void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, void *stream) {
+  if (!n || !n->bound) throw InvalidArg("nvls buffer not bound");
+  if (dtype != AR_F32 && dtype != AR_BF16) throw InvalidArg("unknown dtype");
+  if ((CUdeviceptr)dptr != n->uc) throw InvalidArg("the buffer is not this communicator's NVLS buffer");
+  const int es = dtype == AR_BF16 ? 2 : 4;
+  if (count < 1 || count * es > n->data_bytes) throw InvalidArg("count exceeds the nvls buffer");
+  if (dtype == AR_BF16 && count % 2) throw InvalidArg("nvls bf16 needs an even count");
+  int cur = -1;
+  RT_CALL(cudaGetDevice(&cur));
+  if (cur != n->device) RT_CALL(cudaSetDevice(n->device));
+  NvArgs a{};
+  a.uc = (char *)n->uc;
+  a.mc = (char *)n->mcva;
+  a.flags_uc = (unsigned long long *)((char *)n->uc + n->data_bytes);
+  a.flags_mc = (unsigned long long *)((char *)n->mcva + n->data_bytes);
+  a.epoch_dev = n->dev_words;
+  const long long E = 16 / es;
+  const long long nvec = (long long)count / E;
+  const long long v0 = nvec * n->rank / n->world, v1 = nvec * (n->rank + 1) / n->world;
+  a.off = v0 * E;
+  a.len = (v1 - v0) * E;
+  a.tail_off = nvec * E;
+  a.tail_len = n->rank == n->world - 1 ? (long long)count - nvec * E : 0;
+  a.world = n->world;
+  a.esize = es;
+  a.timeout_ns = n->timeout_ns;
+  a.dyn = n->dyn ? 1 : 0;
+  if (dtype == AR_BF16) nvls_kernel<true><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
+  else nvls_kernel<false><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
+  RT_CALL(cudaGetLastError());
+}
+}  // namespace gtar
 
 #define NV_TRY(...)                                         \
   try {                                                     \
@@ -384,29 +442,7 @@ int ar_nvls_bind(ar_nvls *n, void **uc_ptr_out) {
 int allreduce_exec_nvls(ar_nvls *n, uint64_t count, int32_t dtype, void *stream) {
   NV_TRY({
     if (!n || !n->bound) throw InvalidArg("nvls buffer not bound");
-    if (dtype != AR_F32 && dtype != AR_BF16) throw InvalidArg("unknown dtype");
-    const int es = dtype == AR_BF16 ? 2 : 4;
-    if (count * es > n->data_bytes) throw InvalidArg("count exceeds the nvls buffer");
-    if (count % (uint64_t)n->world || (count / n->world) * es % 16)
-      throw InvalidArg("nvls needs count to be a multiple of world * 16 / element size");
-    int cur = -1;
-    RT_CALL(cudaGetDevice(&cur));
-    if (cur != n->device) RT_CALL(cudaSetDevice(n->device));
-    NvArgs a{};
-    a.uc = (char *)n->uc;
-    a.mc = (char *)n->mcva;
-    a.flags_uc = (unsigned long long *)((char *)n->uc + n->data_bytes);
-    a.flags_mc = (unsigned long long *)((char *)n->mcva + n->data_bytes);
-    a.epoch_dev = n->dev_words;
-    a.len = (long long)(count / n->world);
-    a.off = a.len * n->rank;
-    a.world = n->world;
-    a.esize = es;
-    a.timeout_ns = n->timeout_ns;
-    a.dyn = n->dyn ? 1 : 0;
-    if (dtype == AR_BF16) nvls_kernel<true><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
-    else nvls_kernel<false><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
-    RT_CALL(cudaGetLastError());
+    gtar::nvls_launch(n, (const void *)n->uc, count, dtype, stream);
     return AR_OK;
   })
 }

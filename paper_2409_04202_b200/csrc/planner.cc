@@ -454,6 +454,10 @@ Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce
   if (p.n < 2 || p.n > 4096 || p.count < 1) throw InvalidArg("bad n/count");
   const Json *steps = doc.get("steps");
   if (!steps || steps->kind != Json::Array) throw InvalidArg("steps must be an array");
+  if (const Json *sr = doc.get("switch_reduce")) {
+    if (sr->kind != Json::Bool) throw InvalidArg("switch_reduce must be a boolean");
+    p.switch_reduce = sr->b;
+  }
   auto rank_ok = [&](long long r) {
     if (r < 0 || r >= p.n) throw InvalidArg("rank out of range");
     return (int)r;
@@ -500,7 +504,34 @@ Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce
     if (std::string(e.what()).find("hazard") != std::string::npos) throw;
     allreduce = false;
   }
+  if (p.switch_reduce) check_switch_reduce(p);
   return p;
+}
+
+// An NVLS plan is the single-switch CPS data movement: one RS step in which rank b
+// reduces block b from all ranks, then its reversed AllGather.
+void check_switch_reduce(const Plan &p) {
+  const Plan want = build_plan_natural("cps", p.n, p.count);
+  bool ok = p.steps.size() == want.steps.size();
+  for (size_t i = 0; ok && i < p.steps.size(); i++) {
+    const Step &a = p.steps[i], &b = want.steps[i];
+    ok = a.ag == b.ag && a.reduces.size() == b.reduces.size() && a.transfers.size() == b.transfers.size();
+    if (!ok) break;
+    auto key_r = [](const Reduce &r) { return std::make_tuple(r.server, r.block, r.inputs); };
+    auto key_t = [](const Transfer &t) { return std::make_tuple(t.dst, t.block, t.src); };
+    std::vector<std::tuple<int, int, std::vector<int>>> ra, rb;
+    for (auto &r : a.reduces) ra.push_back(key_r(r));
+    for (auto &r : b.reduces) rb.push_back(key_r(r));
+    std::vector<std::tuple<int, int, int>> ta, tb;
+    for (auto &t : a.transfers) ta.push_back(key_t(t));
+    for (auto &t : b.transfers) tb.push_back(key_t(t));
+    std::sort(ra.begin(), ra.end());
+    std::sort(rb.begin(), rb.end());
+    std::sort(ta.begin(), ta.end());
+    std::sort(tb.begin(), tb.end());
+    ok = ra == rb && ta == tb;
+  }
+  if (!ok) throw InvalidArg("a switch_reduce (NVLS) plan must have the single-switch CPS data movement");
 }
 
 // ---------------------------------------------------------------- canonical JSON (O9)
@@ -541,7 +572,9 @@ std::string plan_to_json(const Plan &p, const char *dtype) {
     }
     o += "]}";
   }
-  o += "]}";
+  o += "]";
+  if (p.switch_reduce) o += ",\"switch_reduce\":true";
+  o += "}";
   return o;
 }
 

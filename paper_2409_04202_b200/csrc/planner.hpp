@@ -65,6 +65,10 @@ struct Plan {
   int n = 0;
   int64_t count = 0;
   std::vector<Step> steps;
+  // NVLS plan kind (readings NV1/NV2): CPS's data movement with every
+  // fan-in-N reduce done inside the NVSwitch — the result is the correctly rounded sum, not
+  // a plan-order sum.  Serialised as "switch_reduce": true.
+  bool switch_reduce = false;
 };
 
 int64_t block_size(int64_t count, int n, int b);
@@ -113,6 +117,7 @@ Plan build_plan_natural(const std::string &kind, int n, int64_t count);   // sta
 // verify_allreduce (data-movement probes need not).  Throws InvalidArg.
 Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce);
 void verify_allreduce(const Plan &p);                                      // throws InvalidArg
+void check_switch_reduce(const Plan &p);                                   // NVLS plans: CPS shape
 std::string plan_to_json(const Plan &p, const char *dtype);
 std::string report_to_json(const std::vector<SwitchReport> &r);
 

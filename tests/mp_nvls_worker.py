@@ -65,6 +65,46 @@ def main():
                 if not (ok and same):
                     print(f"rank {rank} FAIL {dtype} {mode} count={count} ok={ok} same={same}", flush=True)
                     failures += 1
+    # NVLS as a GenTree plan kind (gentree_plan_nvls / force "nvls"): allreduce_exec on a
+    # communicator with the NVLS buffer attached, ragged fp32 counts (vectors split evenly over
+    # the ranks, scalar tail on the last rank), checked bit-for-bit against oracle.simulate of
+    # the oracle's NVLS plan (= the correctly rounded sum, reading NV2) on every rank
+    from oracle import gentree as GT
+    from oracle import genmodel as OG
+    from oracle import topology as T
+    doc = T.single_switch_doc(world, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
+                              {"gamma": 0.0, "delta": 4 / 6.54e12})
+    pp = G.params(9.4e-6, 1.465e-12, 0.0, 0.0, 0.0, 4)
+    nvp = G.params(5.7e-6, 0.9e-12, 0.0, 0.0, 0.0, 1)    # NVLS row cheaper: the min-GenModel pick is NVLS
+    comm = G.Comm.create(rank, world, local)
+    comm.attach_nvls(nv)
+    for count in (1, 3, world * 4 + 1, 1000003, (nbytes // 4) - 5):
+        plan = G.Plan.from_topology_nvls(doc, count, "f32", pp, nvp)
+        oplan, _ = GT.gentree_nvls(T.parse_topology(doc), count, 4, OG.Params(9.4e-6, 1.465e-12, 0, 0, 0, 4),
+                                   OG.Params(5.7e-6, 0.9e-12, 0, 0, 0, 1))
+        ok = plan.switch_reduce and oplan.switch_reduce
+        G.fill_synthetic(nv.ptr, count, "f32", seed, rank, 0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        G.allreduce_exec(plan, comm, nv.ptr)
+        torch.cuda.synchronize()
+        comm.async_error()
+        ok = ok and comm.last_kernel() == "nvls_kernel"
+        got = nv.tensor[: count * 4].cpu().numpy().view(np.uint32)
+        if rank in (0, world - 1):
+            xs = GEN.generate_all(seed, world, count, "f32")
+            want = np.concatenate([SM.simulate(type(oplan)(world, min(1 << 21, count - c0), oplan.steps[:0], True),
+                                               [x[c0:c0 + (1 << 21)] for x in xs], "f32")[rank]
+                                   for c0 in range(0, count, 1 << 21)])
+            if not np.array_equal(got, want.view(np.uint32)):
+                ok = False
+                print(f"rank {rank} nvls plan count={count}: {int(np.sum(got != want.view(np.uint32)))} differ", flush=True)
+        allv = [None] * world
+        dist.all_gather_object(allv, got[-4096:].tobytes())
+        if not (ok and all(a == allv[0] for a in allv)):
+            print(f"rank {rank} FAIL nvls plan count={count}", flush=True)
+            failures += 1
+    comm.destroy()
     dist.barrier()
     nv.destroy()
     dist.destroy_process_group()

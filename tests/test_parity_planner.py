@@ -282,3 +282,48 @@ def test_predict_executed_parity(shared):
                     same_breakdown(got, want)
                     checked += 1
     assert checked > 500
+
+
+def test_nvls_plan_kind_parity():
+    """NVLS as a GenTree plan kind (NEXT #1, readings NV1/NV2): force "nvls" and the
+    min-GenModel choice gentree_plan_nvls give byte-identical plan JSON (CPS movement +
+    "switch_reduce") and bit-identical predictions in library and oracle; bf16 and multi-level
+    topologies are refused; the JSON round-trips and a non-CPS switch_reduce plan is refused."""
+    pp = OG.Params(9.4e-6, 1.465e-12, 0.0, 0.0, 0.0, 4)
+    nv_cheap = OG.Params(5.7e-6, 0.9e-12, 0.0, 0.0, 0.0, 1)
+    nv_dear = OG.Params(50e-6, 3e-12, 0.0, 0.0, 0.0, 1)
+    for n in (2, 3, 4, 8):
+        doc = T.single_switch_doc(n, {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9},
+                                  {"gamma": 0.0, "delta": 4 / 6.54e12})
+        t = T.parse_topology(doc)
+        for count in (1, n - 1, 1000003, 1 << 20):
+            lp = G.Plan.from_topology(doc, count, "f32", lib_params(pp), "nvls")
+            op, orep = GT.gentree(t, count, 4, params=pp, force="nvls")
+            assert lp.to_json() == OP.plan_to_json(op, "f32")
+            assert lp.switch_reduce and '"switch_reduce":true' in lp.to_json()
+            assert lp.report()[-1]["chosen"] == "nvls" == orep[-1].chosen
+            same_breakdown(lp.predict_executed(lib_params(nv_cheap)), OG.predict_executed(op, 4, nv_cheap))
+            back = G.Plan.from_json(lp.to_json())
+            assert back.to_json() == lp.to_json() and back.is_allreduce
+            for nvp in (nv_cheap, nv_dear):
+                lg = G.Plan.from_topology_nvls(doc, count, "f32", lib_params(pp), lib_params(nvp))
+                og, _ = GT.gentree_nvls(t, count, 4, pp, nvp)
+                assert lg.to_json() == OP.plan_to_json(og, "f32")
+                lb = G.Plan.from_topology_nvls(doc, count, "bf16", lib_params(pp), lib_params(nvp))
+                assert not lb.switch_reduce        # bf16 never takes NVLS
+        # large messages: the cheap NVLS row ((N+1)/N·0.9 < 2(N-1)/N·1.465 per byte) wins at
+        # every N, the dear one never
+        big = 1 << 26
+        assert G.Plan.from_topology_nvls(doc, big, "f32", lib_params(pp), lib_params(nv_cheap)).switch_reduce
+        assert not G.Plan.from_topology_nvls(doc, big, "f32", lib_params(pp), lib_params(nv_dear)).switch_reduce
+        with pytest.raises(G.ArInvalid):
+            G.Plan.from_topology(doc, 1024, "bf16", lib_params(pp), "nvls")
+        with pytest.raises(G.ArInvalid):
+            G.Plan.from_topology(doc, 1024, "f32", lib_params(pp), "nvls").lowering()
+    two = T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    with pytest.raises(G.ArInvalid):
+        G.Plan.from_topology(two, 1024, "f32", None, "nvls")
+    ring = json.loads(G.Plan.single_switch(4, 1000, "f32", lib_params(pp), "ring").to_json())
+    ring["switch_reduce"] = True
+    with pytest.raises(G.ArInvalid):
+        G.Plan.from_json(json.dumps(ring))

@@ -26,6 +26,7 @@ import json
 import os
 import statistics
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -66,6 +67,12 @@ def doc(world, p=NOMINAL):
                                  "w_t": int(p["w_t"])},
                       "compute": {"gamma": p["gamma"] * 4, "delta": p["delta"] * 4}})
     return json.dumps({"nodes": nodes})
+
+
+def fitted(name):
+    """A GenModel fit committed under profiles/ (tools/fit_report.py --install)."""
+    with open(os.path.join(ROOT, "profiles", name)) as f:
+        return json.load(f)
 
 
 def kinds_for(world, plans):
@@ -191,7 +198,7 @@ def multi(args):
         def refill():
             G.fill_synthetic(view, count, args.dtype, 11, rank, 0)
 
-        plans = ["cps"] if args.mode == "cps" else kinds_for(world, args.plans)
+        plans = ["cps"] if args.mode == "cps" else ([] if args.plans == "none" else kinds_for(world, args.plans))
         for k in plans:
             if k == "nvls":     # in-switch reduction (NEXT #1), its own multicast-bound buffer
                 if nvls_buf[0] is None:
@@ -210,6 +217,32 @@ def multi(args):
                                 "busbw_mean": busbw(nbytes, world, r["t_mean"])})
                 nv.async_error()
                 continue
+            if k == "gentree+nvls":
+                # GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1) under
+                # the committed B200 fits; an NVLS pick runs through allreduce_exec on the
+                # attached multicast buffer, a plan pick on the IPC-registered one
+                fp, fn = fitted("genmodel_params.json"), fitted("genmodel_params_nvls.json")
+                plan = G.Plan.from_topology_nvls(doc(world), count, args.dtype,
+                                                 G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"],
+                                                          fp["epsilon"], int(fp["w_t"])),
+                                                 G.params(alpha=fn["alpha"], beta=fn["beta"]))
+                target, fill_fn = view, refill
+                if plan.switch_reduce:
+                    if nvls_buf[0] is None:
+                        nvls_buf[0] = G.Nvls(max(sizes), local)
+                    nv = nvls_buf[0]
+                    comm.attach_nvls(nv)
+                    target = nv.ptr
+
+                    def fill_fn():
+                        G.fill_synthetic(nv.ptr, count, args.dtype, 11, rank, 0)
+                for mode in modes:
+                    r = timer.run(lambda: G.Executor(plan, comm, target), reps_for(nbytes), fill_fn, mode)
+                    emit(rank, {"mode": args.mode, "impl": "ours", "plan": k, "chosen": plan.report()[-1]["chosen"],
+                                "n": world, "bytes": nbytes, "dtype": args.dtype, "ctas": args.ctas or "auto", **r,
+                                "busbw_med": busbw(nbytes, world, r["t_med"]),
+                                "busbw_mean": busbw(nbytes, world, r["t_mean"])})
+                continue
             plan = G.Plan.from_topology(doc(world), count, args.dtype, None, None if k == "gentree" else k)
             for mode in modes:
                 r = timer.run(lambda: G.Executor(plan, comm, view), reps_for(nbytes), refill, mode)
@@ -221,7 +254,9 @@ def multi(args):
             t = view.view(tdt)
             for mode in modes:
                 r = timer.run(lambda: (lambda: dist.all_reduce(t)), reps_for(nbytes), refill, mode)
-                emit(rank, {"mode": "sweep", "impl": "nccl", "plan": os.environ.get("NCCL_ALGO", "default"),
+                label = os.environ.get("NCCL_ALGO") or ("nvls_off" if os.environ.get("NCCL_NVLS_ENABLE") == "0"
+                                                        else "default")
+                emit(rank, {"mode": "sweep", "impl": "nccl", "plan": label,
                             "n": world, "bytes": nbytes, "dtype": args.dtype, **r,
                             "busbw_med": busbw(nbytes, world, r["t_med"]),
                             "busbw_mean": busbw(nbytes, world, r["t_mean"]),
@@ -232,29 +267,43 @@ def multi(args):
     dist.destroy_process_group()
 
 
-def probe_plan(kind, n, count, dtype, x=None):
-    """Data-movement plans for the P2P probes (C3-ii) in canonical plan JSON.
+def probe_plan(kind, n, x, count, dtype):
+    """Data-movement plans for the C3-ii fan-in tests (reading Q22) in canonical
+    plan JSON: ONE step in which the x ranks 0..x-1 exchange concurrently (the incast pattern:
+    every receiver has x-1 simultaneous senders).  Block b of the `count`-element buffer has
+    the plan's block size (n blocks).
 
-    pull: rank r copies block (r+k) mod n from rank (r+k) mod n, k = 1..n-1 (one step per k)
-    push: rank r copies its block r into rank (r+k) mod n
-    x-to-x (push among ranks 0..x-1 only): every receiver gets one block from each of the
-    x-1 others, i.e. fan-in x (the paper's full-mesh incast test)."""
-    m = x or n
-    steps = []
-    for k in range(1, m):
-        if kind == "pull":
-            red = [{"block": (r + k) % m, "fan_in": 1, "inputs": [(r + k) % m], "server": r} for r in range(m)]
-            steps.append({"label": f"pull{k}", "phase": "rs", "reduces": red, "transfers": []})
-        else:
-            es = 4 if dtype == "f32" else 2
-            size = lambda b: count // n + (1 if b < count % n else 0)
-            tr = [{"block": r, "dst": (r + k) % m, "size": size(r), "src": r} for r in range(m)]
-            steps.append({"label": f"push{k}", "phase": "ag", "reduces": [], "transfers": tr})
-    return json.dumps({"count": count, "dtype": dtype, "n": n, "steps": steps})
+    x-to-x push  : every rank r < x writes its block r into every other rank of the group
+    x-to-x pull  : every rank r < x reduces block r from all x ranks of the group (CPS's RS
+                   step: one op reading the x-1 peers concurrently)
+    x-to-1 push  : ranks 1..x-1 write their block into rank 0
+    x-to-1 pull  : rank 0 reduces block 0 from ranks 0..x-1 (one receiver, x-1 senders)
+    The pull variants are the reduce kernel's access pattern, the push ones the AllGather's."""
+    size = lambda b: count // n + (1 if b < count % n else 0)
+    red, tr = [], []
+    if kind == "push":
+        tr = [{"block": r, "dst": d, "size": size(r), "src": r} for r in range(x) for d in range(x) if d != r]
+        label, phase = f"push{x}to{x}", "ag"
+    elif kind == "pull":
+        red = [{"block": r, "fan_in": x, "inputs": list(range(x)), "server": r} for r in range(x)]
+        label, phase = f"pull{x}to{x}", "rs"
+    elif kind == "push1":
+        tr = [{"block": r, "dst": 0, "size": size(r), "src": r} for r in range(1, x)]
+        label, phase = f"push{x}to1", "ag"
+    elif kind == "pull1":
+        red = [{"block": 0, "fan_in": x, "inputs": list(range(x)), "server": 0}]
+        label, phase = f"pull{x}to1", "rs"
+    else:
+        raise ValueError(kind)
+    return json.dumps({"count": count, "dtype": dtype, "n": n,
+                       "steps": [{"label": label, "phase": phase, "reduces": red, "transfers": tr}]})
 
 
 def p2p(args):
-    """Pull vs push all-to-all bandwidth and the x-to-x fan-in test over NVLink."""
+    """C3-ii: x-to-x full-mesh and x-to-1 fan-in over NVLink, push and pull, for
+    x = 2..N.  Every receiver gets a fixed total of S bytes (--sizes, default the paper's
+    20 M floats = 80 MB) from its x-1 senders; without incast T(x) = α + Sβ is flat in
+    x, a rise beyond w_t is the incast slope ε."""
     import torch.distributed as dist
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
@@ -263,25 +312,113 @@ def p2p(args):
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = G.Comm.create(rank, world, local)
     es = 4 if args.dtype == "f32" else 2
-    sizes = args.sizes or [1 << 26, 1 << 28, 1 << 30]
-    buf = torch.empty(max(sizes), dtype=torch.uint8, device="cuda")
+    sizes = args.sizes or [80_000_000, 1 << 28]
+    # receiver total S = (x-1) blocks of count/world elements -> count = world*S/((x-1)*es)
+    cap = max(world * S // es * es for S in sizes) + 4096
+    buf = torch.empty(cap, dtype=torch.uint8, device="cuda")
     timer = Timer(dist)
-    for nbytes in sizes:
-        count = nbytes // es
-        view = buf[:nbytes]
-        comm.register(view)
-        cases = [("pull", None), ("push", None)] + [("push", x) for x in range(2, world)]
-        for kind, x in cases:
-            plan = G.Plan.from_json(probe_plan(kind, world, count, args.dtype, x))
-            r = timer.run(lambda: G.Executor(plan, comm, view, movement=True), 10, lambda: None, "graph")
-            m = x or world
-            per_dir = (m - 1) * (nbytes // world) / r["t_mean"] / 1e9
-            emit(rank, {"mode": "p2p", "kind": kind if x is None else f"x-to-x push (x={x})", "n": world,
-                        "x": m, "bytes": nbytes, **r, "gbs_per_direction_per_gpu": per_dir})
+    for S in sizes:
+        for x in range(2, world + 1):
+            count = world * S // ((x - 1) * es)
+            view = buf[: count * es]
+            comm.register(view)
+            for kind in ("push", "pull", "push1", "pull1"):
+                if kind in ("push1", "pull1") and x == 2:
+                    continue   # same as x-to-x at x = 2
+                plan = G.Plan.from_json(probe_plan(kind, world, x, count, args.dtype))
+                r = timer.run(lambda: G.Executor(plan, comm, view, movement=True), 20, lambda: None, "graph")
+                recv = (x - 1) * (count // world) * es
+                emit(rank, {"mode": "p2p", "kind": kind, "pattern": {"push": "x-to-x push", "pull": "x-to-x pull",
+                                                                      "push1": "x-to-1 push", "pull1": "x-to-1 pull"}[kind],
+                            "n": world, "x": x, "recv_bytes": recv, **r,
+                            "gbs_per_receiver": recv / r["t_med"] / 1e9})
     comm.async_error()
     dist.barrier()
     comm.destroy()
     dist.destroy_process_group()
+
+
+def nccl_algo(args):
+    """Log the algorithm/protocol NCCL picks for all_reduce at each size (run with
+    NCCL_DEBUG=INFO NCCL_DEBUG_SUBSYS=TUNING NCCL_DEBUG_FILE=...): one call per size."""
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    tdt = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    es = 4 if args.dtype == "f32" else 2
+    for nbytes in args.sizes or SIZES:
+        t = torch.ones(nbytes // es, dtype=tdt, device="cuda")
+        dist.all_reduce(t)
+        torch.cuda.synchronize()
+        emit(rank, {"mode": "nccl-algo", "bytes": nbytes, "dtype": args.dtype,
+                    "NCCL_ALGO": os.environ.get("NCCL_ALGO", "unset"),
+                    "NCCL_NVLS_ENABLE": os.environ.get("NCCL_NVLS_ENABLE", "unset")})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def fanin_ag(args):
+    """C3-iv ("concurrent memory traffic"): the Eq. 6 local fan-in reduce of k
+    vectors on GPU 0, alone and while GPU 1 streams an AllGather-like copy into
+    GPU 0's HBM over NVLink (copy engine, peer writes), to test whether the memory term stays
+    additive (the model sums the terms of a step).  One process, two GPUs."""
+    import torch.cuda as tc
+    assert tc.device_count() >= 2, "needs 2 GPUs"
+    count = args.count
+    es = 4 if args.dtype == "f32" else 2
+    torch.cuda.set_device(0)
+    bufs = [torch.empty(count * es, dtype=torch.uint8, device="cuda:0") for _ in range(args.kmax + 1)]
+    for i, b in enumerate(bufs):
+        G.fill_synthetic(b, count, args.dtype, 7, i, 0)
+    land = torch.empty(1 << 30, dtype=torch.uint8, device="cuda:0")          # AG destination on GPU 0
+    src = torch.empty(1 << 30, dtype=torch.uint8, device="cuda:1")
+    src.fill_(1)
+    s1 = torch.cuda.Stream(device="cuda:1")
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+
+    def time_reduce(k, reps=20):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+        ev[0].record()
+        for i in range(reps):
+            G.local_reduce(bufs[:k], bufs[-1], count, args.dtype)
+            ev[i + 1].record()
+        torch.cuda.synchronize(0)
+        ts = [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(reps)]
+        return statistics.median(ts), statistics.mean(ts)
+
+    def ag_rate(ncopies):
+        with torch.cuda.stream(s1):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s1)
+            for _ in range(ncopies):
+                land.copy_(src, non_blocking=True)
+            e1.record(s1)
+        return e0, e1
+
+    for _ in range(3):
+        G.local_reduce(bufs[:2], bufs[-1], count, args.dtype)
+    e0, e1 = ag_rate(4)
+    torch.cuda.synchronize(1)
+    ag_alone = 4 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9
+    for k in range(2, args.kmax + 1):
+        t_alone, m_alone = time_reduce(k)
+        reps = 20
+        # enough AG traffic queued to cover the whole timed region
+        ncopies = int(reps * t_alone * ag_alone * 1e9 / (1 << 30)) + 6
+        e0, e1 = ag_rate(ncopies)
+        time.sleep(0.002)
+        t_conc, m_conc = time_reduce(k, reps)
+        torch.cuda.synchronize(1)
+        ag_gbs = ncopies * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9
+        emit(0, {"mode": "fanin-ag", "k": k, "count": count, "dtype": args.dtype,
+                 "t_med_alone": t_alone, "t_med_with_ag": t_conc, "t_mean_alone": m_alone, "t_mean_with_ag": m_conc,
+                 "hbm_bytes": (k + 1) * count * es,
+                 "hbm_gbs_alone": (k + 1) * count * es / t_alone / 1e9,
+                 "hbm_gbs_with_ag": (k + 1) * count * es / t_conc / 1e9,
+                 "ag_gbs_alone": ag_alone, "ag_gbs_during": ag_gbs})
 
 
 def mtrace(args):
@@ -452,7 +589,8 @@ def fanin(args):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "p2p", "mtrace", "hybrid"])
+    ap.add_argument("mode", choices=["sweep", "cps", "emu-sweep", "emu-cps", "fanin", "fanin-ag", "p2p", "mtrace",
+                                     "hybrid", "nccl-algo"])
     ap.add_argument("--dtype", default="f32")
     ap.add_argument("--plans", default="gentree;cps;ring;rhd;rb;hcps:2,2;hcps:4,2;hcps:2,4;hcps:2,2,2",
                     help="';'-separated plan kinds")
@@ -476,5 +614,9 @@ if __name__ == "__main__":
         p2p(a)
     elif a.mode == "fanin":
         fanin(a)
+    elif a.mode == "fanin-ag":
+        fanin_ag(a)
+    elif a.mode == "nccl-algo":
+        nccl_algo(a)
     else:
         emu(a)
