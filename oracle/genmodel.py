@@ -213,7 +213,10 @@ def closed_form_terms(kind: str, c: int, S: int, w_t: int, fanins: tuple = ()):
         # reduce (C = D = 0) and no unicast many-to-one flows (I = 0).
         return 2, (c + 1) * S, 0, 0, 0, c
     if kind == "oneshot":
-        # DESIGN.md reading OS1 (the executor's small-message path): one round; every rank
+        # NOT a paper row: a measured-protocol row of this executor (reading OS1),
+        # kept here only so the library's evaluation of it has a checked counterpart.  Its B
+        # counts the executor's own wire format (16-byte lines carrying 8 payload bytes), so it
+        # describes the kernel, not the method; nothing in the paper pins it.  One round; every rank
         # sends its whole input to each of the N-1 others as 16-byte lines carrying 8 payload
         # bytes (B = 2(N-1)S per direction), then reduces all N blocks itself in plan order
         # (C = (N-1)S, D = (N+1)S); every rank receives from N-1 senders (w = N, as CPS).

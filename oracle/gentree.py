@@ -24,6 +24,7 @@ steps start after all its children's.  The AllGather is the RS reversed 
 from __future__ import annotations
 
 import math
+from fractions import Fraction
 from dataclasses import dataclass, field
 
 from .genmodel import (Params, StepCoeffs, StepParams, closed_form_f64,
@@ -205,8 +206,9 @@ def gentree(topo, count: int, esize: int, params: Params | None = None,
             ni = len(ch_servers)
             if ni < 2:
                 continue
-            ratio = topo.convergence_ratio_f64(nid, ch)
-            k = math.ceil((float(ni) / ratio) * (1.0 - 2.0 ** -40))
+            # subset = the lowest-indexed ceil(n_i / r) servers (reading Q15), exact rationals
+            ratio = topo.convergence_ratio(nid, ch)
+            k = math.ceil(Fraction(ni) / ratio)
             k = max(1, min(ni, k))
             if k >= ni:
                 continue

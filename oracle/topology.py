@@ -11,6 +11,8 @@ pre-order with children in document order (reading R1).
 """
 from __future__ import annotations
 
+from fractions import Fraction
+
 import json
 from dataclasses import dataclass, field
 
@@ -79,6 +81,15 @@ class Topology:
         sa = set(up_a)
         lca = next(x for x in up_b if x in sa)
         return up_a[:up_a.index(lca)] + up_b[:up_b.index(lca)]
+
+    def convergence_ratio(self, switch: str, child: str) -> Fraction:
+        """P:626 "the total bandwidth of A to its children divided by that of C_i" (S:62-70),
+        exactly: r = β_i · Σ_k 1/β_k over A's children, as a rational of the given floats."""
+        sw = self.nodes[switch]
+        if child not in sw.children:
+            raise TopologyError(f"{child!r} is not a child of {switch!r}")
+        inv = sum(Fraction(1) / Fraction(self.nodes[c].uplink["beta"]) for c in sw.children)
+        return Fraction(self.nodes[child].uplink["beta"]) * inv
 
     def convergence_ratio_f64(self, switch: str, child: str) -> float:
         """P:626 "the total bandwidth of A to its children divided by that of C_i"; S:62-70.

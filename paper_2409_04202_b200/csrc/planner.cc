@@ -163,6 +163,96 @@ std::vector<int> Topology::path_links(int a, int b) const {
   return out;
 }
 
+// ---- exact rearrangement subset size (reading Q15): the smallest m >= 1 with
+// m * r >= n_i, r = beta_i * sum_k 1/beta_k, decided exactly.  Every beta is a double
+// M * 2^E (M a 53-bit integer); multiplying m * sum_k M_i 2^(E_i - E_k) / M_k >= n_i through by
+// prod_j M_j * 2^t leaves integers only, compared with a small unsigned big-integer type.
+namespace {
+struct BigU {
+  std::vector<uint64_t> d;   // little-endian 64-bit limbs
+  explicit BigU(uint64_t v = 0) { d.push_back(v); }
+  void trim() { while (d.size() > 1 && d.back() == 0) d.pop_back(); }
+  void mul(uint64_t m) {
+    unsigned __int128 carry = 0;
+    for (auto &x : d) {
+      unsigned __int128 p = (unsigned __int128)x * m + carry;
+      x = (uint64_t)p;
+      carry = p >> 64;
+    }
+    if (carry) d.push_back((uint64_t)carry);
+    trim();
+  }
+  void shl(int bits) {
+    const int w = bits / 64, b = bits % 64;
+    if (b) {
+      uint64_t carry = 0;
+      for (auto &x : d) {
+        const uint64_t nx = (x << b) | carry;
+        carry = x >> (64 - b);
+        x = nx;
+      }
+      if (carry) d.push_back(carry);
+    }
+    d.insert(d.begin(), (size_t)w, 0ull);
+    trim();
+  }
+  void add(const BigU &o) {
+    if (o.d.size() > d.size()) d.resize(o.d.size(), 0);
+    unsigned __int128 carry = 0;
+    for (size_t i = 0; i < d.size(); i++) {
+      unsigned __int128 s = (unsigned __int128)d[i] + (i < o.d.size() ? o.d[i] : 0) + carry;
+      d[i] = (uint64_t)s;
+      carry = s >> 64;
+    }
+    if (carry) d.push_back((uint64_t)carry);
+  }
+  int cmp(const BigU &o) const {
+    if (d.size() != o.d.size()) return d.size() < o.d.size() ? -1 : 1;
+    for (size_t i = d.size(); i-- > 0;)
+      if (d[i] != o.d[i]) return d[i] < o.d[i] ? -1 : 1;
+    return 0;
+  }
+};
+void split_double(double b, uint64_t &m, int &e) {
+  int ex = 0;
+  const double f = std::frexp(b, &ex);   // b = f * 2^ex, 0.5 <= f < 1
+  m = (uint64_t)std::ldexp(f, 53);       // exact: a double has 53 significant bits
+  e = ex - 53;
+}
+}  // namespace
+
+int Topology::rearrangement_subset_size(int sw, int child, int ni) const {
+  const auto &ch = nodes[sw].children;
+  const int K = (int)ch.size();
+  std::vector<uint64_t> M(K);
+  std::vector<int> E(K);
+  for (int k = 0; k < K; k++) split_double(nodes[ch[k]].up.beta, M[k], E[k]);
+  uint64_t Mi;
+  int Ei;
+  split_double(nodes[child].up.beta, Mi, Ei);
+  int smin = 0;
+  for (int k = 0; k < K; k++) smin = std::min(smin, Ei - E[k]);
+  const int tsh = -smin;   // >= 0: every 2^(s_k + t) is an integer power
+  // S = sum_k M_i * prod_{j != k} M_j * 2^(E_i - E_k + t);  R = n_i * prod_j M_j * 2^t
+  BigU S(0);
+  for (int k = 0; k < K; k++) {
+    BigU term(Mi);
+    for (int j = 0; j < K; j++)
+      if (j != k) term.mul(M[j]);
+    term.shl(Ei - E[k] + tsh);
+    S.add(term);
+  }
+  BigU R((uint64_t)ni);
+  for (int j = 0; j < K; j++) R.mul(M[j]);
+  R.shl(tsh);
+  for (int m = 1; m <= ni; m++) {
+    BigU lhs = S;
+    lhs.mul((uint64_t)m);
+    if (lhs.cmp(R) >= 0) return m;
+  }
+  return ni;
+}
+
 double Topology::convergence_ratio_f64(int sw, int child) const {
   double acc = 0.0;
   for (int c : nodes[sw].children) acc = acc + 1.0 / nodes[c].up.beta;
@@ -979,8 +1069,7 @@ PlanResult gentree(const Topology &t, int64_t count, int esize, const Params *ex
       t.servers_under(ch, chs);
       const int ni = (int)chs.size();
       if (ni < 2) continue;
-      double ratio = t.convergence_ratio_f64(nid, ch);
-      int k = (int)std::ceil(((double)ni / ratio) * (1.0 - std::ldexp(1.0, -40)));
+      int k = t.rearrangement_subset_size(nid, ch, ni);   // ceil(n_i / r), exact (Q15)
       k = std::max(1, std::min(ni, k));
       if (k >= ni) continue;
       std::vector<int> subset(chs.begin(), chs.begin() + k);

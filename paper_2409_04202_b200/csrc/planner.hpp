@@ -43,6 +43,7 @@ struct Topology {
   void subtree(int n, std::vector<int> &out) const;
   std::vector<int> path_links(int a, int b) const;          // node indices
   double convergence_ratio_f64(int sw, int child) const;
+  int rearrangement_subset_size(int sw, int child, int ni) const;   // exact ceil(n_i / r), reading Q15
 };
 Topology parse_topology(const std::string &text);           // throws InvalidArg
 

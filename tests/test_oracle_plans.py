@@ -70,6 +70,19 @@ def test_convergence_ratio(spec_examples):
         nd["uplink"]["beta"] = b
     t = T.parse_topology(json.dumps(d))
     assert t.convergence_ratio_f64("sw", "s2") == pytest.approx(5, rel=1e-15)
+    # exact rationals (reading Q15): 2e-9 is exactly 2 x 1e-9 in binary, so r = 2e-9 *
+    # (2/1e-9 + 1/2e-9) = 5 exactly, and equal uplinks give r = the child count exactly
+    from fractions import Fraction
+    assert t.convergence_ratio("sw", "s2") == 5
+    assert t.convergence_ratio("sw", "s0") == Fraction(5, 2)
+    t4 = T.parse_topology(T.single_switch_doc(4, T.TABLE5["middle_sw"], T.TABLE5["server"]))
+    assert t4.convergence_ratio("sw", "s2") == 4
+    # 6.4e-9 is not exactly 10 x 6.4e-10 in binary: the exact ratio differs from 10
+    d2 = json.loads(T.single_switch_doc(2, T.TABLE5["middle_sw"], T.TABLE5["server"]))
+    d2["nodes"][1]["uplink"]["beta"], d2["nodes"][2]["uplink"]["beta"] = 6.4e-10, 6.4e-9
+    r = T.parse_topology(json.dumps(d2)).convergence_ratio("sw", "s1")
+    assert r == Fraction(6.4e-9) * (Fraction(1) / Fraction(6.4e-10) + Fraction(1) / Fraction(6.4e-9))
+    assert r != 11
 
 
 # ------------------------------------------------------------------ blocks

@@ -263,3 +263,29 @@ def test_avg_simulate_at_matches_simulate():
     part = SM.simulate_at(plan, idx, [x[idx] for x in xs], "bf16", op="avg")
     for r in range(n):
         assert np.array_equal(part[r], full[r][idx])
+
+
+def test_exact_sum_and_normwise_error_pins():
+    """Pins for the accuracy reference (reading Q21), independent of the simulator:
+    exact_sum_f64 equals the exact rational sum whenever float64 holds it (fp32 inputs whose
+    exponents span < 53 - 24 - log2 N bits: every partial sum exact), checked with Fraction;
+    normwise_rel_err on hand values: y = ref·(1 + d) gives |d|; an error orthogonal to ref
+    gives ||e|| / ||ref|| (3-4-5 triangle); bf16 bits are widened before the norm; a zero
+    reference reports ||y||."""
+    from fractions import Fraction
+    rng = np.random.default_rng(11)
+    xs = [(rng.integers(-2 ** 23, 2 ** 23, 1000) * 2.0 ** rng.integers(-30, -20)).astype(np.float32)
+          for _ in range(8)]
+    got = SM.exact_sum_f64(xs, "f32")
+    for i in range(0, 1000, 37):
+        assert Fraction(float(got[i])) == sum(Fraction(float(x[i])) for x in xs)
+    ref = np.array([1.0, -2.0, 4.0, 0.5])
+    for d in (1e-3, -2.5e-7):
+        y = (ref * (1 + d)).astype(np.float32)
+        assert SM.normwise_rel_err(y, ref, "f32") == pytest.approx(abs(d), abs=2 ** -23)   # y rounded to fp32
+    assert SM.normwise_rel_err(np.array([3.0, 4.0 + 1.0], np.float32), np.array([3.0, 4.0]), "f32") == pytest.approx(0.2)
+    assert SM.normwise_rel_err(np.array([3.0, 4.0], np.float32), np.array([3.0, 4.0]), "f32") == 0.0
+    bits = np.array([0x3F80, 0x4000], dtype=np.uint16)          # bf16 1.0, 2.0
+    assert SM.normwise_rel_err(bits, np.array([1.0, 2.0]), "bf16") == 0.0
+    assert SM.normwise_rel_err(bits, np.array([1.0, 1.0]), "bf16") == pytest.approx(1 / np.sqrt(2))
+    assert SM.normwise_rel_err(np.array([3.0, 4.0], np.float32), np.zeros(2), "f32") == 5.0
