@@ -186,13 +186,41 @@ def oracle_sample_time(world, dtype, count, force, p):
     return time.perf_counter() - t0
 
 
+def host_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count()}
+
+
+def pinned_one_core(fn):
+    """Run fn() with this process pinned to one core (the oracle's numpy adds are serial;
+    pinning makes `cores: 1` a fact, not an assumption), then restore the affinity."""
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        return fn(), core
+    finally:
+        os.sched_setaffinity(0, old)
+
+
 def cpu_baseline(world, dtype, sample_mib, force, p):
     es = 2 if dtype == "bf16" else 4
     count = int(sample_mib * MIB) // es
-    secs = oracle_sample_time(world, dtype, count, force, p)
+    secs, core = pinned_one_core(lambda: oracle_sample_time(world, dtype, count, force, p))
     return {"value": round(busbw(count * es, world, secs), 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "pinned_core": core, **host_info(),
             "sample": f"{world} ranks x {count} {dtype} elements ({sample_mib:g} MiB/rank), same plan kind, "
-                      f"numpy single-threaded step-by-step simulation; {secs:.2f} s per AllReduce"}
+                      f"numpy single-threaded step-by-step simulation pinned to one core; {secs:.2f} s per "
+                      f"AllReduce (the full 256 MiB workload and the C1/C2/C4 plan: "
+                      f"profiles/round2/cpu_oracle_timing.jsonl)"}
 
 
 def arm_config(args, n, world, chosen, p_src):
@@ -225,9 +253,11 @@ def run_reference(args):
     _, reps = GT.gentree(T.parse_topology(single_switch_doc(world, p)), args.mib * MIB // es, es, params=op,
                          force=args.force)
     chosen = reps[-1].chosen
-    for _ in range(min(args.warmup, 1)):
-        oracle_sample_time(world, args.dtype, count, args.force, p)
-    times = [oracle_sample_time(world, args.dtype, count, args.force, p) for _ in range(max(1, min(args.steps, 3)))]
+    def run():
+        for _ in range(min(args.warmup, 1)):
+            oracle_sample_time(world, args.dtype, count, args.force, p)
+        return [oracle_sample_time(world, args.dtype, count, args.force, p) for _ in range(max(1, min(args.steps, 3)))]
+    times, core = pinned_one_core(run)
     t = sum(times) / len(times)
     v = busbw(count * es, world, t)
     line = {"impl": "reference", "metric": "allreduce_busbw", "value": round(v, 4), "unit": "GB/s",
@@ -235,7 +265,11 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic",
             "config": arm_config(args, n, world, chosen, p_src),
+            "note": (f"the reference arm is the CPU oracle (no reference implementation exists); it runs "
+                     f"{len(times)} timed steps after {min(args.warmup, 1)} warm-up on a bounded sample so the "
+                     f"run ends in minutes — steps/warmup deliberately differ from the GPU arm's"),
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                             "pinned_core": core, **host_info(),
                              "sample": f"each step: the oracle's step-by-step simulation of the same plan on a "
                                        f"bounded sample, {world} ranks x {count} {args.dtype} elements "
                                        f"({args.cpu_sample_mib:g} MiB/rank), numpy single-threaded"},
@@ -273,10 +307,14 @@ def main():
     plan = G.Plan.from_topology(single_switch_doc(world, p), count, args.dtype, None, args.force)
     chosen = plan.report()[-1]["chosen"]
     # a6: GenModel prediction of the executed plan with the B200 fit of this machine kind
+    # (N = 1: all ranks share one GPU's HBM — reading A6e, genmodel_predict_executed_shared;
+    # N > 1: reading A6x).  Both fits use CPS rows only and never the bench's own point (the
+    # emulated fit uses 2..7 ranks, the NVLink fit leaves out the 256 MiB rows), so the
+    # prediction below is held out; the fit's validation summary is carried into the line.
     fp = fitted_params(emulated=n == 1) or NOMINAL
     pred_src = ("fitted " + fp["source"]) if "source" in fp else "nominal"
     gp = G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"], fp["epsilon"], int(fp["w_t"]))
-    pred = plan.predict_executed(gp)["total"]
+    pred = (plan.predict_executed_shared(gp) if n == 1 else plan.predict_executed(gp))["total"]
     seed = 0x240904202 ^ 4
     stream = torch.cuda.current_stream()
 
@@ -483,7 +521,10 @@ def main():
         "clocks": clk,
         "genmodel": {"predicted_ms": round(pred * 1e3, 4), "measured_ms": round(t_step * 1e3, 4),
                      "pred_err": round(abs(pred - t_step) / t_step, 4), "params": pred_src,
-                     "model": "per-step GenModel of the executed (fused, full-duplex) steps"},
+                     "bench_point_in_fit": False,
+                     "model": ("GenModel of the executed steps, all ranks sharing one HBM (reading A6e)" if n == 1
+                               else "GenModel of the executed (fused, full-duplex) steps (reading A6x)"),
+                     "validation_held_out": fp.get("validation")},
         "busbw_per_step_min_median_max": [round(busbw(nbytes, world, max(per_step)), 2),
                                           round(busbw(nbytes, world, statistics.median(per_step)), 2),
                                           round(busbw(nbytes, world, min(per_step)), 2)],

@@ -1,15 +1,27 @@
 #!/usr/bin/env python
-"""Fit GenModel on B200 measurements and report its prediction error.
+"""Fit GenModel on B200 measurements and report its prediction error on HELD-OUT rows
+(the paper fits from CPS benchmarks and predicts other plans, P:530-532,
+P:776).
 
-    python tools/fit_report.py --cps cps.jsonl --val val_*.jsonl --tag nvlink [--timing graph]
+    python tools/fit_report.py --cps cps_*.jsonl --val val_*.jsonl --tag nvlink \
+        [--holdout-bytes 268435456] [--install]
+    python tools/fit_report.py --shared --cps cps_emu.jsonl --val val_emu8.jsonl --tag emulated \
+        [--holdout-n 8] [--install]
 
-1. §3.4: fit (α, k = 2β+γ, δ, ε, w_t) from the Co-located-PS rows (n ranks,
-   bytes per rank, mean time) with the library's `genmodel_fit` (C-ABI; NNLS per w_t).
-2. The (α,β,γ) model the paper compares against: the same rows fitted with δ = ε = 0.
-3. Every validation row (plan kind, n, bytes, measured mean time) is predicted by
-   `genmodel_predict` on the plan the library builds for it; error = |pred − meas| / meas
-   (the paper's definition, reproducing its 2.6 % and 19.8 %).
-Writes profiles/genmodel_fit_<tag>.json (+ genmodel_params.json when --install).
+NVLink ranks (one per GPU): §3.4's fit — (α, k = 2β+γ, δ, ε, w_t) by the library's
+`genmodel_fit` (NNLS per w_t) on the CPS rows — minus the held-out rows (--holdout-bytes: the
+bench.py size is never fitted); prediction = `genmodel_predict_executed` (reading A6x, bit-
+identical to oracle.genmodel.predict_executed) of the plan the library builds for the row.
+Also reported: the (α,β,γ) model fitted on the same rows (P:876's comparison) and GenModel on
+the paper's unfused step structure (`genmodel_predict`).
+
+Emulated ranks (all on one GPU, --shared; reading A6e): T = A·α + C·γ + D·δ with the shared
+coefficients (every rank's memory traffic through one HBM), (α, γ, δ) by NNLS on the CPS rows
+of rank counts below --holdout-n; prediction = `genmodel_predict_executed_shared`.
+
+Every validation row is a plan/size the fit never saw.  Error = |pred − meas| / meas (the
+paper's definition).  Writes profiles/genmodel_fit_<tag>.json (+ the params file bench.py
+reads with --install).
 """
 from __future__ import annotations
 
@@ -34,15 +46,96 @@ def load(paths, timing):
         for line in open(p):
             if line.startswith("{"):
                 r = json.loads(line)
-                if r.get("timing", timing) == timing and r.get("impl") == "ours":
+                if r.get("timing", timing) == timing and r.get("impl", "ours") == "ours":
                     rows.append(r)
     return rows
 
 
-def predict(kind, n, nbytes, dtype, p):
-    es = 4 if dtype == "f32" else 2
-    plan = G.Plan.from_topology(doc(n), nbytes // es, dtype, p, None if kind == "gentree" else kind)
-    return plan.predict(p)["total"], plan.predict_executed(p)["total"], plan.report()[-1]["chosen"]
+_plans = {}
+
+
+def plan_for(kind, n, nbytes, dtype):
+    key = (kind, n, nbytes, dtype)
+    if key not in _plans:
+        es = 4 if dtype == "f32" else 2
+        _plans[key] = G.Plan.from_topology(doc(n), nbytes // es, dtype, None, None if kind == "gentree" else kind)
+    return _plans[key]
+
+
+def summarize(out_rows, key):
+    es = [x[key] for x in out_rows]
+    by = {}
+    for x in out_rows:
+        by.setdefault(x["plan"], []).append(x[key])
+    return {"median": statistics.median(es) if es else None, "max": max(es) if es else None,
+            "by_plan_max": {k: max(v) for k, v in sorted(by.items())},
+            "by_plan_median": {k: statistics.median(v) for k, v in sorted(by.items())}}
+
+
+def fit_nvlink(a, cps, val):
+    hold = set(a.holdout_bytes or [])
+    rows = [(r["n"], r["bytes"], r["t_mean"]) for r in cps if r["bytes"] >= a.min_bytes and r["bytes"] not in hold]
+    nmax = max(n for n, _, _ in rows)
+    wt_lo = a.wt_min or 2
+    wt_hi = max(wt_lo, a.wt_max or max(2, nmax))
+    fit, sse = G.genmodel_fit(rows, wt_lo, wt_hi)
+    A = np.array([[2.0, (n - 1) * s / n] for n, s, _ in rows])
+    t = np.array([x for _, _, x in rows])
+    (alpha3, k3), *_ = np.linalg.lstsq(A, t, rcond=None)
+    abc = G.params(max(alpha3, 0.0), 0.0, 0.0, 0.0, 0.0, 1 << 20, combined=max(k3, 0.0))
+    out_rows = []
+    fit_keys = {(n, s) for n, s, _ in rows}
+    for r in val:
+        if r["bytes"] < a.min_bytes:
+            continue
+        plan = plan_for(r["plan"], r["n"], r["bytes"], r["dtype"])
+        pg = plan.predict_executed(fit)["total"]
+        pa = plan.predict_executed(abc)["total"]
+        ps = plan.predict(fit)["total"]
+        m = r["t_mean"]
+        in_fit = r["plan"] in ("cps", "gentree") and (r["n"], r["bytes"]) in fit_keys
+        out_rows.append({"plan": r["plan"], "executed": plan.report()[-1]["chosen"], "n": r["n"], "bytes": r["bytes"],
+                         "dtype": r["dtype"], "measured_s": m, "genmodel_s": pg, "abc_s": pa,
+                         "genmodel_paper_steps_s": ps, "cps_point_in_fit": in_fit,
+                         "err_genmodel": abs(pg - m) / m, "err_abc": abs(pa - m) / m,
+                         "err_genmodel_paper_steps": abs(ps - m) / m})
+    p = fit.as_dict()
+    params = {"alpha": p["alpha"], "beta": p["combined"] / 2 if p["has_combined"] else p["beta"],
+              "gamma": 0.0 if p["has_combined"] else p["gamma"], "delta": p["delta"], "epsilon": p["epsilon"],
+              "w_t": p["w_t"], "n_max_fit": nmax}
+    return params, {"fit_rows": len(rows), "params_per_byte": p, "fit_sse": sse,
+                    "abc_params": {"alpha": abc.alpha, "combined": abc.combined},
+                    "held_out_bytes": sorted(hold)}, out_rows
+
+
+def fit_shared(a, cps, val):
+    from scipy.optimize import nnls
+    rows = [r for r in cps if r["bytes"] >= a.min_bytes and r["n"] < a.holdout_n]
+    X, t = [], []
+    for r in rows:
+        plan = plan_for("cps", r["n"], r["bytes"], r["dtype"])
+        # the shared coefficients' A, C, D: read back through unit parameters (bit-exact
+        # per-step sums of the library's A6e evaluation)
+        ua = plan.predict_executed_shared(G.params(1.0, 0, 0, 0, 0, 1))["latency"]
+        uc = plan.predict_executed_shared(G.params(0, 0, 1.0, 0, 0, 1))["compute"]
+        ud = plan.predict_executed_shared(G.params(0, 0, 0, 1.0, 0, 1))["memory"]
+        X.append([ua, uc, ud])
+        t.append(r["t_mean"])
+    x, res = nnls(np.array(X), np.array(t))
+    gp = G.params(x[0], 0.0, x[1], x[2], 0.0, 1 << 20)
+    out_rows = []
+    for r in val:
+        if r["bytes"] < a.min_bytes:
+            continue
+        plan = plan_for(r["plan"], r["n"], r["bytes"], r["dtype"])
+        pg = plan.predict_executed_shared(gp)["total"]
+        m = r["t_mean"]
+        out_rows.append({"plan": r["plan"], "executed": plan.report()[-1]["chosen"], "n": r["n"], "bytes": r["bytes"],
+                         "dtype": r["dtype"], "measured_s": m, "genmodel_s": pg, "err_genmodel": abs(pg - m) / m})
+    params = {"alpha": x[0], "beta": 0.0, "gamma": x[1], "delta": x[2], "epsilon": 0.0, "w_t": 1 << 20,
+              "model": "shared (reading A6e)", "n_fit": sorted({r["n"] for r in rows})}
+    return params, {"fit_rows": len(rows), "params_per_byte": params, "fit_residual": res,
+                    "held_out_n": a.holdout_n}, out_rows
 
 
 def main():
@@ -52,9 +145,11 @@ def main():
     ap.add_argument("--tag", required=True)
     ap.add_argument("--timing", default="graph")
     ap.add_argument("--min-bytes", type=int, default=1 << 20)
-    ap.add_argument("--install", action="store_true", help="write profiles/genmodel_params.json")
+    ap.add_argument("--install", action="store_true", help="write the params file bench.py reads")
     ap.add_argument("--fanin", default=None, help="harness fanin JSONL (C3-i, Eq. 6)")
-    ap.add_argument("--emulated", action="store_true", help="install as the emulated-ranks fit")
+    ap.add_argument("--shared", action="store_true", help="emulated ranks on one GPU (reading A6e)")
+    ap.add_argument("--holdout-n", type=int, default=8, help="--shared: fit on rank counts below this")
+    ap.add_argument("--holdout-bytes", type=int, nargs="*", default=None, help="CPS sizes never fitted")
     ap.add_argument("--wt-min", type=int, default=0, help="incast threshold lower bound (x-to-x probe)")
     ap.add_argument("--wt-max", type=int, default=0)
     a = ap.parse_args()
@@ -71,63 +166,31 @@ def main():
                "points": [{"x": int(x), "t_per_add_s": float(y)} for x, y in zip(xs, ys)],
                "strictly_decreasing": bool(np.all(np.diff(ys) < 0))}
     cps = [r for r in load(a.cps, a.timing) if r["plan"] == "cps"]
-    # rows at or below the one-shot cut-off (1.5 MiB/(N-1)) run ar_ll_kernel, whose step
-    # structure GenModel's executed-plan view does not describe: --min-bytes excludes them
-    rows = [(r["n"], r["bytes"], r["t_mean"]) for r in cps if r["bytes"] >= a.min_bytes]
-    nmax = max(n for n, _, _ in rows)
-    # w_t: from the x-to-x fan-in test when given ("no incast for 2 <= x <= w_t"),
-    # else scanned by the fit
-    wt_lo = a.wt_min or 2
-    wt_hi = max(wt_lo, a.wt_max or max(2, nmax))
-    fit, sse = G.genmodel_fit(rows, wt_lo, wt_hi)
-    # (alpha, beta, gamma) model: least squares on [2, (n-1)s/n] only (delta = eps = 0)
-    A = np.array([[2.0, (n - 1) * s / n] for n, s, _ in rows])
-    t = np.array([x for _, _, x in rows])
-    (alpha3, k3), *_ = np.linalg.lstsq(A, t, rcond=None)
-    abc = G.params(max(alpha3, 0.0), 0.0, 0.0, 0.0, 0.0, 1 << 20, combined=max(k3, 0.0))
-    val = [r for r in load(a.val, a.timing) if r["bytes"] >= a.min_bytes]
-    out_rows = []
-    for r in val:
-        pseq, pg, chosen = predict(r["plan"], r["n"], r["bytes"], r["dtype"], fit)
-        _, pa, _ = predict(r["plan"], r["n"], r["bytes"], r["dtype"], abc)
-        out_rows.append({"plan": r["plan"], "executed": r.get("chosen", r["plan"]), "n": r["n"],
-                         "bytes": r["bytes"], "measured_s": r["t_mean"], "genmodel_s": pg, "abc_s": pa,
-                         "genmodel_paper_steps_s": pseq,
-                         "err_genmodel": abs(pg - r["t_mean"]) / r["t_mean"],
-                         "err_abc": abs(pa - r["t_mean"]) / r["t_mean"],
-                         "err_genmodel_paper_steps": abs(pseq - r["t_mean"]) / r["t_mean"]})
-    eg = [x["err_genmodel"] for x in out_rows]
-    ea = [x["err_abc"] for x in out_rows]
-    es_ = [x["err_genmodel_paper_steps"] for x in out_rows]
-    by_plan = {}
-    for x in out_rows:
-        by_plan.setdefault(x["plan"], []).append(x["err_genmodel"])
-    summary = {
-        "tag": a.tag, "timing": a.timing, "fit_rows": len(rows), "validation_rows": len(out_rows),
-        "params_per_byte": fit.as_dict(), "fit_sse": sse,
-        "abc_params": {"alpha": abc.alpha, "combined": abc.combined},
-        "genmodel_err": {"median": statistics.median(eg) if eg else None, "max": max(eg) if eg else None},
-        "abc_err": {"median": statistics.median(ea) if ea else None, "max": max(ea) if ea else None},
-        "genmodel_paper_steps_err": {"median": statistics.median(es_) if es_ else None,
-                                     "max": max(es_) if es_ else None},
-        "genmodel_err_by_plan_max": {k: max(v) for k, v in by_plan.items()},
-        "eq6_local_fanin": eq6,
-        "rows": out_rows,
-    }
+    val = load(a.val, a.timing)
+    if a.shared:
+        params, info, out_rows = fit_shared(a, cps, val)
+    else:
+        params, info, out_rows = fit_nvlink(a, cps, val)
+    held = [x for x in out_rows if not x.get("cps_point_in_fit")]
+    summary = {"tag": a.tag, "timing": a.timing, "model": "shared" if a.shared else "executed", **info,
+               "validation_rows": len(held),
+               "genmodel_err": summarize(held, "err_genmodel"),
+               "eq6_local_fanin": eq6, "rows": out_rows}
+    if not a.shared:
+        summary["abc_err"] = summarize(held, "err_abc")
+        summary["genmodel_paper_steps_err"] = summarize(held, "err_genmodel_paper_steps")
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"genmodel_fit_{a.tag}.json"), "w") as f:
         json.dump(summary, f, indent=1)
     if a.install:
-        p = fit.as_dict()
-        beta = p["combined"] / 2 if p["has_combined"] else p["beta"]
-        gamma = 0.0 if p["has_combined"] else p["gamma"]
-        name = "genmodel_params_emulated.json" if a.emulated else "genmodel_params.json"
+        name = "genmodel_params_emulated.json" if a.shared else "genmodel_params.json"
+        params.update({"source": f"genmodel_fit_{a.tag}.json",
+                       "validation": {"rows": len(held), "median": summary["genmodel_err"]["median"],
+                                      "max": summary["genmodel_err"]["max"],
+                                      "by_plan_max": summary["genmodel_err"]["by_plan_max"]},
+                       "note": "per byte; fitted on CPS rows only, validated on held-out plans/sizes"})
         with open(os.path.join(ROOT, "profiles", name), "w") as f:
-            json.dump({"alpha": p["alpha"], "beta": beta, "gamma": gamma, "delta": p["delta"],
-                       "epsilon": p["epsilon"], "w_t": p["w_t"], "n_max_fit": nmax,
-                       "source": f"genmodel_fit_{a.tag}.json",
-                       "note": "per byte; beta = (2beta+gamma)/2 and gamma = 0 when only the combined "
-                               "term is identifiable (P:532)"}, f, indent=1)
+            json.dump(params, f, indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "rows"}, indent=1))
 
 
