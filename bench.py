@@ -403,7 +403,14 @@ def main():
                 "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                 "frac": round(achieved / NVLINK_PEAK_GBS, 4), "traffic": None,
                 "algorithmic_bytes_per_launch": int(wire),
-                "peak_source": "measured peer copy per direction (B200_PROFILING.md)"}
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                "nominal_peak": 900.0, "frac_nominal": round(achieved / 900.0, 4),
+                # NVLink wire bytes per user byte of the pull -> add -> push step, from ncu's
+                # nvltx/nvlrx counters (profiles/README.md: writes 1.269, read responses 1.148,
+                # read requests 0.221 per byte read): (1.269 + 1.148 + 0.221) / 2 = 1.319 per
+                # direction, so 900 GB/s of wire carries at most 682 GB/s of user data
+                "wire_per_user_byte": 1.319, "wire_user_ceiling": round(900.0 / 1.319, 1),
+                "frac_wire_ceiling": round(achieved / (900.0 / 1.319), 4)}
 
     # NVLS in-switch reduction (NEXT #1 plan kind, not a GenTree candidate), same size (N > 1)
     nvls = None

@@ -117,15 +117,19 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
 
 /* GenTree with the NVLS plan kind as an extra candidate (reading NV1;
  * the paper's min-GenModel selection): builds gentree_plan's plan, and on a
- * single-switch topology with dtype AR_F32 replaces it by the NVLS plan when
- * genmodel_choose_nvls(plan, params, nvls_params) prefers NVLS.  NVLS plans (also
+ * single-switch topology with dtype AR_F32 replaces it by the NVLS plan when the NVLS row
+ * predicts less time than the path the executor would run the plan on: the one-shot row
+ * (reading OS1, `oneshot_params`) when oneshot_params != NULL, the plan is one-shot eligible
+ * and count·esize <= oneshot_max_bytes (the communicator's cut-off); else the executed-plan
+ * prediction (genmodel_choose_nvls).  NVLS plans (also
  * force_kind "nvls" in gentree_plan; fp32 only, single switch) have the CPS data movement
  * and "switch_reduce": true in their JSON; every element ends as the correctly rounded fp32
  * sum of the ranks' inputs (reading NV2, measured) — the oracle's exactsum, bit for bit.
  * They run through allreduce_exec on a communicator with an attached NVLS buffer
  * (ar_comm_attach_nvls; dptr = that buffer).  params and nvls_params are required. */
 int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
-                      const gm_params *nvls_params, gt_plan **out);
+                      const gm_params *nvls_params, const gm_params *oneshot_params, uint64_t oneshot_max_bytes,
+                      gt_plan **out);
 
 /* Convenience: single switch with `world` ranks and uniform `params` (required). */
 int gentree_plan_single_switch(int32_t world, uint64_t count, int32_t dtype, const gm_params *params,

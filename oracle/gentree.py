@@ -396,16 +396,35 @@ def predict_plan(topo, plan: Plan, esize: int, params: Params | None = None) -> 
     return predict_f64(coeffs, sp)
 
 
-def gentree_nvls(topo, count: int, esize: int, params: Params, nvls_params: Params):
+def oneshot_eligible(plan: Plan) -> bool:
+    """A plan the executor's one-shot path runs with the plan's own bits: an
+    RS step of N reduces, one per block, each over all N ranks in one common order, then one
+    AG step."""
+    if plan.switch_reduce or len(plan.steps) != 2:
+        return False
+    rs, ag = plan.steps
+    if rs.phase != "rs" or ag.phase != "ag" or len(rs.reduces) != plan.n:
+        return False
+    order = rs.reduces[0].inputs
+    return (sorted(order) == list(range(plan.n)) and all(r.inputs == order for r in rs.reduces)
+            and sorted(r.block for r in rs.reduces) == list(range(plan.n)))
+
+
+def gentree_nvls(topo, count: int, esize: int, params: Params, nvls_params: Params,
+                 oneshot_params: Params | None = None, oneshot_max_bytes: int = 0):
     """GenTree with the NVLS plan kind as one more candidate (reading NV1; the paper's
     minimum-GenModel choice): on a single-switch topology in fp32, the NVLS plan
     replaces GenTree's plan iff the NVLS row's closed form (P:441-444 with its own α, β) is
-    strictly below the executed-plan prediction of GenTree's plan (ties keep the plan)."""
+    strictly below the prediction of the path the executor runs GenTree's plan on — the
+    one-shot row (reading OS1) for one-shot-eligible plans up to oneshot_max_bytes when its
+    parameters are given, else the executed-plan prediction (ties keep the plan)."""
     from .genmodel import predict_executed
     plan, reps = gentree(topo, count, esize, params)
     single = sum(1 for nd in topo.nodes.values() if nd.kind != "server") == 1
     if esize == 4 and single:
         t_plan = predict_executed(plan, esize, params)["total"]
+        if oneshot_params is not None and count * esize <= oneshot_max_bytes and oneshot_eligible(plan):
+            t_plan = closed_form_f64("oneshot", len(topo.servers), count * esize, oneshot_params)["total"]
         t_nvls = closed_form_f64("nvls", len(topo.servers), count * esize, nvls_params)["total"]
         if t_nvls < t_plan:
             return gentree(topo, count, esize, params, "nvls")

@@ -106,11 +106,15 @@ class Plan:
 
     @classmethod
     def from_topology_nvls(cls, topology_json: str, count: int, dtype, params: GmParams,
-                           nvls_params: GmParams) -> "Plan":
-        """GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1)."""
+                           nvls_params: GmParams, oneshot_params: GmParams | None = None,
+                           oneshot_max_bytes: int = 0) -> "Plan":
+        """GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1); with
+        oneshot_params, messages up to oneshot_max_bytes are compared on the one-shot row."""
         h = ctypes.c_void_p()
         check(lib.gentree_plan_nvls(topology_json.encode(), count, dtype_code(dtype), ctypes.byref(params),
-                                    ctypes.byref(nvls_params), ctypes.byref(h)))
+                                    ctypes.byref(nvls_params),
+                                    ctypes.byref(oneshot_params) if oneshot_params is not None else None,
+                                    int(oneshot_max_bytes), ctypes.byref(h)))
         return cls(h)
 
     @property

@@ -1683,24 +1683,6 @@ constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
 // scatter has landed).  Kept for A/B measurement behind AR_PUSH_MAX_MB.
 constexpr long long kPushDefaultMaxBytes = 0;
 
-// A plan the one-shot path can run with identical bits: two steps (RS, AG) whose RS step has
-// one reduce per block, every reduce over all ranks in the same order.  Returns that order.
-static std::vector<int> ll_order_of(const Plan &P) {
-  if (P.steps.size() != 2 || P.steps[0].ag || !P.steps[1].ag || (int)P.steps[0].reduces.size() != P.n) return {};
-  const std::vector<int> &ord = P.steps[0].reduces[0].inputs;
-  if ((int)ord.size() != P.n) return {};
-  std::vector<char> seen(P.n, 0), blk(P.n, 0);
-  for (int x : ord) {
-    if (x < 0 || x >= P.n || seen[x]) return {};
-    seen[x] = 1;
-  }
-  for (auto &rd : P.steps[0].reduces) {
-    if (rd.inputs != ord || rd.block < 0 || rd.block >= P.n || blk[rd.block]) return {};
-    blk[rd.block] = 1;
-  }
-  return ord;
-}
-
 static void init_comm(ar_comm *c) {
   CUDA_OK(cudaSetDevice(c->device));
   int nsm = 0;
@@ -2294,7 +2276,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   if (c->ll_opened && (long long)nbytes_call <= c->ll_max_bytes) {
     // low-latency one-shot path for CPS-shaped plans (see ar_ll_kernel)
     auto lit = c->ll_shape.find(plan->uid);
-    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
     if (!lit->second.empty()) {
       LLArgs la{};
       la.buf = (char *)dptr;
@@ -2323,7 +2305,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   if (c->local && c->flat && c->bulk && c->store_tma && c->trace == nullptr) {
     // emulated ranks, CPS-shaped plan: one flag-free launch over every SM (ar_flat_kernel)
     auto lit = c->ll_shape.find(plan->uid);
-    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
     if (!lit->second.empty()) {
       FlatArgs fa{};
       fa.base = (char *)dptr;
@@ -2386,7 +2368,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   bool use_push = false;
   if (c->ll_opened && c->push_max_bytes > 0 && (long long)bytes <= c->push_max_bytes) {
     auto lit = c->ll_shape.find(plan->uid);
-    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
     use_push = !lit->second.empty();
   }
   std::map<uint64_t, Lowered> &cache = use_push ? c->lowered_push : c->lowered;
@@ -2412,7 +2394,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       // and any CTA of a peer having posted implies the whole peer buffer is ready / done, so
       // tiles need not belong to fixed CTAs (range waits of multi-step plans do need that)
       auto lit = c->ll_shape.find(plan->uid);
-      if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, ll_order_of(plan->plan)).first;
+      if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
       if (!lit->second.empty() && !ops.empty()) {
         L.nops = (int)ops.size();
         CUDA_OK(cudaMalloc(&L.dyn_ctr, ops.size() * sizeof(unsigned int)));
@@ -2484,7 +2466,7 @@ int ar_exec_movement_plan(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t 
 // A plan whose every element is summed in ascending rank order by one reduce (natural CPS):
 // any element range can then run as its own CPS plan with the same bits.
 static bool ascending_cps(const Plan &p) {
-  std::vector<int> ord = ll_order_of(p);
+  std::vector<int> ord = oneshot_order(p);
   if (ord.empty()) return false;
   for (int i = 0; i < (int)ord.size(); i++)
     if (ord[i] != i) return false;

@@ -598,6 +598,26 @@ Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce
   return p;
 }
 
+// A plan the executor's one-shot path can run with identical bits: two steps
+// (RS, AG) whose RS step has one reduce per block, every reduce over all ranks in the same
+// order.  Returns that order (empty: not eligible).
+std::vector<int> oneshot_order(const Plan &P) {
+  if (P.switch_reduce) return {};
+  if (P.steps.size() != 2 || P.steps[0].ag || !P.steps[1].ag || (int)P.steps[0].reduces.size() != P.n) return {};
+  const std::vector<int> &ord = P.steps[0].reduces[0].inputs;
+  if ((int)ord.size() != P.n) return {};
+  std::vector<char> seen(P.n, 0), blk(P.n, 0);
+  for (int x : ord) {
+    if (x < 0 || x >= P.n || seen[x]) return {};
+    seen[x] = 1;
+  }
+  for (auto &rd : P.steps[0].reduces) {
+    if (rd.inputs != ord || rd.block < 0 || rd.block >= P.n || blk[rd.block]) return {};
+    blk[rd.block] = 1;
+  }
+  return ord;
+}
+
 // An NVLS plan is the single-switch CPS data movement: one RS step in which rank b
 // reduces block b from all ranks, then its reversed AllGather.
 void check_switch_reduce(const Plan &p) {

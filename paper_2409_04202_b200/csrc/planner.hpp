@@ -119,6 +119,7 @@ Plan build_plan_natural(const std::string &kind, int n, int64_t count);   // sta
 Plan plan_from_json(const std::string &text, std::string &dtype, bool &allreduce);
 void verify_allreduce(const Plan &p);                                      // throws InvalidArg
 void check_switch_reduce(const Plan &p);                                   // NVLS plans: CPS shape
+std::vector<int> oneshot_order(const Plan &p);   // one-shot-eligible plans: the common input order
 std::string plan_to_json(const Plan &p, const char *dtype);
 std::string report_to_json(const std::vector<SwitchReport> &r);
 

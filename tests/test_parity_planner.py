@@ -305,10 +305,15 @@ def test_nvls_plan_kind_parity():
             same_breakdown(lp.predict_executed(lib_params(nv_cheap)), OG.predict_executed(op, 4, nv_cheap))
             back = G.Plan.from_json(lp.to_json())
             assert back.to_json() == lp.to_json() and back.is_allreduce
+            osp = OG.Params(4.61e-6, 2.963e-12, 0.0, 0.0, 0.0, 1)     # one-shot row (reading OS1)
+            cut = min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256
             for nvp in (nv_cheap, nv_dear):
                 lg = G.Plan.from_topology_nvls(doc, count, "f32", lib_params(pp), lib_params(nvp))
                 og, _ = GT.gentree_nvls(t, count, 4, pp, nvp)
                 assert lg.to_json() == OP.plan_to_json(og, "f32")
+                lo = G.Plan.from_topology_nvls(doc, count, "f32", lib_params(pp), lib_params(nvp), lib_params(osp), cut)
+                oo, _ = GT.gentree_nvls(t, count, 4, pp, nvp, osp, cut)
+                assert lo.to_json() == OP.plan_to_json(oo, "f32")
                 lb = G.Plan.from_topology_nvls(doc, count, "bf16", lib_params(pp), lib_params(nvp))
                 assert not lb.switch_reduce        # bf16 never takes NVLS
         # large messages: the cheap NVLS row ((N+1)/N·0.9 < 2(N-1)/N·1.465 per byte) wins at
@@ -316,6 +321,12 @@ def test_nvls_plan_kind_parity():
         big = 1 << 26
         assert G.Plan.from_topology_nvls(doc, big, "f32", lib_params(pp), lib_params(nv_cheap)).switch_reduce
         assert not G.Plan.from_topology_nvls(doc, big, "f32", lib_params(pp), lib_params(nv_dear)).switch_reduce
+        # small messages: the one-shot row (4.6 µs) beats the NVLS row's 2α = 11.4 µs, so the
+        # plan stays although NVLS beats the flag-protocol prediction (2 × 9.4 µs)
+        small = 4096
+        assert G.Plan.from_topology_nvls(doc, small, "f32", lib_params(pp), lib_params(nv_cheap)).switch_reduce
+        assert not G.Plan.from_topology_nvls(doc, small, "f32", lib_params(pp), lib_params(nv_cheap),
+                                             lib_params(OG.Params(4.61e-6, 2.963e-12, 0, 0, 0, 1)), 1 << 20).switch_reduce
         with pytest.raises(G.ArInvalid):
             G.Plan.from_topology(doc, 1024, "bf16", lib_params(pp), "nvls")
         with pytest.raises(G.ArInvalid):

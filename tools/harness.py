@@ -222,10 +222,13 @@ def multi(args):
                 # the committed B200 fits; an NVLS pick runs through allreduce_exec on the
                 # attached multicast buffer, a plan pick on the IPC-registered one
                 fp, fn = fitted("genmodel_params.json"), fitted("genmodel_params_nvls.json")
+                fo = fitted("genmodel_fit_oneshot_graph.json")
+                cut = min(1536 * 1024, (3 << 19) // (world - 1)) // 256 * 256   # the comm's default cut-off
                 plan = G.Plan.from_topology_nvls(doc(world), count, args.dtype,
                                                  G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"],
                                                           fp["epsilon"], int(fp["w_t"])),
-                                                 G.params(alpha=fn["alpha"], beta=fn["beta"]))
+                                                 G.params(alpha=fn["alpha"], beta=fn["beta"]),
+                                                 G.params(alpha=fo["alpha"], beta=fo["beta"]), cut)
                 target, fill_fn = view, refill
                 if plan.switch_reduce:
                     if nvls_buf[0] is None:
@@ -400,14 +403,16 @@ def fanin_ag(args):
 
     for _ in range(3):
         G.local_reduce(bufs[:2], bufs[-1], count, args.dtype)
-    e0, e1 = ag_rate(4)
+    ag_rate(2)                       # warm-up: the first peer copy sets up the mapping
     torch.cuda.synchronize(1)
-    ag_alone = 4 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9
+    e0, e1 = ag_rate(8)
+    torch.cuda.synchronize(1)
+    ag_alone = 8 * (1 << 30) / (e0.elapsed_time(e1) / 1e3) / 1e9
     for k in range(2, args.kmax + 1):
         t_alone, m_alone = time_reduce(k)
         reps = 20
         # enough AG traffic queued to cover the whole timed region
-        ncopies = int(reps * t_alone * ag_alone * 1e9 / (1 << 30)) + 6
+        ncopies = int(1.5 * reps * t_alone * ag_alone * 1e9 / (1 << 30)) + 4
         e0, e1 = ag_rate(ncopies)
         time.sleep(0.002)
         t_conc, m_conc = time_reduce(k, reps)
@@ -418,7 +423,8 @@ def fanin_ag(args):
                  "hbm_bytes": (k + 1) * count * es,
                  "hbm_gbs_alone": (k + 1) * count * es / t_alone / 1e9,
                  "hbm_gbs_with_ag": (k + 1) * count * es / t_conc / 1e9,
-                 "ag_gbs_alone": ag_alone, "ag_gbs_during": ag_gbs})
+                 "ag_gbs_alone": ag_alone, "ag_gbs_during": ag_gbs,
+                 "ag_covers_timed_region": bool(ncopies * (1 << 30) / (ag_gbs * 1e9) >= reps * t_conc)})
 
 
 def mtrace(args):

@@ -1,0 +1,233 @@
+"""Regenerate profiles/round2/README.md from the round-2 evidence files under profiles/round2/.
+
+    python tools/profiles_report_r2.py > profiles/round2/README.md
+
+Every number comes from a file committed next to it (bench lines, harness JSONL sweeps, fit
+reports, ncu summaries)."""
+import glob
+import json
+import os
+import statistics
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+P = os.path.join(ROOT, "profiles", "round2")
+
+
+def jl(path):
+    if not os.path.exists(path):
+        return []
+    with open(path) as f:
+        return [json.loads(l) for l in f if l.startswith("{")]
+
+
+def jload(path):
+    rows = jl(path)
+    return rows[0] if rows else None
+
+
+def size(b):
+    if b >= 1 << 30:
+        return f"{b >> 30} GiB"
+    return f"{b >> 20} MiB" if b >= 1 << 20 else f"{b >> 10} KiB"
+
+
+def bench_section(out):
+    out.append("## 1. bench.py lines\n")
+    out.append("| file | GPUs | dtype | plan | kernel | busbw GB/s | roofline | NCCL default / Ring / NVLS-off | ours ÷ NCCL (default, Ring, NVLS-off) | NVLS kind | GenModel pred. err (held out) |")
+    out.append("|---|---|---|---|---|---|---|---|---|---|---|")
+    for f in sorted(glob.glob(os.path.join(P, "bench_*.json"))):
+        d = jload(f)
+        if not d or "value" not in d or d.get("impl") == "reference":
+            continue
+        rf = d["roofline"]
+        nc = d.get("nccl") or {}
+        ncs = " / ".join(str(nc.get(k, {}).get("busbw", "-")) for k in ("default", "ring", "nvls_off")) if nc else "-"
+        vs = d.get("vs_nccl") or {}
+        vss = ", ".join(f"{vs[k]:.3f}" for k in ("default", "ring", "nvls_off") if k in vs) or "-"
+        roof = f"{rf['bound']} {rf['achieved']} / {rf['peak']} = {rf['frac']}"
+        if "frac_wire_ceiling" in rf:
+            roof += f"; {rf['frac_wire_ceiling']} of the {rf['wire_user_ceiling']} wire ceiling"
+        nv = (d.get("nvls") or {}).get("busbw", "-")
+        out.append(f"| `{os.path.basename(f)}` | {d['n_gpus']} | {d['dtype']} | {d['config']['plan']} | "
+                   f"`{rf.get('kernel')}` | {d['value']} | {roof} | {ncs} | {vss} | {nv} | "
+                   f"{d.get('genmodel', {}).get('pred_err', '-')} |")
+    out.append("")
+
+
+def nccl_algo_section(out):
+    logs = sorted(glob.glob(os.path.join(P, "nccl", "nccl_tuning*.log")))
+    if not logs:
+        return
+    out.append("## 2b. NCCL's algorithm choice (NCCL_DEBUG_SUBSYS=TUNING, default env, 4 GPUs, fp32)\n")
+    seen = {}
+    for f in logs[:1]:
+        for line in open(f):
+            if "Algo" in line and "Bytes" in line:
+                try:
+                    tail = line.split("AllReduce:")[1].strip()
+                except IndexError:
+                    continue
+                nb = int(tail.split()[0])
+                seen.setdefault(nb, tail)
+    out.append("| bytes | NCCL's line |")
+    out.append("|---|---|")
+    for nb in sorted(seen):
+        out.append(f"| {size(nb)} | `{seen[nb][:110]}` |")
+    out.append("")
+
+
+def c2_section(out):
+    out.append("## 2. C2: fp32 busbw vs size — GenTree, GenTree incl. NVLS (min-GenModel pick), NCCL default / Ring / NVLS-off\n")
+    for n in (4, 2):
+        ours = jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
+        if not ours:
+            continue
+        ring = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclring.jsonl"))
+        off = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclnvlsoff.jsonl"))
+        for timing in ("graph", "eager"):
+            def get(rows, impl, plan):
+                return {r["bytes"]: r for r in rows if r.get("timing") == timing and r["impl"] == impl
+                        and r["plan"] == plan}
+            g = get(ours, "ours", "gentree")
+            gn = get(ours, "ours", "gentree+nvls")
+            nv = get(ours, "ours", "nvls")
+            nd = get(ours, "nccl", "default")
+            nr = get(ring, "nccl", "Ring")
+            no = get(off, "nccl", "nvls_off")
+            if not g:
+                continue
+            out.append(f"**{n} × B200, fp32, {timing} timing** (busbw GB/s, median)\n")
+            out.append("| size | GenTree | GenTree incl. NVLS (pick) | NVLS | NCCL default | NCCL Ring | NCCL NVLS-off | GenTree ÷ NCCL Ring | pick ÷ best NCCL |")
+            out.append("|---|---|---|---|---|---|---|---|---|")
+            for b in sorted(g):
+                def v(d):
+                    return d[b]["busbw_med"] if b in d else float("nan")
+                pick = f"{v(gn):.1f} ({gn[b]['chosen']})" if b in gn else "-"
+                best = max(x for x in (v(nd), v(nr), v(no)) if x == x) if any(b in d for d in (nd, nr, no)) else float("nan")
+                out.append(f"| {size(b)} | {v(g):.1f} | {pick} | {v(nv):.1f} | {v(nd):.1f} | {v(nr):.1f} | {v(no):.1f} | "
+                           f"{v(g) / v(nr):.2f} | {(v(gn) / best) if b in gn else float('nan'):.2f} |")
+            out.append("")
+
+
+def fit_section(out):
+    for tag, title in (("nvlink_r2", "NVLink ranks (one per GPU), N = 2..4"),
+                       ("emulated8_shared", "8 ranks emulated on one GPU (shared HBM, reading A6e)")):
+        f = os.path.join(ROOT, "profiles", f"genmodel_fit_{tag}.json")
+        if not os.path.exists(f):
+            continue
+        d = json.load(open(f))
+        ge = d["genmodel_err"]
+        out.append(f"### GenModel, {title} — `profiles/genmodel_fit_{tag}.json`\n")
+        out.append(f"* fit rows (CPS only): {d['fit_rows']}; held-out validation rows: {d['validation_rows']}")
+        pp = d["params_per_byte"]
+        out.append(f"* params per byte: " + ", ".join(f"{k} = {pp[k]:.4g}" for k in ("alpha", "beta", "gamma", "delta",
+                                                                                      "epsilon", "combined")
+                                                        if k in pp and isinstance(pp[k], float)) +
+                   (f", w_t = {pp['w_t']}" if "w_t" in pp else ""))
+        out.append(f"* held-out error: median {ge['median']:.3f}, max {ge['max']:.3f}")
+        out.append("")
+        out.append("| plan | median | max |")
+        out.append("|---|---|---|")
+        for k in ge["by_plan_max"]:
+            out.append(f"| {k} | {ge['by_plan_median'][k]:.3f} | {ge['by_plan_max'][k]:.3f} |")
+        if "abc_err" in d:
+            out.append("")
+            out.append(f"(α,β,γ) model on the same rows: median {d['abc_err']['median']:.3f}, max {d['abc_err']['max']:.3f}; "
+                       f"GenModel on the paper's unfused steps: median {d['genmodel_paper_steps_err']['median']:.3f}, "
+                       f"max {d['genmodel_paper_steps_err']['max']:.3f}.")
+        out.append("")
+
+
+def push_section(out):
+    rows = []
+    for n in (2, 4):
+        pu = {r["bytes"]: r for r in jl(os.path.join(P, "push", f"pull_n{n}.jsonl"))}
+        ps = {r["bytes"]: r for r in jl(os.path.join(P, "push", f"push_n{n}.jsonl"))}
+        for b in sorted(pu):
+            if b in ps:
+                rows.append((n, b, pu[b]["busbw_med"], ps[b]["busbw_med"]))
+    if not rows:
+        return
+    out.append("## 4. Write-only (push) protocol vs pull → add → push, bf16, graph timing\n")
+    out.append("| GPUs | size | pull (default) busbw | push (AR_PUSH_MAX_MB) busbw | push ÷ pull |")
+    out.append("|---|---|---|---|---|")
+    for n, b, a, c in rows:
+        out.append(f"| {n} | {size(b)} | {a:.1f} | {c:.1f} | {c / a:.3f} |")
+    out.append("")
+
+
+def fence_section(out):
+    a = {(r["bytes"], r["timing"]): r for r in jl(os.path.join(P, "latency", "fence0_n4.jsonl"))}
+    b = {(r["bytes"], r["timing"]): r for r in jl(os.path.join(P, "latency", "fence1_n4.jsonl"))}
+    if not a:
+        return
+    out.append("## 5. Entry-flag ordering: relaxed (default) vs fence.acq_rel.sys first (AR_ENTRY_FENCE=1), 4 GPUs, fp32, one-shot path off\n")
+    out.append("| size | timing | relaxed µs | fenced µs | fenced ÷ relaxed |")
+    out.append("|---|---|---|---|---|")
+    for k in sorted(a):
+        if k in b:
+            out.append(f"| {size(k[0])} | {k[1]} | {a[k]['t_med'] * 1e6:.1f} | {b[k]['t_med'] * 1e6:.1f} | "
+                       f"{b[k]['t_med'] / a[k]['t_med']:.3f} |")
+    out.append("")
+
+
+def p2p_section(out):
+    rows = jl(os.path.join(P, "c3", "p2p_n4.jsonl"))
+    if not rows:
+        return
+    out.append("## 6. C3-ii: x-to-x and x-to-1 fan-in over NVLink (4 × B200, fp32; P:418-428)\n")
+    out.append("| receiver bytes | pattern | x | µs (median) | GB/s per receiver |")
+    out.append("|---|---|---|---|---|")
+    for r in rows:
+        out.append(f"| {size(r['recv_bytes'])} | {r['pattern']} | {r['x']} | {r['t_med'] * 1e6:.1f} | {r['gbs_per_receiver']:.1f} |")
+    out.append("")
+
+
+def fanin_ag_section(out):
+    rows = jl(os.path.join(P, "c3", "fanin_ag.jsonl"))
+    if not rows:
+        return
+    out.append("## 7. C3-iv: Eq. 6 local fan-in alone and under an incoming NVLink AllGather stream\n")
+    out.append("| x | T alone µs | T with AG µs | HBM GB/s alone | HBM GB/s with AG | AG GB/s alone | AG GB/s during | slowdown |")
+    out.append("|---|---|---|---|---|---|---|---|")
+    for r in rows:
+        out.append(f"| {r['k']} | {r['t_med_alone'] * 1e6:.1f} | {r['t_med_with_ag'] * 1e6:.1f} | {r['hbm_gbs_alone']:.0f} | "
+                   f"{r['hbm_gbs_with_ag']:.0f} | {r['ag_gbs_alone']:.0f} | {r['ag_gbs_during']:.0f} | "
+                   f"{r['t_med_with_ag'] / r['t_med_alone']:.3f} |")
+    out.append("")
+
+
+def cpu_section(out):
+    rows = jl(os.path.join(P, "cpu_oracle_timing.jsonl"))
+    if not rows:
+        return
+    out.append("## 8. CPU oracle timing plan (SURVEY §8(d)), one pinned core of the GPU box's host\n")
+    r0 = rows[0]
+    out.append(f"Host: {r0['cpu_model']}, os.cpu_count() = {r0['cpu_count']}, pinned to core {r0['pinned_core']}.\n")
+    out.append("| config | ranks | size/rank | dtype | plan build s | simulate s | oracle busbw GB/s |")
+    out.append("|---|---|---|---|---|---|---|")
+    for r in rows:
+        out.append(f"| {r['config']} | {r['ranks']} | {size(r['bytes_per_rank'])} | {r['dtype']} | {r['t_plan_s']:.3f} | "
+                   f"{r['t_simulate_s']:.2f} | {r['oracle_busbw_gbs']:.3f} |")
+    out.append("")
+
+
+def main():
+    out = ["# profiles/round2 — measured evidence (round 2)\n",
+           "Generated by `tools/profiles_report_r2.py` from the files in this directory.  Commands:",
+           "`COMMANDS.md`.  Round-1 evidence: `../README.md`.\n"]
+    bench_section(out)
+    c2_section(out)
+    nccl_algo_section(out)
+    out.append("## 3. GenModel fit and held-out prediction error\n")
+    fit_section(out)
+    push_section(out)
+    fence_section(out)
+    p2p_section(out)
+    fanin_ag_section(out)
+    cpu_section(out)
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main()
