@@ -44,20 +44,29 @@ def main():
         count = nbytes // 4
         plan = G.Plan.single_switch(n, count, "f32", gp)
         kind = plan.report()[-1]["chosen"]
+        op = G.params(alpha=oj["alpha"], beta=oj["beta"])
         if nbytes <= ll_max:
-            t_plan = oj["alpha"] + 2 * (n - 1) * nbytes * oj["beta"]
+            t_plan = G.genmodel_closed_form("oneshot", n, nbytes, op)["total"]
             path = "one-shot"
         else:
             t_plan = plan.predict_executed(gp)["total"]
             path = f"{kind} (executed steps)"
         c = plan.choose_nvls(gp, npar)
+        doc = json.dumps({"nodes": [{"id": "sw", "kind": "switch", "parent": None, "uplink": None}] + [
+            {"id": f"s{i}", "kind": "server", "parent": "sw",
+             "uplink": {"alpha": 0, "beta": 1, "epsilon": 0, "w_t": 1}, "compute": {"gamma": 0, "delta": 0}}
+            for i in range(n)]})
+        pick = G.Plan.from_topology_nvls(doc, count, "f32", gp, npar, op, ll_max)
+        t_pick = c["t_nvls"] if pick.switch_reduce else t_plan
         rows.append({"bytes": nbytes, "gentree_plan": kind, "path": path, "t_pred_s": t_plan,
                      "busbw_pred": round(busbw(nbytes, n, t_plan), 1), "t_nvls_pred_s": c["t_nvls"],
-                     "nvls_busbw_pred": round(busbw(nbytes, n, c["t_nvls"]), 1)})
+                     "nvls_busbw_pred": round(busbw(nbytes, n, c["t_nvls"]), 1),
+                     "gentree_incl_nvls_pick": "nvls" if pick.switch_reduce else kind,
+                     "pick_busbw_pred": round(busbw(nbytes, n, t_pick), 1)})
     out = {"tool": "predict8", "world": n, "dtype": "f32", "kind": "GenModel prediction, not a measurement",
            "params": pj["source"], "nvls_params": nj["source"], "oneshot_params": "genmodel_fit_oneshot_graph.json",
            "oneshot_max_bytes": ll_max,
-           "fit_range": "parameters fitted on N = 2..4 (w_t >= 4, eps = 0: no incast seen up to the whole box)",
+           "fit_range": "parameters fitted on CPS rows at N = 2..4 (w_t >= 4, eps = 0: no incast seen up to the 4-GPU lease)",
            "context": "NCCL 8-rank all-reduce busbw 725 GB/s at 1 GiB on B200 (B200_PROFILING.md)",
            "rows": rows}
     print(json.dumps(out, indent=1))
