@@ -1111,6 +1111,183 @@ __global__ void __launch_bounds__(kThreads) ar_ll_kernel(const __grid_constant__
   }
 }
 
+// ------------------------------------------------------------------ LL128 two-shot path
+// Mid-size messages on one rank per GPU, CPS-shaped plans whose blocks start on 16-byte
+// boundaries: the CPS plan's RS and AG steps with the flags carried IN the data, so no flag
+// round trip and no system-scope release is needed (each costs microseconds on B200, §6).
+// Data moves in 128-byte lines: 120 payload bytes + an 8-byte flag = the call's epoch in the
+// last 8 bytes.  Eight lanes write one line with one warp-wide 16-byte-per-lane store, which
+// NVLink delivers as one 128-byte write; a reader loads the line the same way (one 128-byte
+// read) and accepts it only when the flag equals its epoch — the property NCCL's LL128
+// protocol relies on.  Per call and rank r:
+//   1. for every block b != r: write my slice of block b as lines into owner b's RS area;
+//   2. reduce my block r in the plan's order (my own slice from my buffer, the others'
+//      from my RS area once their flags arrive), store the result into my buffer and as
+//      lines into every peer's AG area;
+//   3. copy every other owner's result lines from my AG area into my buffer.
+// Same inputs, same association and the same rounding as the CPS plan: the plan's bits.
+// Scratch is double-buffered by epoch parity, with the argument of ar_ll_kernel.
+struct LL128Args {
+  char *buf;                              // this rank's data (in place)
+  char *peer_scr[AR_MAX_RANKS];           // rank -> its LL128 region as seen here
+  char *my_scr;
+  int order[AR_MAX_RANKS];                // the plan's summation order
+  long long blk_bytes;                    // bytes per block (all blocks equal, multiple of 16)
+  long long lines;                        // 128-byte lines per block
+  long long lines_cap;                    // lines per (parity, area, source) slot
+  int me, world, esize, avg_n;
+  unsigned long long *epoch_dev;          // last completed LL128 call (device-resident)
+  unsigned int *done_ctr;
+  unsigned long long *err;
+  unsigned long long timeout_ns;
+};
+constexpr int kLineBytes = 128, kLinePayload = 120;
+
+__device__ __forceinline__ void st_vol_v2u64(void *p, unsigned long long a, unsigned long long b) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_vol_v2u64(const void *p, unsigned long long &a, unsigned long long &b) {
+  asm volatile("ld.volatile.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// scratch line: [parity][area (0 = RS, 1 = AG)][source rank][line]
+__device__ __forceinline__ char *ll128_line(char *base, const LL128Args &a, int par, int area, int src, long long i) {
+  return base + ((((long long)par * 2 + area) * a.world + src) * a.lines_cap + i) * kLineBytes;
+}
+// this lane's payload words of line i of a block that starts at `blk` (part j < 7: bytes
+// 16j..16j+15, part 7: bytes 112..119); words past the block's end read as 0
+__device__ __forceinline__ void ll128_payload(const char *blk, long long blk_bytes, long long i, int j,
+                                              unsigned long long &w0, unsigned long long &w1) {
+  const long long o = i * kLinePayload + 16LL * j;
+  w0 = o + 8 <= blk_bytes ? *(const unsigned long long *)(blk + o) : 0ull;
+  w1 = (j < 7 && o + 16 <= blk_bytes) ? *(const unsigned long long *)(blk + o + 8) : 0ull;
+}
+__device__ __forceinline__ void ll128_store_payload(char *blk, long long blk_bytes, long long i, int j,
+                                                    unsigned long long w0, unsigned long long w1) {
+  const long long o = i * kLinePayload + 16LL * j;
+  if (o + 8 <= blk_bytes) *(unsigned long long *)(blk + o) = w0;
+  if (j < 7 && o + 16 <= blk_bytes) *(unsigned long long *)(blk + o + 8) = w1;
+}
+// Load line i from a scratch slot until its flag (lane 7 of the 8-lane group, second word)
+// equals `flag`.  Every lane of the warp runs the loop (__any_sync); lanes without a line
+// (live == false) count as valid.
+__device__ __forceinline__ bool ll128_load(const char *line, int j, bool live, unsigned long long flag,
+                                           unsigned long long &w0, unsigned long long &w1,
+                                           const LL128Args &a, unsigned long long start) {
+  const int lane = threadIdx.x & 31;
+  unsigned int spins = 0;
+  for (;;) {
+    if (live) ld_vol_v2u64(line + 16 * j, w0, w1);
+    const unsigned long long f = __shfl_sync(0xffffffffu, w1, (lane & ~7) | 7);
+    const bool bad = live && f != flag;
+    if (!__any_sync(0xffffffffu, bad)) return true;
+    if ((++spins & 1023u) == 0 && globaltimer() - start > a.timeout_ns) {
+      atomicExch(a.err, 1ull);
+      return false;
+    }
+  }
+}
+
+template <bool BF16>
+__device__ __forceinline__ void ll128_acc(float (&acc)[8], unsigned long long w0, unsigned long long w1, bool first) {
+  const uint32_t u[4] = {(uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32)};
+#pragma unroll
+  for (int k = 0; k < (BF16 ? 8 : 4); k++) {
+    const float v = BF16 ? ((k & 1) ? bf_hi(u[k >> 1]) : bf_lo(u[k >> 1])) : __uint_as_float(u[k]);
+    acc[k] = first ? v : __fadd_rn(acc[k], v);
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ void ll128_pack(const float (&acc)[8], unsigned long long &w0, unsigned long long &w1) {
+  uint32_t u[4];
+  if (BF16) {
+#pragma unroll
+    for (int k = 0; k < 4; k++) u[k] = f2bf(acc[2 * k]) | (f2bf(acc[2 * k + 1]) << 16);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; k++) u[k] = __float_as_uint(acc[k]);
+  }
+  w0 = (unsigned long long)u[0] | ((unsigned long long)u[1] << 32);
+  w1 = (unsigned long long)u[2] | ((unsigned long long)u[3] << 32);
+}
+
+template <bool BF16>
+__global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constant__ LL128Args a) {
+  __shared__ unsigned long long s_epoch;
+  if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
+  __syncthreads();
+  const unsigned long long epoch = s_epoch;
+  const int par = (int)(epoch & 1ull);
+  const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3;
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long L = a.lines;
+  const long long iters = (L + nwarps * 4 - 1) / (nwarps * 4);   // same trip count in every lane
+  const unsigned long long start = globaltimer();
+  // 1. scatter my slices of the other blocks to their owners
+  for (int b = 0; b < a.world; b++) {
+    if (b == a.me) continue;
+    const char *blk = a.buf + (long long)b * a.blk_bytes;
+    char *dst = ll128_line(a.peer_scr[b], a, par, 0, a.me, 0);
+    for (long long it = 0; it < iters; it++) {
+      const long long i = (it * nwarps + gwarp) * 4 + sub;
+      if (i >= L) continue;
+      unsigned long long w0, w1;
+      ll128_payload(blk, a.blk_bytes, i, j, w0, w1);
+      st_vol_v2u64(dst + i * kLineBytes + 16 * j, w0, j == 7 ? epoch : w1);
+    }
+  }
+  // 2. reduce my block in the plan's order; result to my buffer and every peer's AG area
+  {
+    char *blk = a.buf + (long long)a.me * a.blk_bytes;
+    for (long long it = 0; it < iters; it++) {
+      const long long i = (it * nwarps + gwarp) * 4 + sub;
+      const bool live = i < L;
+      float acc[8];
+      for (int k = 0; k < a.world; k++) {
+        const int q = a.order[k];
+        unsigned long long w0 = 0, w1 = 0;
+        if (q == a.me) {
+          if (live) ll128_payload(blk, a.blk_bytes, i, j, w0, w1);
+        } else {
+          ll128_load(ll128_line(a.my_scr, a, par, 0, q, live ? i : 0), j, live, epoch, w0, w1, a, start);
+          if (j == 7) w1 = 0ull;   // the flag word carries no payload
+        }
+        ll128_acc<BF16>(acc, w0, w1, k == 0);
+      }
+      if (!live) continue;
+      if (a.avg_n)
+        for (int k = 0; k < 8; k++) acc[k] = __fdiv_rn(acc[k], (float)a.avg_n);
+      unsigned long long r0, r1;
+      ll128_pack<BF16>(acc, r0, r1);
+      ll128_store_payload(blk, a.blk_bytes, i, j, r0, r1);
+      for (int d = 0; d < a.world; d++) {
+        if (d == a.me) continue;
+        st_vol_v2u64(ll128_line(a.peer_scr[d], a, par, 1, a.me, i) + 16 * j, r0, j == 7 ? epoch : r1);
+      }
+    }
+  }
+  // 3. gather the other owners' results
+  for (int o = 0; o < a.world; o++) {
+    if (o == a.me) continue;
+    char *blk = a.buf + (long long)o * a.blk_bytes;
+    for (long long it = 0; it < iters; it++) {
+      const long long i = (it * nwarps + gwarp) * 4 + sub;
+      const bool live = i < L;
+      unsigned long long w0 = 0, w1 = 0;
+      ll128_load(ll128_line(a.my_scr, a, par, 1, o, live ? i : 0), j, live, epoch, w0, w1, a, start);
+      if (live) ll128_store_payload(blk, a.blk_bytes, i, j, w0, w1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (atomicAdd(a.done_ctr, 1u) == gridDim.x - 1) {
+      *(volatile unsigned int *)a.done_ctr = 0;
+      *(volatile unsigned long long *)a.epoch_dev = epoch;
+      __threadfence();
+    }
+  }
+}
+
 // ------------------------------------------------------------------ synthetic inputs
 __device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
   x += 0x9E3779B97F4A7C15ull;
@@ -1256,6 +1433,11 @@ struct ar_comm {
   std::vector<char *> ll_peer;                 // rank -> scratch as seen here
   bool ll_opened = false;
   int ll_ctas = 32;
+  // LL128 two-shot path (ar_ll128_kernel) for CPS-shaped plans with 16-byte-aligned equal
+  // blocks, ll_max_bytes < message <= ll128_max_bytes (AR_LL128_MAX_KB; 0 = off); its scratch
+  // follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
+  long long ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
+  int ll128_ctas = 64;
   std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
   // chunked end-to-end path (exec_host_chunked)
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -1283,7 +1465,7 @@ struct Blob {
   // the CTA count the range/paired waits are computed for, the one-shot scratch plane size and
   // the path cut-offs
   int32_t nctas, cta_cap, rpp, pad2;
-  int64_t ll_cap_lines, ll_max_bytes, push_max_bytes;
+  int64_t ll_cap_lines, ll_max_bytes, push_max_bytes, ll128_max_bytes;
   // same-process peers (several communicators in one process, e.g. one per rank on one GPU):
   // CUDA IPC handles cannot be opened by the exporting process, so the raw pointers are used
   int64_t pid;
@@ -1677,6 +1859,8 @@ static int resident_ctas(int device) {
   }
 
 constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
+// LL128 two-shot path up to this message size (AR_LL128_MAX_KB; 0 = off)
+constexpr long long kLL128DefaultMaxBytes = 16LL << 20;
 // Off by default: measured slower than the pull protocol on 2 and 4 B200s (4 GPUs, 1 MiB:
 // 27.7 vs 22.0 us; 16 MiB: 66.9 vs 55.4 us — the scatter step's per-block copies serialise
 // load -> store -> completion per tile, and the owner cannot start before every source's
@@ -1700,9 +1884,9 @@ static void init_comm(ar_comm *c) {
   CUDA_OK(cudaMalloc(&c->sig_local, pages * c->page_elems * sizeof(unsigned long long)));
   CUDA_OK(cudaMemset(c->sig_local, 0, pages * c->page_elems * sizeof(unsigned long long)));
   // device words: [0] error, [1] last completed epoch, [2] finished-CTA counter,
-  // [3] last completed LL epoch, [4] LL finished-CTA counter
-  CUDA_OK(cudaMalloc(&c->err, 6 * sizeof(unsigned long long)));
-  CUDA_OK(cudaMemset(c->err, 0, 6 * sizeof(unsigned long long)));
+  // [3] last completed LL epoch, [4] LL finished-CTA counter, [5] LL128 epoch, [6] LL128 counter
+  CUDA_OK(cudaMalloc(&c->err, 8 * sizeof(unsigned long long)));
+  CUDA_OK(cudaMemset(c->err, 0, 8 * sizeof(unsigned long long)));
   if (c->local) {   // ar_flat_kernel's tile counters (dynamic scheduling)
     CUDA_OK(cudaMalloc(&c->flat_ctr, (AR_MAX_RANKS + 1) * sizeof(unsigned int)));
     CUDA_OK(cudaMemset(c->flat_ctr, 0, (AR_MAX_RANKS + 1) * sizeof(unsigned int)));
@@ -1742,13 +1926,18 @@ static void init_comm(ar_comm *c) {
     if (const char *v = std::getenv("AR_LL_MAX_KB")) c->ll_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
     c->ll_max_bytes = std::max(0LL, c->ll_max_bytes);
     c->push_max_bytes = std::max(0LL, c->push_max_bytes);
-    if (c->ll_max_bytes > 0 || c->push_max_bytes > 0) {
+    c->ll128_max_bytes = kLL128DefaultMaxBytes;
+    if (const char *v = std::getenv("AR_LL128_MAX_KB")) c->ll128_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
+    c->ll128_max_bytes = std::max(0LL, c->ll128_max_bytes);
+    if (c->ll_max_bytes > 0 || c->push_max_bytes > 0 || c->ll128_max_bytes > 0) {
       c->ll_cap_lines = (2 * c->ll_max_bytes + 7) / 8;   // room to raise the cut-off 2x (ar_comm_set_oneshot_max)
       c->ll_region = ((long long)2 * c->world * c->ll_cap_lines * 16 + 255) / 256 * 256;
       // one block of the largest pushed message + 16 bytes of alignment phase
       c->push_slot = ((c->push_max_bytes + c->world - 1) / c->world + 16 + 255) / 256 * 256;
       c->push_plane = c->push_slot * c->world;
-      const size_t sz = (size_t)c->ll_region + (c->push_max_bytes > 0 ? (size_t)2 * c->push_plane : 0);
+      c->ll128_off = c->ll_region + (c->push_max_bytes > 0 ? 2 * c->push_plane : 0);
+      c->ll128_cap_lines = (c->ll128_max_bytes / c->world + kLinePayload - 1) / kLinePayload;
+      const size_t sz = (size_t)c->ll128_off + (size_t)4 * c->world * c->ll128_cap_lines * kLineBytes;
       CUDA_OK(cudaMalloc(&c->ll_scratch, sz));
       CUDA_OK(cudaMemset(c->ll_scratch, 0, sz));
       c->ll_peer.assign(c->world, nullptr);
@@ -1756,6 +1945,7 @@ static void init_comm(ar_comm *c) {
     }
   }
   if (const char *v = std::getenv("AR_LL_CTAS")) c->ll_ctas = std::max(1, std::atoi(v));
+  if (const char *v = std::getenv("AR_LL128_CTAS")) c->ll128_ctas = std::max(1, std::atoi(v));
 }
 
 }  // namespace
@@ -1874,6 +2064,7 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     b.ll_cap_lines = c->ll_cap_lines;
     b.ll_max_bytes = c->ll_max_bytes;
     b.push_max_bytes = c->push_max_bytes;
+    b.ll128_max_bytes = c->ll128_max_bytes;
     b.pid = (int64_t)getpid();
     b.device = c->device;
     b.raw_base = (uint64_t)(uintptr_t)base;
@@ -1920,9 +2111,10 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
         throw InvalidArg("corrupt or misordered blob");
       if (b->bytes != mine->bytes) throw InvalidArg("ranks registered buffers of different sizes");
       if (b->nctas != c->nctas || b->cta_cap != c->cta_cap || b->rpp != c->rpp || b->ll_cap_lines != c->ll_cap_lines ||
-          b->ll_max_bytes != mine->ll_max_bytes || b->push_max_bytes != c->push_max_bytes)
+          b->ll_max_bytes != mine->ll_max_bytes || b->push_max_bytes != c->push_max_bytes ||
+          b->ll128_max_bytes != c->ll128_max_bytes)
         throw InvalidArg("ranks disagree on communicator settings (ar_comm_set_ctas, AR_LL_MAX_KB, "
-                         "AR_PUSH_MAX_MB or the one-shot cut-off must be identical on every rank)");
+                         "AR_LL128_MAX_KB, AR_PUSH_MAX_MB or the one-shot cut-off must be identical on every rank)");
       if (t == c->proc) continue;
       const bool same_proc = b->pid == me_pid;
       if (same_proc && b->device != c->device) {
@@ -2299,6 +2491,39 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
       c->last_kernel = "ar_ll_kernel";
+      return AR_OK;
+    }
+  }
+  if (c->ll_opened && c->ll128_max_bytes > 0 && (long long)nbytes_call > c->ll_max_bytes &&
+      (long long)nbytes_call <= c->ll128_max_bytes && count % (uint64_t)c->world == 0 &&
+      (count / c->world) * plan->esize % 16 == 0) {
+    // LL128 two-shot path for CPS-shaped plans with equal 16-byte-aligned blocks (ar_ll128_kernel)
+    auto lit = c->ll_shape.find(plan->uid);
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
+    if (!lit->second.empty()) {
+      LL128Args la{};
+      la.buf = (char *)dptr;
+      for (int t = 0; t < c->world; t++) la.peer_scr[t] = c->ll_peer[t] + c->ll128_off;
+      la.my_scr = c->ll_scratch + c->ll128_off;
+      for (int k = 0; k < c->world; k++) la.order[k] = lit->second[k];
+      la.blk_bytes = (long long)(count / c->world) * plan->esize;
+      la.lines = (la.blk_bytes + kLinePayload - 1) / kLinePayload;
+      la.lines_cap = c->ll128_cap_lines;
+      la.me = c->rank;
+      la.world = c->world;
+      la.esize = plan->esize;
+      la.avg_n = avg_n;
+      la.epoch_dev = c->err + 5;
+      la.done_ctr = (unsigned int *)(c->err + 6);
+      la.err = c->err;
+      la.timeout_ns = c->timeout_ns;
+      const long long warps_needed = (la.lines + 3) / 4;
+      const int ctas = (int)std::max(1LL, std::min<long long>(c->ll128_ctas, (warps_needed + 15) / 16));
+      if (plan->esize == 2) ar_ll128_kernel<true><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      else ar_ll128_kernel<false><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      CUDA_OK(cudaGetLastError());
+      c->last_launches = 1;
+      c->last_kernel = "ar_ll128_kernel";
       return AR_OK;
     }
   }

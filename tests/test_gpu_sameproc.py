@@ -282,3 +282,29 @@ def test_unverified_plan_is_refused():
             G.allreduce_exec(good, comm, buf[: count * 4])
     finally:
         comm.destroy()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_ll128_path(world, dtype):
+    """ar_ll128_kernel (mid-size CPS-shaped plans with equal 16-byte-aligned blocks): the CPS
+    plan's RS and AG steps with the flag inside every 128-byte line — bit-identical to the
+    plan; partial last lines; SUM and AVG; back-to-back calls alternating with the one-shot
+    and the flag paths on the same communicators (epoch parity of both scratch areas)."""
+    es = 4 if dtype == "f32" else 2
+    sp = SameProcess(world, 16 << 20)
+    unit = world * 16 // es                        # blocks start on 16-byte boundaries
+    try:
+        sizes = [(2 << 20) // es // unit * unit, 2_000_000 // unit * unit, (16 << 20) // es - unit]
+        for count in sizes:
+            check(sp, world, count, dtype, None, expect_kernel="ar_ll128_kernel")
+        check(sp, world, sizes[1], dtype, None, op="avg", expect_kernel="ar_ll128_kernel")
+        for count, kern in ((sizes[0], "ar_ll128_kernel"), (4093, "ar_ll_kernel"), (sizes[0] + 1, "ar_exec_kernel"),
+                            (sizes[1], "ar_ll128_kernel"), (sizes[1], "ar_ll128_kernel")):
+            check(sp, world, count, dtype, None, calls=2, expect_kernel=kern)
+        for mode in ("integer", "specials"):
+            check(sp, world, sizes[1], dtype, None, mode=mode, expect_kernel="ar_ll128_kernel")
+        if world == 4:   # multi-step plans never take it
+            check(sp, world, sizes[0], dtype, "ring", expect_kernel="ar_exec_kernel")
+    finally:
+        sp.destroy()
