@@ -274,7 +274,10 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
  * and the tile counters (dynamic tile scheduling of CPS-shaped plans) that the
  * previous launch left.  Every element of every rank's buffer ends
  * equal to the plan's left-to-right fp32 sum of the ranks' inputs (bit-exact to the CPU
- * oracle).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
+ * oracle).  One rank per GPU, CPS-shaped plans take a flag-free path by size: the one-shot
+ * kernel up to the one-shot cut-off, the LL128 two-shot kernel (flags inside 128-byte lines)
+ * up to AR_LL128_MAX_KB (16 MiB default) when the blocks are equal and 16-byte aligned, else
+ * the step-table kernel — all with the plan's bits (ar_comm_last_kernel tells which).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
  * plan's, unregistered or misaligned buffer; AR_ESYS on launch failure. */
 int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
                    void *stream);
@@ -309,8 +312,9 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *comm, void *dptr, void *ho
 /* Device kernels launched by the last allreduce_exec of this comm (per rank, per call). */
 int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
 /* Name of the kernel the last allreduce_exec of this comm launched: "ar_exec_kernel" (the
- * step-table kernel and its flag protocol), "ar_ll_kernel" (one-shot small-message path) or
- * "ar_flat_kernel" (emulated single-step plans); "" before the first call.  Static storage. */
+ * step-table kernel and its flag protocol), "ar_ll_kernel" (one-shot small-message path),
+ * "ar_ll128_kernel" (mid-size two-shot path), "ar_flat_kernel" (emulated single-step plans)
+ * or "nvls_kernel" (NVLS plans); "" before the first call.  Static storage. */
 const char *ar_comm_last_kernel(ar_comm *comm);
 
 /* Largest message (bytes per rank) run through the one-shot small-message path (default the
