@@ -109,6 +109,30 @@ def c2_section(out):
             out.append("")
 
 
+def pick_section(out):
+    """The final build's "GenTree incl. NVLS" column: the min-GenModel pick aware of the
+    executor's one-shot path (gentree_plan_nvls with the OS1 row)."""
+    for n in (4, 2):
+        pk = jl(os.path.join(P, "c2", f"c2pick_n{n}_f32.jsonl"))
+        base = jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
+        ring = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclring.jsonl"))
+        if not pk:
+            continue
+        g = {r["bytes"]: r for r in base if r.get("timing") == "graph" and r["impl"] == "ours" and r["plan"] == "gentree"}
+        nv = {r["bytes"]: r for r in base if r.get("timing") == "graph" and r["impl"] == "ours" and r["plan"] == "nvls"}
+        nr = {r["bytes"]: r for r in ring if r.get("timing") == "graph" and r["impl"] == "nccl"}
+        p = {r["bytes"]: r for r in pk if r.get("timing") == "graph"}
+        out.append(f"**{n} × B200, fp32, graph timing: GenTree incl. NVLS with the one-shot-aware choice (final build)**\n")
+        out.append("| size | pick | pick busbw | GenTree busbw | NVLS busbw | best of the two | pick ÷ best | pick ÷ NCCL Ring |")
+        out.append("|---|---|---|---|---|---|---|---|")
+        for b in sorted(p):
+            best = max(g[b]["busbw_med"], nv[b]["busbw_med"]) if b in g and b in nv else float("nan")
+            out.append(f"| {size(b)} | {p[b]['chosen']} | {p[b]['busbw_med']:.1f} | {g[b]['busbw_med'] if b in g else float('nan'):.1f} | "
+                       f"{nv[b]['busbw_med'] if b in nv else float('nan'):.1f} | {best:.1f} | {p[b]['busbw_med'] / best:.3f} | "
+                       f"{p[b]['busbw_med'] / nr[b]['busbw_med'] if b in nr else float('nan'):.2f} |")
+        out.append("")
+
+
 def fit_section(out):
     for tag, title in (("nvlink_r2", "NVLink ranks (one per GPU), N = 2..4"),
                        ("emulated8_shared", "8 ranks emulated on one GPU (shared HBM, reading A6e)")):
@@ -218,6 +242,7 @@ def main():
            "`COMMANDS.md`.  Round-1 evidence: `../README.md`.\n"]
     bench_section(out)
     c2_section(out)
+    pick_section(out)
     nccl_algo_section(out)
     out.append("## 3. GenModel fit and held-out prediction error\n")
     fit_section(out)
