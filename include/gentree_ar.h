@@ -87,13 +87,14 @@ int genmodel_fit(const gm_measurement *rows, size_t n_rows, int32_t wt_min, int3
 int genmodel_fit_nvls(const gm_measurement *rows, size_t n_rows, gm_params *out, double *sse);
 
 /* The same NNLS for (α, β) on the A and B coefficients of another measured-protocol row:
- * kind "nvls" (= genmodel_fit_nvls) or "oneshot" (reading OS1: the executor's one-shot
- * small-message path, T = α + 2(N−1)S·β).  AR_EINVAL for another kind. */
+ * kind "nvls" (= genmodel_fit_nvls), "oneshot" (reading OS1: the executor's one-shot
+ * small-message path, T = α + 2(N−1)S·β) or "ll128" (the LL128 two-shot path,
+ * T = α + (16/15)·2(N−1)S/N·β).  AR_EINVAL for another kind. */
 int genmodel_fit_row(const char *kind, const gm_measurement *rows, size_t n_rows, gm_params *out, double *sse);
 
 /* Table 2 closed form (readings Q5-Q7) of `kind` ("cps", "ring", "rhd", "rb",
  * "hcps:f0,f1,...", "nvls" = the in-switch row of reading NV1, "oneshot" = the small-message
- * row of reading OS1) for n ranks and `bytes`
+ * row of reading OS1, "ll128" = the mid-size two-shot row) for n ranks and `bytes`
  * per rank, evaluated in the fixed float64 order of DESIGN.md.  Errors: AR_EINVAL for
  * n < 2, unknown kind, bad factorization. */
 int genmodel_closed_form(const char *kind, int32_t n, uint64_t bytes, const gm_params *params,

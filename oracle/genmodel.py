@@ -221,6 +221,14 @@ def closed_form_terms(kind: str, c: int, S: int, w_t: int, fanins: tuple = ()):
         # bytes (B = 2(N-1)S per direction), then reduces all N blocks itself in plan order
         # (C = (N-1)S, D = (N+1)S); every rank receives from N-1 senders (w = N, as CPS).
         return 1, 2 * (c - 1) * S, (c - 1) * S, (c + 1) * S, 2 * (c - 1) * S * max(c - w_t, 0), 1
+    if kind == "ll128":
+        # NOT a paper row: the executor's LL128 two-shot path, a measured-protocol
+        # row like "oneshot".  One round (the flags travel in the data); every rank writes its
+        # N-1 slices of S/N and its result to N-1 peers as 128-byte lines of 120 payload bytes
+        # (B = 2(N-1)S/N · 128/120 per direction), reduces its own block from N inputs (CPS's
+        # C and D), and receives from N-1 senders (w = N, as CPS).  Common denominator 15N.
+        return (1, 32 * (c - 1) * S, 15 * (c - 1) * S, 15 * (c + 1) * S,
+                32 * (c - 1) * S * max(c - w_t, 0), 15 * c)
     raise ValueError(f"no closed form for {kind!r}")
 
 

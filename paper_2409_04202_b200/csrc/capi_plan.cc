@@ -101,7 +101,8 @@ int genmodel_fit_row(const char *kind, const gm_measurement *rows, size_t n_rows
   AR_TRY({
     if (!kind || !rows || !out) throw InvalidArg("null argument");
     const std::string k(kind);
-    if (k != "nvls" && k != "oneshot") throw InvalidArg("genmodel_fit_row: kind must be nvls or oneshot");
+    if (k != "nvls" && k != "oneshot" && k != "ll128")
+      throw InvalidArg("genmodel_fit_row: kind must be nvls, oneshot or ll128");
     std::vector<Measurement> m;
     for (size_t i = 0; i < n_rows; i++) {
       if (rows[i].n < 2 || rows[i].bytes < 1 || !(rows[i].seconds > 0)) throw InvalidArg("bad measurement row");

@@ -856,6 +856,10 @@ static void closed_form_terms(const std::string &kind, int c, int64_t S, int w_t
   } else if (kind == "oneshot") {
     // DESIGN.md reading OS1: the executor's one-shot small-message path
     A = 1; Bn = 2 * cm1 * S; Cn = cm1 * S; Dn = (int64_t)(c + 1) * S; In = 2 * cm1 * S * over; den = 1;
+  } else if (kind == "ll128") {
+    // the executor's LL128 two-shot path: 128-byte lines of 120 payload bytes, one round
+    A = 1; Bn = 32 * cm1 * S; Cn = 15 * cm1 * S; Dn = 15 * (int64_t)(c + 1) * S; In = 32 * cm1 * S * over;
+    den = 15 * (int64_t)c;
   } else {
     throw InvalidArg("no closed form for " + kind);
   }

@@ -391,3 +391,28 @@ def test_executed_fusion_refused_on_hazard():
     P.add_implied_transfers(rs2, c3, n3)
     ag2 = P.Step("ag", "y", [], [P.Transfer(0, 1, 0, 3)])
     assert len(G.executed_steps(P.Plan(n3, c3, [rs2, ag2]))) == 2
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_ll128_row_matches_line_count(n):
+    """The LL128 row (measured-protocol), counted line by line: every rank writes
+    its slice of each of the N-1 other blocks, then its reduced block to each of the N-1 peers,
+    as 128-byte lines carrying 120 payload bytes; it reduces its own block from N inputs."""
+    S = 120 * 16 * n          # bytes per rank: whole lines per block
+    blk = S // n
+    lines = -(-blk // 120)
+    out = [0] * n
+    inn = [0] * n
+    for r in range(n):
+        for o in range(n):
+            if o != r:
+                out[r] += 128 * lines          # RS: my slice of block o -> owner o
+                inn[o] += 128 * lines
+                out[o] += 128 * lines          # AG: owner o's result -> me
+                inn[r] += 128 * lines
+    A, Bn, Cn, Dn, In, den = G.closed_form_terms("ll128", n, S, 1 << 20)
+    assert A == 1 and Fraction(Bn, den) == max(max(out), max(inn))
+    assert Fraction(Cn, den) == Fraction((n - 1) * S, n) and Fraction(Dn, den) == Fraction((n + 1) * S, n)
+    assert In == 0
+    _, _, _, _, In2, den2 = G.closed_form_terms("ll128", n, S, 1)
+    assert Fraction(In2, den2) == (n - 1) * Fraction(Bn, den)

@@ -180,6 +180,19 @@ def test_nvls_row_and_fit_parity():
     assert sse == pytest.approx(o["sse"], rel=1e-6)
 
 
+def test_ll128_row_parity():
+    """The LL128 row: library closed form and fit ≡ oracle."""
+    p = OG.Params(3e-6, 1.5e-12, 0.0, 0.0, 0.0, 1)
+    for n in (2, 3, 4, 8):
+        for S in (4096, 1 << 20, 12345678):
+            same_breakdown(G.genmodel_closed_form("ll128", n, S, lib_params(p)), OG.closed_form_f64("ll128", n, S, p))
+    rows = [(n, s, OG.closed_form_f64("ll128", n, s, p)["total"]) for n in (2, 4) for s in (1 << 20, 1 << 22, 1 << 24)]
+    lp, _ = G.genmodel_fit_row("ll128", rows)
+    o = OF.fit_row("ll128", rows)
+    assert lp.alpha == pytest.approx(o["alpha"], rel=1e-9) and lp.beta == pytest.approx(o["beta"], rel=1e-9)
+    assert lp.alpha == pytest.approx(3e-6, rel=1e-9) and lp.beta == pytest.approx(1.5e-12, rel=1e-9)
+
+
 def test_oneshot_row_and_fit_parity():
     p = OG.Params(4e-6, 1.0e-12, 2e-13, 3e-13, 1e-14, 3)
     for n in (2, 4, 8):
