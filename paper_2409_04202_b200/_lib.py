@@ -105,7 +105,7 @@ _SIGS = {
     "allreduce_exec_nvls": (I32, [P, U64, I32, P]),
     "ar_comm_attach_nvls": (I32, [P, P]),
     "gentree_plan_nvls": (I32, [ctypes.c_char_p, U64, I32, ctypes.POINTER(GmParams), ctypes.POINTER(GmParams),
-                                ctypes.POINTER(GmParams), U64, ctypes.POINTER(P)]),
+                                ctypes.POINTER(GmParams), U64, ctypes.POINTER(GmParams), U64, ctypes.POINTER(P)]),
     "ar_nvls_get_async_error": (I32, [P]),
     "ar_nvls_destroy": (I32, [P]),
     "ar_comm_set_trace": (I32, [P, I32]),

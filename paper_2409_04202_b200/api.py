@@ -107,14 +107,17 @@ class Plan:
     @classmethod
     def from_topology_nvls(cls, topology_json: str, count: int, dtype, params: GmParams,
                            nvls_params: GmParams, oneshot_params: GmParams | None = None,
-                           oneshot_max_bytes: int = 0) -> "Plan":
-        """GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1); with
-        oneshot_params, messages up to oneshot_max_bytes are compared on the one-shot row."""
+                           oneshot_max_bytes: int = 0, ll128_params: GmParams | None = None,
+                           ll128_max_bytes: int = 0) -> "Plan":
+        """GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1); the plan
+        side is predicted on the row of the path the executor takes (one-shot, LL128, steps)."""
         h = ctypes.c_void_p()
         check(lib.gentree_plan_nvls(topology_json.encode(), count, dtype_code(dtype), ctypes.byref(params),
                                     ctypes.byref(nvls_params),
                                     ctypes.byref(oneshot_params) if oneshot_params is not None else None,
-                                    int(oneshot_max_bytes), ctypes.byref(h)))
+                                    int(oneshot_max_bytes),
+                                    ctypes.byref(ll128_params) if ll128_params is not None else None,
+                                    int(ll128_max_bytes), ctypes.byref(h)))
         return cls(h)
 
     @property

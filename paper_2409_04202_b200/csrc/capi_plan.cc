@@ -247,11 +247,12 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
 
 int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
                       const gm_params *nvls_params, const gm_params *oneshot_params, uint64_t oneshot_max_bytes,
-                      gt_plan **out) {
+                      const gm_params *ll128_params, uint64_t ll128_max_bytes, gt_plan **out) {
   AR_TRY({
     if (!topology_json || !nvls_params || !params || !out) throw InvalidArg("null argument");
     check_params(nvls_params);
     if (oneshot_params) check_params(oneshot_params);
+    if (ll128_params) check_params(ll128_params);
     Topology t = parse_topology(topology_json);
     gt_plan *g = nullptr;
     int rc = make_plan(t, count, dtype, params, nullptr, &g);
@@ -267,9 +268,16 @@ int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, 
         return rc;
       }
       const int64_t S = (int64_t)count * esize_of(dtype);
-      if (oneshot_params && (uint64_t)S <= oneshot_max_bytes && !oneshot_order(g->plan).empty()) {
+      const bool eligible = !oneshot_order(g->plan).empty();
+      const int n = g->plan.n;
+      if (oneshot_params && (uint64_t)S <= oneshot_max_bytes && eligible) {
         // the executor runs this plan through its one-shot path: compare that row instead
-        tp = closed_form_f64("oneshot", g->plan.n, S, to_params(oneshot_params), {}).total;
+        tp = closed_form_f64("oneshot", n, S, to_params(oneshot_params), {}).total;
+        use = tn < tp ? 1 : 0;
+      } else if (ll128_params && (uint64_t)S <= ll128_max_bytes && eligible && count % (uint64_t)n == 0 &&
+                 (count / n) * esize_of(dtype) % 16 == 0) {
+        // ... or through its LL128 two-shot path (equal, 16-byte-aligned blocks)
+        tp = closed_form_f64("ll128", n, S, to_params(ll128_params), {}).total;
         use = tn < tp ? 1 : 0;
       }
       if (use) {

@@ -1437,7 +1437,7 @@ struct ar_comm {
   // blocks, ll_max_bytes < message <= ll128_max_bytes (AR_LL128_MAX_KB; 0 = off); its scratch
   // follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
   long long ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
-  int ll128_ctas = 64;
+  int ll128_ctas = 148;
   std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
   // chunked end-to-end path (exec_host_chunked)
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -1945,6 +1945,8 @@ static void init_comm(ar_comm *c) {
     }
   }
   if (const char *v = std::getenv("AR_LL_CTAS")) c->ll_ctas = std::max(1, std::atoi(v));
+  // one CTA per SM: measured best of 32 / 64 / 148 on 2 and 4 B200s (profiles/round2/ll128)
+  c->ll128_ctas = nsm;
   if (const char *v = std::getenv("AR_LL128_CTAS")) c->ll128_ctas = std::max(1, std::atoi(v));
 }
 

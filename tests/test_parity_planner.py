@@ -327,6 +327,12 @@ def test_nvls_plan_kind_parity():
                 lo = G.Plan.from_topology_nvls(doc, count, "f32", lib_params(pp), lib_params(nvp), lib_params(osp), cut)
                 oo, _ = GT.gentree_nvls(t, count, 4, pp, nvp, osp, cut)
                 assert lo.to_json() == OP.plan_to_json(oo, "f32")
+                llp = OG.Params(5.1e-6, 1.74e-12, 0.0, 0.0, 0.0, 1)   # LL128 row
+                for c2 in (count, n * 4 * 4096):                      # ragged / aligned blocks
+                    l2 = G.Plan.from_topology_nvls(doc, c2, "f32", lib_params(pp), lib_params(nvp), lib_params(osp),
+                                                   cut, lib_params(llp), 16 << 20)
+                    o2, _ = GT.gentree_nvls(t, c2, 4, pp, nvp, osp, cut, llp, 16 << 20)
+                    assert l2.to_json() == OP.plan_to_json(o2, "f32")
                 lb = G.Plan.from_topology_nvls(doc, count, "bf16", lib_params(pp), lib_params(nvp))
                 assert not lb.switch_reduce        # bf16 never takes NVLS
         # large messages: the cheap NVLS row ((N+1)/N·0.9 < 2(N-1)/N·1.465 per byte) wins at

@@ -1,0 +1,50 @@
+"""Fit the LL128 row (the executor's mid-size two-shot path) from the rows of
+harness sweeps that ran through it (GenTree plan, equal 16-byte-aligned blocks, one-shot
+cut-off < bytes <= the LL128 maximum), and report its prediction error.
+
+    python tools/fit_ll128.py SWEEP.jsonl [...] [--timing graph] [--max-bytes 16777216]
+
+Writes profiles/genmodel_fit_ll128_<timing>.json."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2409_04202_b200 as G  # noqa: E402
+
+
+def oneshot_cutoff(n):
+    return min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("files", nargs="+")
+    ap.add_argument("--timing", default="graph")
+    ap.add_argument("--max-bytes", type=int, default=16 << 20)
+    a = ap.parse_args()
+    rows = []
+    for f in a.files:
+        rows += [json.loads(l) for l in open(f) if l.startswith("{")]
+    sel = [r for r in rows if r.get("timing") == a.timing and r["plan"] == "gentree" and r.get("impl", "ours") == "ours"
+           and oneshot_cutoff(r["n"]) < r["bytes"] <= a.max_bytes and r["bytes"] % (r["n"] * 16) == 0]
+    fit_rows = [(r["n"], r["bytes"], r["t_mean"]) for r in sel]
+    p, sse = G.genmodel_fit_row("ll128", fit_rows)
+    errs = []
+    for r in sel:
+        pred = G.genmodel_closed_form("ll128", r["n"], r["bytes"], p)["total"]
+        errs.append({"n": r["n"], "bytes": r["bytes"], "measured_s": r["t_mean"], "predicted_s": pred,
+                     "rel_err": abs(pred - r["t_mean"]) / r["t_mean"]})
+    e = sorted(x["rel_err"] for x in errs)
+    out = {"timing": a.timing, "rows": len(errs), "alpha": p.alpha, "beta": p.beta,
+           "line_gbs": 1 / p.beta / 1e9 if p.beta > 0 else None, "sse": sse, "max_bytes": a.max_bytes,
+           "pred_err_median": e[len(e) // 2], "pred_err_max": e[-1], "points": errs, "sources": a.files}
+    json.dump(out, open(os.path.join(ROOT, "profiles", f"genmodel_fit_ll128_{a.timing}.json"), "w"), indent=1)
+    print(json.dumps({k: v for k, v in out.items() if k not in ("points", "sources")}, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -35,6 +35,7 @@ def main():
     pj = json.load(open(os.path.join(P, "genmodel_params.json")))
     nj = json.load(open(os.path.join(P, "genmodel_params_nvls.json")))
     oj = json.load(open(os.path.join(P, "genmodel_fit_oneshot_graph.json")))
+    lj = json.load(open(os.path.join(P, "genmodel_fit_ll128_graph.json")))
     gp = G.params(pj["alpha"], pj["beta"], pj["gamma"], pj["delta"], pj["epsilon"], pj["w_t"])
     npar = G.params(alpha=nj["alpha"], beta=nj["beta"])
     ll_max = min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256   # executor default (exec.cu, init_comm)
@@ -45,9 +46,13 @@ def main():
         plan = G.Plan.single_switch(n, count, "f32", gp)
         kind = plan.report()[-1]["chosen"]
         op = G.params(alpha=oj["alpha"], beta=oj["beta"])
+        lp = G.params(alpha=lj["alpha"], beta=lj["beta"])
         if nbytes <= ll_max:
             t_plan = G.genmodel_closed_form("oneshot", n, nbytes, op)["total"]
             path = "one-shot"
+        elif nbytes <= lj["max_bytes"] and count % n == 0 and (count // n) * 4 % 16 == 0:
+            t_plan = G.genmodel_closed_form("ll128", n, nbytes, lp)["total"]
+            path = "LL128 two-shot"
         else:
             t_plan = plan.predict_executed(gp)["total"]
             path = f"{kind} (executed steps)"
@@ -56,7 +61,7 @@ def main():
             {"id": f"s{i}", "kind": "server", "parent": "sw",
              "uplink": {"alpha": 0, "beta": 1, "epsilon": 0, "w_t": 1}, "compute": {"gamma": 0, "delta": 0}}
             for i in range(n)]})
-        pick = G.Plan.from_topology_nvls(doc, count, "f32", gp, npar, op, ll_max)
+        pick = G.Plan.from_topology_nvls(doc, count, "f32", gp, npar, op, ll_max, lp, lj["max_bytes"])
         t_pick = c["t_nvls"] if pick.switch_reduce else t_plan
         rows.append({"bytes": nbytes, "gentree_plan": kind, "path": path, "t_pred_s": t_plan,
                      "busbw_pred": round(busbw(nbytes, n, t_plan), 1), "t_nvls_pred_s": c["t_nvls"],
@@ -65,6 +70,7 @@ def main():
                      "pick_busbw_pred": round(busbw(nbytes, n, t_pick), 1)})
     out = {"tool": "predict8", "world": n, "dtype": "f32", "kind": "GenModel prediction, not a measurement",
            "params": pj["source"], "nvls_params": nj["source"], "oneshot_params": "genmodel_fit_oneshot_graph.json",
+           "ll128_params": "genmodel_fit_ll128_graph.json",
            "oneshot_max_bytes": ll_max,
            "fit_range": "parameters fitted on CPS rows at N = 2..4 (w_t >= 4, eps = 0: no incast seen up to the 4-GPU lease)",
            "context": "NCCL 8-rank all-reduce busbw 725 GB/s at 1 GiB on B200 (B200_PROFILING.md)",
