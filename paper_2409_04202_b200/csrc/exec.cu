@@ -1437,7 +1437,7 @@ struct ar_comm {
   // blocks, ll_max_bytes < message <= ll128_max_bytes (AR_LL128_MAX_KB; 0 = off); its scratch
   // follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
   long long ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
-  int ll128_ctas = 148;
+  int ll128_ctas = 296;
   std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
   // chunked end-to-end path (exec_host_chunked)
   cudaStream_t h2d = nullptr, d2h = nullptr;
@@ -1945,8 +1945,8 @@ static void init_comm(ar_comm *c) {
     }
   }
   if (const char *v = std::getenv("AR_LL_CTAS")) c->ll_ctas = std::max(1, std::atoi(v));
-  // one CTA per SM: measured best of 32 / 64 / 148 on 2 and 4 B200s (profiles/round2/ll128)
-  c->ll128_ctas = nsm;
+  // two CTAs per SM: measured best of 32 / 64 / 148 / 296 on 2 and 4 B200s (profiles/round2/ll128)
+  c->ll128_ctas = 2 * nsm;
   if (const char *v = std::getenv("AR_LL128_CTAS")) c->ll128_ctas = std::max(1, std::atoi(v));
 }
 
@@ -2520,7 +2520,10 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       la.err = c->err;
       la.timeout_ns = c->timeout_ns;
       const long long warps_needed = (la.lines + 3) / 4;
-      const int ctas = (int)std::max(1LL, std::min<long long>(c->ll128_ctas, (warps_needed + 15) / 16));
+      // at most two CTAs per step-table CTA: ar_comm_set_ctas is the caller's share of the GPU
+      // (e.g. several ranks' communicators on one GPU must all be resident at once)
+      const long long cap = std::min<long long>(c->ll128_ctas, 2LL * c->nctas);
+      const int ctas = (int)std::max(1LL, std::min<long long>(cap, (warps_needed + 15) / 16));
       if (plan->esize == 2) ar_ll128_kernel<true><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
       else ar_ll128_kernel<false><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
       CUDA_OK(cudaGetLastError());

@@ -77,9 +77,12 @@ def nccl_algo_section(out):
 
 
 def c2_section(out):
-    out.append("## 2. C2: fp32 busbw vs size — GenTree, GenTree incl. NVLS (min-GenModel pick), NCCL default / Ring / NVLS-off\n")
+    out.append("## 2. C2: fp32 busbw vs size — GenTree, GenTree incl. NVLS (path-aware min-GenModel pick), NCCL default / Ring / NVLS-off\n")
+    out.append("Our columns and NCCL default: the final executor (`final_c2_*`: one-shot ≤ 1.5 MiB/(N−1), LL128 two-shot to"
+               " 16 MiB, step-table kernel above); NCCL Ring / NVLS-off: separate processes with the variable set"
+               " (`c2_*_ncclring`, `c2_*_ncclnvlsoff`).  The first C2 run, before the LL128 path, is `c2_n*_f32.jsonl`.\n")
     for n in (4, 2):
-        ours = jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
+        ours = jl(os.path.join(P, "c2", f"final_c2_n{n}_f32.jsonl")) or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
         if not ours:
             continue
         ring = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclring.jsonl"))
@@ -110,19 +113,21 @@ def c2_section(out):
 
 
 def pick_section(out):
-    """The final build's "GenTree incl. NVLS" column: the min-GenModel pick aware of the
-    executor's one-shot path (gentree_plan_nvls with the OS1 row)."""
+    """The final build's "GenTree incl. NVLS" column: the min-GenModel pick with the plan side
+    predicted on the row of the path the executor takes (gentree_plan_nvls with the OS1 and
+    LL128 rows)."""
     for n in (4, 2):
-        pk = jl(os.path.join(P, "c2", f"c2pick_n{n}_f32.jsonl"))
-        base = jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
+        final = jl(os.path.join(P, "c2", f"final_c2_n{n}_f32.jsonl"))
+        pk = [r for r in final if r.get("plan") == "gentree+nvls"] or jl(os.path.join(P, "c2", f"c2pick_n{n}_f32.jsonl"))
+        base = final or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
         ring = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclring.jsonl"))
         if not pk:
             continue
         g = {r["bytes"]: r for r in base if r.get("timing") == "graph" and r["impl"] == "ours" and r["plan"] == "gentree"}
         nv = {r["bytes"]: r for r in base if r.get("timing") == "graph" and r["impl"] == "ours" and r["plan"] == "nvls"}
         nr = {r["bytes"]: r for r in ring if r.get("timing") == "graph" and r["impl"] == "nccl"}
-        p = {r["bytes"]: r for r in pk if r.get("timing") == "graph"}
-        out.append(f"**{n} × B200, fp32, graph timing: GenTree incl. NVLS with the one-shot-aware choice (final build)**\n")
+        p = {r["bytes"]: r for r in pk if r.get("timing") == "graph" and r.get("impl", "ours") == "ours"}
+        out.append(f"**{n} × B200, fp32, graph timing: GenTree incl. NVLS, the plan side predicted on the path the executor takes (one-shot / LL128 / steps)**\n")
         out.append("| size | pick | pick busbw | GenTree busbw | NVLS busbw | best of the two | pick ÷ best | pick ÷ NCCL Ring |")
         out.append("|---|---|---|---|---|---|---|---|")
         for b in sorted(p):
@@ -159,6 +164,31 @@ def fit_section(out):
             out.append(f"(α,β,γ) model on the same rows: median {d['abc_err']['median']:.3f}, max {d['abc_err']['max']:.3f}; "
                        f"GenModel on the paper's unfused steps: median {d['genmodel_paper_steps_err']['median']:.3f}, "
                        f"max {d['genmodel_paper_steps_err']['max']:.3f}.")
+        out.append("")
+
+
+def ll128_section(out):
+    d = os.path.join(P, "ll128")
+    if not os.path.isdir(d):
+        return
+    out.append("## 2c. LL128 two-shot path vs the step-table kernel (CPS plan, fp32, graph timing, busbw GB/s)\n")
+    out.append("`off` = AR_LL128_MAX_KB=0 (flag protocol); `cN` = the LL128 path with N CTAs (148 = one per SM,"
+               " the default); 512 KiB at N = 4 and ≤ 1 MiB at N = 2 run the one-shot path in every column.\n")
+    for n in (4, 2):
+        def load(f):
+            return {r["bytes"]: r for r in jl(os.path.join(d, f)) if r.get("timing") == "graph" and r.get("impl") == "ours"}
+        off = load(f"off_n{n}.jsonl")
+        cs = {c: load(f"on_n{n}_c{c}.jsonl") for c in (32, 64, 148)}
+        c296 = {r["bytes"]: r for r in jl(os.path.join(P, "c2", f"ll296_n{n}.jsonl")) if r.get("timing") == "graph"}
+        if not off:
+            continue
+        out.append(f"**{n} × B200**\n")
+        out.append("| size | off | c32 | c64 | c148 | c296 | c148 ÷ off |")
+        out.append("|---|---|---|---|---|---|---|")
+        for b in sorted(off):
+            v = [off[b]["busbw_med"]] + [cs[c][b]["busbw_med"] if b in cs[c] else float("nan") for c in (32, 64, 148)]
+            v.append(c296[b]["busbw_med"] if b in c296 else float("nan"))
+            out.append(f"| {size(b)} | " + " | ".join(f"{x:.1f}" for x in v) + f" | {v[3] / v[0]:.2f} |")
         out.append("")
 
 
@@ -243,6 +273,7 @@ def main():
     bench_section(out)
     c2_section(out)
     pick_section(out)
+    ll128_section(out)
     nccl_algo_section(out)
     out.append("## 3. GenModel fit and held-out prediction error\n")
     fit_section(out)
