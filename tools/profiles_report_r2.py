@@ -112,6 +112,27 @@ def c2_section(out):
             out.append("")
 
 
+def bf16_section(out):
+    rows4 = jl(os.path.join(P, "c2", "final_c2_n4_bf16.jsonl"))
+    if not rows4:
+        return
+    out.append("**bf16, graph timing, final executor: GenTree plan vs NCCL default (busbw GB/s)**\n")
+    out.append("| size | GenTree N=4 | NCCL N=4 | ratio | GenTree N=2 | NCCL N=2 | ratio |")
+    out.append("|---|---|---|---|---|---|---|")
+    d = {}
+    for n in (4, 2):
+        rows = jl(os.path.join(P, "c2", f"final_c2_n{n}_bf16.jsonl"))
+        d[n] = ({r["bytes"]: r["busbw_med"] for r in rows if r["impl"] == "ours"},
+                {r["bytes"]: r["busbw_med"] for r in rows if r["impl"] == "nccl"})
+    for b in sorted(d[4][0]):
+        cells = []
+        for n in (4, 2):
+            g, c = d[n]
+            cells += [f"{g.get(b, float('nan')):.1f}", f"{c.get(b, float('nan')):.1f}", f"{g.get(b, float('nan')) / c.get(b, float('nan')):.2f}"]
+        out.append(f"| {size(b)} | " + " | ".join(cells) + " |")
+    out.append("")
+
+
 def pick_section(out):
     """The final build's "GenTree incl. NVLS" column: the min-GenModel pick with the plan side
     predicted on the row of the path the executor takes (gentree_plan_nvls with the OS1 and
@@ -272,6 +293,7 @@ def main():
            "`COMMANDS.md`.  Round-1 evidence: `../README.md`.\n"]
     bench_section(out)
     c2_section(out)
+    bf16_section(out)
     pick_section(out)
     ll128_section(out)
     nccl_algo_section(out)
