@@ -1142,7 +1142,6 @@ struct LL128Args {
   unsigned long long timeout_ns;
 };
 constexpr int kLineBytes = 128, kLinePayload = 120;
-constexpr int kLL128MaxRanks = 8;       // ranks of one NVSwitch box; larger worlds use the step-table kernel
 
 __device__ __forceinline__ void st_vol_v2u64(void *p, unsigned long long a, unsigned long long b) {
   asm volatile("st.volatile.global.v2.u64 [%0], {%1,%2};" ::"l"(p), "l"(a), "l"(b) : "memory");
@@ -1168,6 +1167,26 @@ __device__ __forceinline__ void ll128_store_payload(char *blk, long long blk_byt
   if (o + 8 <= blk_bytes) *(unsigned long long *)(blk + o) = w0;
   if (j < 7 && o + 16 <= blk_bytes) *(unsigned long long *)(blk + o + 8) = w1;
 }
+// Load line i from a scratch slot until its flag (lane 7 of the 8-lane group, second word)
+// equals `flag`.  Every lane of the warp runs the loop (__any_sync); lanes without a line
+// (live == false) count as valid.
+__device__ __forceinline__ bool ll128_load(const char *line, int j, bool live, unsigned long long flag,
+                                           unsigned long long &w0, unsigned long long &w1,
+                                           const LL128Args &a, unsigned long long start) {
+  const int lane = threadIdx.x & 31;
+  unsigned int spins = 0;
+  for (;;) {
+    if (live) ld_vol_v2u64(line + 16 * j, w0, w1);
+    const unsigned long long f = __shfl_sync(0xffffffffu, w1, (lane & ~7) | 7);
+    const bool bad = live && f != flag;
+    if (!__any_sync(0xffffffffu, bad)) return true;
+    if ((++spins & 1023u) == 0 && globaltimer() - start > a.timeout_ns) {
+      atomicExch(a.err, 1ull);
+      return false;
+    }
+  }
+}
+
 template <bool BF16>
 __device__ __forceinline__ void ll128_acc(float (&acc)[8], unsigned long long w0, unsigned long long w1, bool first) {
   const uint32_t u[4] = {(uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32)};
@@ -1191,8 +1210,8 @@ __device__ __forceinline__ void ll128_pack(const float (&acc)[8], unsigned long 
   w1 = (unsigned long long)u[2] | ((unsigned long long)u[3] << 32);
 }
 
-template <bool BF16, int MAXQ>
-__global__ void __launch_bounds__(kThreads, 2) ar_ll128_kernel(const __grid_constant__ LL128Args a) {
+template <bool BF16>
+__global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constant__ LL128Args a) {
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
   __syncthreads();
@@ -1217,47 +1236,21 @@ __global__ void __launch_bounds__(kThreads, 2) ar_ll128_kernel(const __grid_cons
       st_vol_v2u64(dst + i * kLineBytes + 16 * j, w0, j == 7 ? epoch : w1);
     }
   }
-  // 2. reduce my block in the plan's order; result to my buffer and every peer's AG area.
-  // The N-1 incoming lines of a line index are loaded together (memory-level parallelism),
-  // then validated; only the lines whose flag has not arrived are loaded again.
+  // 2. reduce my block in the plan's order; result to my buffer and every peer's AG area
   {
     char *blk = a.buf + (long long)a.me * a.blk_bytes;
     for (long long it = 0; it < iters; it++) {
       const long long i = (it * nwarps + gwarp) * 4 + sub;
       const bool live = i < L;
-      unsigned long long v0[MAXQ], v1[MAXQ];
-      unsigned int need = 0;
-#pragma unroll
-      for (int k = 0; k < MAXQ; k++) {
-        v0[k] = v1[k] = 0ull;
-        if (k < a.world && a.order[k] != a.me) need |= 1u << k;
-      }
-      unsigned int spins = 0;
-      while (need) {
-#pragma unroll
-        for (int k = 0; k < MAXQ; k++)
-          if (((need >> k) & 1u) && live)
-            ld_vol_v2u64(ll128_line(a.my_scr, a, par, 0, a.order[k], i) + 16 * j, v0[k], v1[k]);
-        unsigned int bad = 0;
-#pragma unroll
-        for (int k = 0; k < MAXQ; k++) {
-          const unsigned long long f = __shfl_sync(0xffffffffu, v1[k], (lane & ~7) | 7);
-          if (((need >> k) & 1u) && live && f != epoch) bad |= 1u << k;
-        }
-        need = __reduce_or_sync(0xffffffffu, bad);
-        if (need && (++spins & 1023u) == 0 && globaltimer() - start > a.timeout_ns) {
-          atomicExch(a.err, 1ull);
-          break;
-        }
-      }
       float acc[8];
-#pragma unroll
-      for (int k = 0; k < MAXQ; k++) {
-        if (k >= a.world) break;
-        unsigned long long w0 = v0[k], w1 = j == 7 ? 0ull : v1[k];   // lane 7's second word is the flag
-        if (a.order[k] == a.me) {
-          w0 = w1 = 0ull;
+      for (int k = 0; k < a.world; k++) {
+        const int q = a.order[k];
+        unsigned long long w0 = 0, w1 = 0;
+        if (q == a.me) {
           if (live) ll128_payload(blk, a.blk_bytes, i, j, w0, w1);
+        } else {
+          ll128_load(ll128_line(a.my_scr, a, par, 0, q, live ? i : 0), j, live, epoch, w0, w1, a, start);
+          if (j == 7) w1 = 0ull;   // the flag word carries no payload
         }
         ll128_acc<BF16>(acc, w0, w1, k == 0);
       }
@@ -1273,39 +1266,17 @@ __global__ void __launch_bounds__(kThreads, 2) ar_ll128_kernel(const __grid_cons
       }
     }
   }
-  // 3. gather the other owners' results (all owners' lines of a line index loaded together)
-  for (long long it = 0; it < iters; it++) {
-    const long long i = (it * nwarps + gwarp) * 4 + sub;
-    const bool live = i < L;
-    unsigned long long v0[MAXQ], v1[MAXQ];
-    unsigned int need = 0;
-#pragma unroll
-    for (int o = 0; o < MAXQ; o++) {
-      v0[o] = v1[o] = 0ull;
-      if (o < a.world && o != a.me) need |= 1u << o;
+  // 3. gather the other owners' results
+  for (int o = 0; o < a.world; o++) {
+    if (o == a.me) continue;
+    char *blk = a.buf + (long long)o * a.blk_bytes;
+    for (long long it = 0; it < iters; it++) {
+      const long long i = (it * nwarps + gwarp) * 4 + sub;
+      const bool live = i < L;
+      unsigned long long w0 = 0, w1 = 0;
+      ll128_load(ll128_line(a.my_scr, a, par, 1, o, live ? i : 0), j, live, epoch, w0, w1, a, start);
+      if (live) ll128_store_payload(blk, a.blk_bytes, i, j, w0, w1);
     }
-    unsigned int spins = 0;
-    while (need) {
-#pragma unroll
-      for (int o = 0; o < MAXQ; o++)
-        if (((need >> o) & 1u) && live) ld_vol_v2u64(ll128_line(a.my_scr, a, par, 1, o, i) + 16 * j, v0[o], v1[o]);
-      unsigned int bad = 0;
-#pragma unroll
-      for (int o = 0; o < MAXQ; o++) {
-        const unsigned long long f = __shfl_sync(0xffffffffu, v1[o], (lane & ~7) | 7);
-        if (((need >> o) & 1u) && live && f != epoch) bad |= 1u << o;
-      }
-      need = __reduce_or_sync(0xffffffffu, bad);
-      if (need && (++spins & 1023u) == 0 && globaltimer() - start > a.timeout_ns) {
-        atomicExch(a.err, 1ull);
-        break;
-      }
-    }
-    if (!live) continue;
-#pragma unroll
-    for (int o = 0; o < MAXQ; o++)
-      if (o < a.world && o != a.me)
-        ll128_store_payload(a.buf + (long long)o * a.blk_bytes, a.blk_bytes, i, j, v0[o], v1[o]);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1466,7 +1437,7 @@ struct ar_comm {
   // blocks, ll_max_bytes < message <= ll128_max_bytes (AR_LL128_MAX_KB; 0 = off); its scratch
   // follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
   long long ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
-  int ll128_per_sm = 1;        // resident ar_ll128_kernel CTAs per SM (all CTAs must be resident)
+  int ll128_per_sm = 1;        // resident ar_ll128_kernel CTAs per SM
   int ll128_ctas = 296;
   std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
   // chunked end-to-end path (exec_host_chunked)
@@ -1975,17 +1946,15 @@ static void init_comm(ar_comm *c) {
     }
   }
   if (const char *v = std::getenv("AR_LL_CTAS")) c->ll_ctas = std::max(1, std::atoi(v));
-  // two CTAs per SM: measured best of 32 / 64 / 148 / 296 on 2 and 4 B200s (profiles/round2/ll128).
-  // Every CTA of every rank must be resident at once (a resident CTA may wait for lines a
-  // not-yet-scheduled CTA of a peer would write), so the grid never exceeds the occupancy.
+  // two CTAs per SM: measured best of 32 / 64 / 148 / 296 on 2 and 4 B200s (profiles/round2/ll128;
+  // a variant batching the loads of the N-1 incoming lines measured 0-6 % slower: not kept)
   {
-    int per = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_ll128_kernel<false, 8>, kThreads, 0));
-    int per4 = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per4, ar_ll128_kernel<true, 4>, kThreads, 0));
-    c->ll128_per_sm = std::max(1, std::min(per, per4));
+    int per = 0, per2 = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_ll128_kernel<false>, kThreads, 0));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, ar_ll128_kernel<true>, kThreads, 0));
+    c->ll128_per_sm = std::max(1, std::min(per, per2));
   }
-  c->ll128_ctas = c->ll128_per_sm * nsm;
+  c->ll128_ctas = std::min(2, c->ll128_per_sm) * nsm;
   if (const char *v = std::getenv("AR_LL128_CTAS")) c->ll128_ctas = std::max(1, std::atoi(v));
 }
 
@@ -2535,7 +2504,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       return AR_OK;
     }
   }
-  if (c->ll_opened && c->ll128_max_bytes > 0 && c->world <= kLL128MaxRanks && (long long)nbytes_call > c->ll_max_bytes &&
+  if (c->ll_opened && c->ll128_max_bytes > 0 && c->world <= 8 && (long long)nbytes_call > c->ll_max_bytes &&
       (long long)nbytes_call <= c->ll128_max_bytes && count % (uint64_t)c->world == 0 &&
       (count / c->world) * plan->esize % 16 == 0) {
     // LL128 two-shot path for CPS-shaped plans with equal 16-byte-aligned blocks (ar_ll128_kernel)
@@ -2559,18 +2528,13 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       la.err = c->err;
       la.timeout_ns = c->timeout_ns;
       const long long warps_needed = (la.lines + 3) / 4;
-      // at most two CTAs per step-table CTA: ar_comm_set_ctas is the caller's share of the GPU
-      // (e.g. several ranks' communicators on one GPU must all be resident at once)
+      // every CTA of every rank must be resident at once (a resident CTA may wait for lines a
+      // not-yet-scheduled CTA of a peer would write): at most the kernel's occupancy per SM times
+      // the caller's share of the GPU (ar_comm_set_ctas; several ranks' comms on one GPU)
       const long long cap = std::min<long long>(c->ll128_ctas, (long long)c->ll128_per_sm * c->nctas);
       const int ctas = (int)std::max(1LL, std::min<long long>(cap, (warps_needed + 15) / 16));
-      // arrays of the batched line loads sized for the world (registers: 2 CTAs per SM)
-      if (c->world <= 4) {
-        if (plan->esize == 2) ar_ll128_kernel<true, 4><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
-        else ar_ll128_kernel<false, 4><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
-      } else {
-        if (plan->esize == 2) ar_ll128_kernel<true, 8><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
-        else ar_ll128_kernel<false, 8><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
-      }
+      if (plan->esize == 2) ar_ll128_kernel<true><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      else ar_ll128_kernel<false><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
       c->last_kernel = "ar_ll128_kernel";
