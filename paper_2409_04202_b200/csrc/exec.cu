@@ -475,11 +475,9 @@ __device__ __noinline__ void body_bulk_st(const OpShared &s, size_t v0, size_t v
         }
       }
     }
-    if (storer) {
-      // the writes must be complete before this CTA releases its flags
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
+    // no drain here: the caller completes this CTA's bulk stores (bulk_store_drain) once per
+    // step, before its flags are released — consecutive ops of a step then overlap their
+    // store completion with the next op's loads
   }
   g += ntiles;
 }
@@ -562,12 +560,19 @@ __device__ __noinline__ void body_bulk_st_dyn(const OpShared &s, size_t v0, size
         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
       }
     }
-    if (storer) {
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
+    // completed by the caller (bulk_store_drain), as in body_bulk_st
   }
   g += used;
+}
+
+// Complete every bulk store this CTA's storer thread (threadIdx.x == 32) issued and order them
+// before later generic-proxy operations: called once per step before the step's flags are
+// released (the bar.sync of the notify then makes it cumulative), and before a kernel exits.
+__device__ __forceinline__ void bulk_store_drain() {
+  if (threadIdx.x == 32) {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
 }
 
 template <bool BF16>
@@ -789,6 +794,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       if (cta == 0 && vb * 16 > b0) scalar_elems(sh, op.off, vb * vec_elems, bf16);
       if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(sh, ve * vec_elems, op.off + op.len, bf16);
     }
+    if (st.op_count > 0 && a.bulk && a.store_tma) bulk_store_drain();
     AR_TRACE(2 + 3 * si);
     // ---- notify (release our slot on every consumer's page)
     if (st.notify_count > 0) {
@@ -944,6 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_const
         }
       }
     }
+    bulk_store_drain();
     __syncthreads();
     if (threadIdx.x == 0 && atomicAdd(a.ctr + a.world, 1u) == gridDim.x - 1)
       for (int i = 0; i <= a.world; i++) a.ctr[i] = 0u;   // every CTA is past every block
@@ -987,6 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_const
     }
     acc += nv;
   }
+  bulk_store_drain();
 }
 
 // ------------------------------------------------------------------ low-latency one-shot path
