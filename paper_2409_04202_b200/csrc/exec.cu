@@ -287,7 +287,7 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
 constexpr int kMaxStages = 8;
 constexpr int kDefStages = 4;
 constexpr int kDefStageBytes = 40 * 1024;
-constexpr int kMaxDynSmem = 224 * 1024;   // 227 KB per block minus the static shared state
+constexpr int kMaxDynSmem = 220 * 1024;   // 227 KB per block minus the static shared state
 // dynamic smem: stages x stage_bytes input ring + 2 output tiles of stage_bytes / 2
 inline int dyn_smem_bytes(int stages, int stage_bytes) { return (stages + 1) * stage_bytes; }
 
@@ -691,7 +691,6 @@ __device__ __forceinline__ unsigned long long *flag_ptr(const ExecArgs &a, int p
 }
 
 __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_constant__ ExecArgs a) {
-  __shared__ OpShared sh;
   __shared__ Pipe pp;
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   const int lr = blockIdx.y;
@@ -714,6 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
   // op overlap inside a step (bulk loads + bulk stores, the default): two op-descriptor slots
   __shared__ OpShared shq[2];
+  OpShared &sh = shq[0];   // the barrier-per-op path (AR_OP_OVERLAP=0 and non-bulk bodies)
   __shared__ unsigned long long op_ready[2], op_done[2];
   const bool overlap = a.bulk && a.store_tma && a.op_overlap;
   uint32_t kop = 0;   // ops started so far (identical in every thread)
