@@ -95,7 +95,6 @@ struct ExecArgs {
   unsigned int *dyn_ctr;     // nullptr = static per-CTA slices
   int dyn_nops;
   int entry_fence;           // 1 = fence.acq_rel.sys before the relaxed entry flags (AR_ENTRY_FENCE)
-  int op_overlap;            // 1 = consecutive ops of a step overlap (AR_OP_OVERLAP=0: barrier per op)
 };
 
 // Buffer references in op rank lists: r < kScrRef is rank r's data buffer; kScrRef + o·64 + s
@@ -287,7 +286,7 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
 constexpr int kMaxStages = 8;
 constexpr int kDefStages = 4;
 constexpr int kDefStageBytes = 40 * 1024;
-constexpr int kMaxDynSmem = 220 * 1024;   // 227 KB per block minus the static shared state
+constexpr int kMaxDynSmem = 224 * 1024;   // 227 KB per block minus the static shared state
 // dynamic smem: stages x stage_bytes input ring + 2 output tiles of stage_bytes / 2
 inline int dyn_smem_bytes(int stages, int stage_bytes) { return (stages + 1) * stage_bytes; }
 
@@ -691,6 +690,7 @@ __device__ __forceinline__ unsigned long long *flag_ptr(const ExecArgs &a, int p
 }
 
 __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_constant__ ExecArgs a) {
+  __shared__ OpShared sh;
   __shared__ Pipe pp;
   extern __shared__ __align__(128) uint8_t dyn_smem[];
   const int lr = blockIdx.y;
@@ -711,22 +711,12 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   // every CTA reads the same value and the launch carries no per-call host argument
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
-  // op overlap inside a step (bulk loads + bulk stores, the default): two op-descriptor slots
-  __shared__ OpShared shq[2];
-  OpShared &sh = shq[0];   // the barrier-per-op path (AR_OP_OVERLAP=0 and non-bulk bodies)
-  __shared__ unsigned long long op_ready[2], op_done[2];
-  const bool overlap = a.bulk && a.store_tma && a.op_overlap;
-  uint32_t kop = 0;   // ops started so far (identical in every thread)
   if (a.bulk && threadIdx.x == 0) {
     pp.stages = a.stages;
     pp.stage_bytes = a.stage_bytes;
     for (int s = 0; s < a.stages; s++) {
       mbar_init(&pp.full[s], 1);
       mbar_init(&pp.empty[s], a.store_tma ? 1 : blockDim.x / 32 - 1);
-    }
-    for (int b = 0; b < 2; b++) {
-      mbar_init(&op_ready[b], 1);
-      mbar_init(&op_done[b], blockDim.x - 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -759,56 +749,13 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
       }
       __syncthreads();
       // the bulk loads below run in the async proxy: order them after the generic-proxy
-      // writes this acquire made visible
-      asm volatile("fence.proxy.async.global;" ::: "memory");
+      // writes this acquire made visible.  Only their issuer (thread 0, the bulk producer)
+      // needs the proxy fence — executed by all 512 threads it was the kernel's top stall
+      // (ncu, RHD on 8 emulated ranks: 12 % of the warp samples)
+      if (!a.bulk || threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     AR_TRACE(1 + 3 * si);
     // ---- ops (a2 / a4)
-    if (overlap) {
-      // Ops of a step run back to back without CTA-wide barriers: thread 0 (the bulk producer)
-      // fills the op descriptor of op k into shq[k & 1] and starts its loads while the other
-      // warps still finish op k-1; op_ready / op_done mbarriers hand the two descriptor slots
-      // over.  The ops of one step touch disjoint regions (no intra-step hazard), so only the
-      // slots need ordering.
-      for (int oi = 0; oi < st.op_count; oi++, kop++) {
-        const DevOp op = a.ops[st.op_begin + oi];
-        const int b = kop & 1;
-        const uint32_t use = kop >> 1;
-        if (threadIdx.x == 0) {
-          if (use > 0) mbar_wait(&op_done[b], (use - 1) & 1);
-          const int *sr = a.ranks + op.src_begin;
-          const int *dr = a.ranks + op.dst_begin;
-          for (int i = 0; i < op.nsrc; i++) shq[b].src[i] = (const uint4 *)ref_base(a, sr[i], op.off, epoch);
-          for (int i = 0; i < op.ndst; i++) shq[b].dst[i] = (uint4 *)ref_base(a, dr[i], op.off, epoch);
-          shq[b].nsrc = op.nsrc;
-          shq[b].ndst = op.ndst;
-          shq[b].div = op.fin ? a.avg_n : 0;
-          mbar_arrive(&op_ready[b]);
-        } else {
-          mbar_wait(&op_ready[b], use & 1);
-        }
-        const OpShared &so = shq[b];
-        const long long b0 = op.off * a.esize, b1 = (op.off + op.len) * a.esize;
-        const long long vb = (b0 + 15) / 16, ve = b1 / 16;
-        if (vb >= ve) {
-          if (cta == 0) scalar_elems(so, op.off, op.off + op.len, bf16);
-        } else {
-          const long long nv = ve - vb;
-          const size_t v0 = (size_t)(vb + nv * cta / nctas), v1 = (size_t)(vb + nv * (cta + 1) / nctas);
-          if (a.dyn_ctr && op.nsrc >= 2 && op.nsrc <= 8) {
-            unsigned int *ctr = a.dyn_ctr + st.op_begin + oi;
-            if (bf16) body_dispatch_bulk_st_dyn<true>(so, (size_t)vb, (size_t)ve, g, dyn_smem, pp, ctr);
-            else body_dispatch_bulk_st_dyn<false>(so, (size_t)vb, (size_t)ve, g, dyn_smem, pp, ctr);
-          } else {
-            if (bf16) body_dispatch_bulk_st<true>(so, v0, v1, g, dyn_smem, pp);
-            else body_dispatch_bulk_st<false>(so, v0, v1, g, dyn_smem, pp);
-          }
-          if (cta == 0 && vb * 16 > b0) scalar_elems(so, op.off, vb * vec_elems, bf16);
-          if (cta == nctas - 1 && ve * 16 < b1) scalar_elems(so, ve * vec_elems, op.off + op.len, bf16);
-        }
-        if (threadIdx.x != 0) mbar_arrive(&op_done[b]);
-      }
-    } else
     for (int oi = 0; oi < st.op_count; oi++) {
       const DevOp op = a.ops[st.op_begin + oi];
       const int *sr = a.ranks + op.src_begin;
@@ -1513,7 +1460,6 @@ struct ar_comm {
   char *checked_base = nullptr;                // local comms: last buffer extent validated
   size_t checked_need = 0;
   bool entry_fence = false;                    // AR_ENTRY_FENCE=1: fence.acq_rel.sys before relaxed entry flags
-  bool op_overlap = true;                      // AR_OP_OVERLAP=0: a CTA barrier between the ops of a step
   ar_nvls *nvls = nullptr;                     // NVLS buffer for switch_reduce plans (ar_comm_attach_nvls)
 };
 
@@ -1981,7 +1927,6 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_FLAT")) c->flat = std::string(v) != "0";
   if (const char *v = std::getenv("AR_DYN")) c->dyn = std::string(v) != "0";
   if (const char *v = std::getenv("AR_ENTRY_FENCE")) c->entry_fence = std::string(v) == "1";
-  if (const char *v = std::getenv("AR_OP_OVERLAP")) c->op_overlap = std::string(v) != "0";
   if (!c->local && c->rpp == 1) {
     c->push_max_bytes = kPushDefaultMaxBytes;
     if (const char *v = std::getenv("AR_PUSH_MAX_MB")) c->push_max_bytes = std::strtoll(v, nullptr, 10) << 20;
@@ -2742,7 +2687,6 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.dyn_ctr = (a.bulk && a.store_tma) ? L.dyn_ctr : nullptr;
   a.dyn_nops = a.dyn_ctr ? L.nops : 0;
   a.entry_fence = c->entry_fence ? 1 : 0;
-  a.op_overlap = c->op_overlap ? 1 : 0;
   c->fast_args = a;
   c->fast_uid = plan->uid;
   c->fast_dptr = dptr;
