@@ -58,8 +58,6 @@ struct DevStep {
   int notify_begin, notify_count;
   int pad;
 };
-// shared-memory cache of one rank's program in ar_exec_kernel (larger programs read global memory)
-constexpr int kCacheSteps = 48, kCacheOps = 96, kCacheWaits = 96, kCacheRanks = 768;
 constexpr int kWaitPaired = 0;   // wait for the producer's same-index CTA
 constexpr int kWaitFull = 1;     // wait for every producer CTA
 constexpr int kWaitRange = 2;    // wait for the producer CTAs whose slice of [p_off, p_len) meets ours of [c_off, c_len)
@@ -75,7 +73,6 @@ struct ExecArgs {
   const int *ranks;          // op src/dst rank lists and notify lists
   const int *prog_begin;     // per local rank
   const int *prog_len;
-  const int *prog_win;       // per local rank: {op_lo, op_n, wait_lo, wait_n, rank_lo, rank_n} of its program
   char *bufs[AR_MAX_RANKS];            // rank -> data buffer base (as seen here)
   unsigned long long *sigs[AR_MAX_RANKS];  // rank -> flag page base (as seen here)
   unsigned long long *err;
@@ -289,7 +286,7 @@ __device__ void body_dispatch(const OpShared &s, size_t v0, size_t v1) {
 constexpr int kMaxStages = 8;
 constexpr int kDefStages = 4;
 constexpr int kDefStageBytes = 40 * 1024;
-constexpr int kMaxDynSmem = 210 * 1024;   // 227 KB per block minus the static shared state (program cache)
+constexpr int kMaxDynSmem = 224 * 1024;   // 227 KB per block minus the static shared state
 // dynamic smem: stages x stage_bytes input ring + 2 output tiles of stage_bytes / 2
 inline int dyn_smem_bytes(int stages, int stage_bytes) { return (stages + 1) * stage_bytes; }
 
@@ -704,31 +701,6 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   const int vec_elems = 16 / a.esize;
   const DevStep *prog = a.steps + a.prog_begin[lr];
   const int nst = a.prog_len[lr];
-  // This rank's program (steps, ops, waits, rank lists) is copied into shared memory once:
-  // every op and wait then reads its descriptor from smem instead of a chain of dependent
-  // global loads (ncu: the op prologue's loads and their spills were the next stall after the
-  // proxy fence).  Programs larger than the cache read global memory as before.
-  __shared__ __align__(16) DevStep c_steps[kCacheSteps];
-  __shared__ __align__(16) DevOp c_ops[kCacheOps];
-  __shared__ __align__(16) DevWait c_waits[kCacheWaits];
-  __shared__ int c_ranks[kCacheRanks];
-  const int *win = a.prog_win + 6 * lr;
-  const int op_lo = win[0], op_n = win[1], wt_lo = win[2], wt_n = win[3], rk_lo = win[4], rk_n = win[5];
-  const bool cached = nst <= kCacheSteps && op_n <= kCacheOps && wt_n <= kCacheWaits && rk_n <= kCacheRanks;
-  if (cached) {
-    auto copy = [](void *dst, const void *src, int bytes) {
-      for (int i = threadIdx.x; i < bytes / 4; i += blockDim.x) ((int *)dst)[i] = ((const int *)src)[i];
-    };
-    copy(c_steps, prog, nst * (int)sizeof(DevStep));
-    copy(c_ops, a.ops + op_lo, op_n * (int)sizeof(DevOp));
-    copy(c_waits, a.waits + wt_lo, wt_n * (int)sizeof(DevWait));
-    copy(c_ranks, a.ranks + rk_lo, rk_n * (int)sizeof(int));
-  }
-  const DevStep *PS = cached ? c_steps : prog;
-  const DevOp *PO = cached ? c_ops : a.ops;
-  const DevWait *PW = cached ? c_waits : a.waits;
-  const int *PR = cached ? c_ranks : a.ranks;
-  const int opb = cached ? op_lo : 0, wtb = cached ? wt_lo : 0, rkb = cached ? rk_lo : 0;
   const unsigned long long t_start = globaltimer();
   unsigned long long *tr = a.trace ? a.trace + (size_t)(lr * gridDim.x + cta) * kTraceSlots : nullptr;
 #define AR_TRACE(i) \
@@ -752,12 +724,12 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
   const unsigned long long epoch = s_epoch;
 
   for (int si = 0; si < nst; si++) {
-    const DevStep st = PS[si];
+    const DevStep st = prog[si];
     // ---- waits (a1 / a3 / a5)
     if (st.wait_count > 0) {
       const int tot = st.wait_count * nctas;  // (wait, producer CTA) pairs over the threads
       for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        const DevWait &w = PW[st.wait_begin - wtb + i / nctas];
+        const DevWait &w = a.waits[st.wait_begin + i / nctas];
         const int c = i % nctas;
         if (w.kind == kWaitPaired && c != cta) continue;
         if (w.kind == kWaitRange) {
@@ -785,9 +757,9 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
     AR_TRACE(1 + 3 * si);
     // ---- ops (a2 / a4)
     for (int oi = 0; oi < st.op_count; oi++) {
-      const DevOp op = PO[st.op_begin - opb + oi];
-      const int *sr = PR + (op.src_begin - rkb);
-      const int *dr = PR + (op.dst_begin - rkb);
+      const DevOp op = a.ops[st.op_begin + oi];
+      const int *sr = a.ranks + op.src_begin;
+      const int *dr = a.ranks + op.dst_begin;
       const long long b0 = op.off * a.esize, b1 = (op.off + op.len) * a.esize;
       const long long vb = (b0 + 15) / 16, ve = b1 / 16;   // whole 16-byte vectors
       __syncthreads();
@@ -852,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
           __syncthreads();
         }
         for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
-          const int consumer = PR[st.notify_begin - rkb + i];
+          const int consumer = a.ranks[st.notify_begin + i];
           asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(flag_ptr(a, consumer, st.slot, me, cta)),
                        "l"(epoch)
                        : "memory");
@@ -866,21 +838,21 @@ __global__ void __launch_bounds__(kThreads, 1) ar_exec_kernel(const __grid_const
         if (threadIdx.x == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
         __syncthreads();
         for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
-          const int consumer = PR[st.notify_begin - rkb + i];
+          const int consumer = a.ranks[st.notify_begin + i];
           asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(flag_ptr(a, consumer, st.slot, me, cta)),
                        "l"(epoch)
                        : "memory");
         }
       } else if (a.fence_mode == 3) {   // all ranks on this GPU (emulated comm): gpu scope
         for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
-          const int consumer = PR[st.notify_begin - rkb + i];
+          const int consumer = a.ranks[st.notify_begin + i];
           asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(flag_ptr(a, consumer, st.slot, me, cta)),
                        "l"(epoch)
                        : "memory");
         }
       } else {
         for (int i = threadIdx.x; i < st.notify_count; i += blockDim.x) {
-          const int consumer = PR[st.notify_begin - rkb + i];
+          const int consumer = a.ranks[st.notify_begin + i];
           st_release_sys(flag_ptr(a, consumer, st.slot, me, cta), epoch);
         }
       }
@@ -1418,7 +1390,6 @@ struct Lowered {
   int *ranks = nullptr;
   int *prog_begin = nullptr;
   int *prog_len = nullptr;
-  int *prog_win = nullptr;
   int nctas = 0;
   bool ll_shape = false;     // CPS-shaped: one all-rank reduce per block, identical input order
   std::vector<int> ll_order;
@@ -1872,7 +1843,6 @@ static void free_lowered(Lowered &L) {
   cudaFree(L.ranks);
   cudaFree(L.prog_begin);
   cudaFree(L.prog_len);
-  cudaFree(L.prog_win);
   if (L.dyn_ctr) cudaFree(L.dyn_ctr);
 }
 
@@ -2660,33 +2630,11 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     if (use_push) lower_push(plan->plan, c->ll_shape[plan->uid], st, ops, w, rk, pb, pl);
     else lower_plan(plan->plan, c->world, st, ops, w, rk, pb, pl);
     Lowered L;
-    // per rank: the windows of ops, waits and rank-list entries its steps use (contiguous by
-    // construction of the lowering; the kernel caches them in shared memory)
-    std::vector<int> pw;
-    for (size_t r = 0; r < pb.size(); r++) {
-      int olo = INT32_MAX, ohi = 0, wlo = INT32_MAX, whi = 0, rlo = INT32_MAX, rhi = 0;
-      for (int i = pb[r]; i < pb[r] + pl[r]; i++) {
-        const DevStep &d = st[i];
-        if (d.op_count) { olo = std::min(olo, d.op_begin); ohi = std::max(ohi, d.op_begin + d.op_count); }
-        if (d.wait_count) { wlo = std::min(wlo, d.wait_begin); whi = std::max(whi, d.wait_begin + d.wait_count); }
-        if (d.notify_count) { rlo = std::min(rlo, d.notify_begin); rhi = std::max(rhi, d.notify_begin + d.notify_count); }
-        for (int k = d.op_begin; k < d.op_begin + d.op_count; k++) {
-          rlo = std::min(rlo, std::min(ops[k].src_begin, ops[k].dst_begin));
-          rhi = std::max(rhi, std::max(ops[k].src_begin + ops[k].nsrc, ops[k].dst_begin + ops[k].ndst));
-        }
-      }
-      if (olo > ohi) olo = ohi = 0;
-      if (wlo > whi) wlo = whi = 0;
-      if (rlo > rhi) rlo = rhi = 0;
-      pw.insert(pw.end(), {olo, ohi - olo, wlo, whi - wlo, rlo, rhi - rlo});
-    }
     if (!c->local) {  // this process runs only the programs of the ranks it hosts
       std::vector<int> pb1(pb.begin() + c->rank, pb.begin() + c->rank + c->rpp);
       std::vector<int> pl1(pl.begin() + c->rank, pl.begin() + c->rank + c->rpp);
-      std::vector<int> pw1(pw.begin() + 6 * c->rank, pw.begin() + 6 * (c->rank + c->rpp));
       pb = pb1;
       pl = pl1;
-      pw = pw1;
     }
     L.steps = upload(st);
     L.ops = upload(ops);
@@ -2706,7 +2654,6 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     L.ranks = upload(rk);
     L.prog_begin = upload(pb);
     L.prog_len = upload(pl);
-    L.prog_win = upload(pw);
     it = cache.emplace(plan->uid, L).first;
   }
   if (use_push)
@@ -2720,7 +2667,6 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
   a.ranks = L.ranks;
   a.prog_begin = L.prog_begin;
   a.prog_len = L.prog_len;
-  a.prog_win = L.prog_win;
   a.err = c->err;
   ++c->epoch;
   a.epoch_dev = c->err + 1;
