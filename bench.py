@@ -85,9 +85,10 @@ def model_params(world=None, emulated=False):
     the largest measured n); otherwise nominal B200 values (α 3 µs,
     β 1/900 GB/s, δ 1/6.54 TB/s, no incast below 9)."""
     if emulated:
-        # emulated ranks share one GPU's HBM: the fitted per-rank model attributes that shared
-        # bandwidth to incast (genmodel_fit_emulated8_graph.json), so selection uses nominal
-        return dict(NOMINAL), "nominal (emulated ranks)"
+        # emulated ranks share one GPU's HBM: their fit (reading A6e, used for the prediction
+        # below) has no link term, and a topology link needs β > 0 — plan selection therefore
+        # uses the nominal B200 values; both give CPS (δ-optimal, fewest steps) on one switch
+        return dict(NOMINAL), "nominal (emulated ranks; the shared-HBM fit has no link term)"
     p = fitted_params(emulated)
     if p is not None and (world is None or world <= p.get("n_max_fit", 0)):
         return p, "fitted (%s)" % p.get("source", "profiles")

@@ -232,7 +232,7 @@ int ar_comm_create_local(int32_t world, int32_t cuda_device, ar_comm **out);
 /* Number of CTAs per rank used by the step-table kernel (0 = automatic).  Same value on all
  * ranks (checked by ar_comm_open_peers); multi-process comms: call before ar_comm_register —
  * AR_EINVAL once peers are open.  The flat and one-shot paths size their own grids and ignore
- * it; the LL128 path uses at most twice this many CTAs. */
+ * it; the LL128 path uses at most its occupancy per SM (2) times this many CTAs. */
 int ar_comm_set_ctas(ar_comm *comm, int32_t ctas);
 
 /* Export `bytes` of device memory at `dptr` (16-byte aligned; may be an interior pointer of
