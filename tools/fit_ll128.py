@@ -39,7 +39,20 @@ def main():
         errs.append({"n": r["n"], "bytes": r["bytes"], "measured_s": r["t_mean"], "predicted_s": pred,
                      "rel_err": abs(pred - r["t_mean"]) / r["t_mean"]})
     e = sorted(x["rel_err"] for x in errs)
-    out = {"timing": a.timing, "rows": len(errs), "alpha": p.alpha, "beta": p.beta,
+    # held out across the rank count: fit on one N, predict the other
+    cross = {}
+    ns = sorted({r["n"] for r in sel})
+    for fit_n in ns:
+        rows_f = [(r["n"], r["bytes"], r["t_mean"]) for r in sel if r["n"] == fit_n]
+        if len({b for _, b, _ in rows_f}) < 2:
+            continue
+        pf, _ = G.genmodel_fit_row("ll128", rows_f)
+        ev = [abs(G.genmodel_closed_form("ll128", r["n"], r["bytes"], pf)["total"] - r["t_mean"]) / r["t_mean"]
+              for r in sel if r["n"] != fit_n]
+        if ev:
+            cross[f"fit_n{fit_n}"] = {"alpha": pf.alpha, "beta": pf.beta, "heldout_rows": len(ev),
+                                      "heldout_err_median": sorted(ev)[len(ev) // 2], "heldout_err_max": max(ev)}
+    out = {"timing": a.timing, "rows": len(errs), "alpha": p.alpha, "beta": p.beta, "cross_n": cross,
            "line_gbs": 1 / p.beta / 1e9 if p.beta > 0 else None, "sse": sse, "max_bytes": a.max_bytes,
            "pred_err_median": e[len(e) // 2], "pred_err_max": e[-1], "points": errs, "sources": a.files}
     json.dump(out, open(os.path.join(ROOT, "profiles", f"genmodel_fit_ll128_{a.timing}.json"), "w"), indent=1)
