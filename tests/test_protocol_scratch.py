@@ -12,7 +12,8 @@ This module executes that protocol under random schedules — every rank a seque
 each call a sequence of writes (always enabled) and flag-checked reads (enabled once the
 awaited line carries the call's epoch) — and asserts that no write ever lands on a line whose
 current content has not been read yet, and that every schedule completes.  A single-buffered
-variant (parity removed) must violate the invariant: the model can fail."""
+one-shot variant (parity removed) must violate the invariant: the model can fail.  (Each slot
+stands for all lines one writer sends one reader in a call; the argument is per line.)"""
 import random
 
 import pytest
