@@ -1956,15 +1956,16 @@ static void init_comm(ar_comm *c) {
     }
   }
   if (const char *v = std::getenv("AR_LL_CTAS")) c->ll_ctas = std::max(1, std::atoi(v));
-  // two CTAs per SM: measured best of 32 / 64 / 148 / 296 on 2 and 4 B200s (profiles/round2/ll128;
-  // a variant batching the loads of the N-1 incoming lines measured 0-6 % slower: not kept)
+  // as many CTAs as are resident (3 per SM): measured best of 32 / 64 / 148 / 296 / 444 on 2 and
+  // 4 B200s (profiles/round2/ll128; a variant batching the loads of the N-1 incoming lines
+  // measured 0-6 % slower: not kept)
   {
     int per = 0, per2 = 0;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_ll128_kernel<false>, kThreads, 0));
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, ar_ll128_kernel<true>, kThreads, 0));
     c->ll128_per_sm = std::max(1, std::min(per, per2));
   }
-  c->ll128_ctas = std::min(2, c->ll128_per_sm) * nsm;
+  c->ll128_ctas = c->ll128_per_sm * nsm;   // 3 per SM: equal to 2 up to 8 MiB, +1-11 % at 16-32 MiB
   if (const char *v = std::getenv("AR_LL128_CTAS")) c->ll128_ctas = std::max(1, std::atoi(v));
 }
 
