@@ -152,11 +152,18 @@ __device__ void nv_barrier(const NvArgs &a, int slot, unsigned long long epoch, 
   __syncthreads();
 }
 
-template <bool BF16>
+// MODE: 0 = fp32; 1 = bf16 with fp32 accumulation in the switch (acc::f32, the default);
+// 2 = bf16 accumulated in bf16 by the switch (measurement only: AR_NVLS_BF16_ACC=bf16)
+template <int MODE>
 __device__ __forceinline__ uint4 ld_reduce(const void *mc) {
   uint4 v;
-  if (BF16)
+  if (MODE == 1)
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(mc)
+                 : "memory");
+  else if (MODE == 2)
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(mc)
                  : "memory");
@@ -167,9 +174,9 @@ __device__ __forceinline__ uint4 ld_reduce(const void *mc) {
                  : "memory");
   return v;
 }
-template <bool BF16>
+template <int MODE>
 __device__ __forceinline__ void mc_store(void *mc, const uint4 &v) {
-  if (BF16)
+  if (MODE != 0)
     asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1,%2,%3,%4};" ::"l"(mc), "r"(v.x), "r"(v.y),
                  "r"(v.z), "r"(v.w)
                  : "memory");
@@ -180,11 +187,14 @@ __device__ __forceinline__ void mc_store(void *mc, const uint4 &v) {
 }
 
 // Scalar tail (count not a multiple of 16 bytes): fp32 one element, bf16 an element pair.
-template <bool BF16>
+template <int MODE>
 __device__ __forceinline__ void tail_reduce_store(char *mc) {
   uint32_t v;
-  if (BF16) {
+  if (MODE == 1)
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.bf16x2 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
+  else if (MODE == 2)
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.bf16x2 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
+  if (MODE != 0) {
     asm volatile("multimem.st.relaxed.sys.global.bf16x2 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
   } else {
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
@@ -192,7 +202,7 @@ __device__ __forceinline__ void tail_reduce_store(char *mc) {
   }
 }
 
-template <bool BF16>
+template <int MODE, int U>
 __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant__ NvArgs a) {
   __shared__ unsigned long long s_epoch;
   const unsigned long long t0 = nv_timer();
@@ -202,7 +212,6 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
   nv_barrier(a, 0, epoch, t0);   // every rank's input is in place
   const long long vb = a.off * a.esize / 16, nv = a.len * a.esize / 16;
   const long long v0 = vb + nv * blockIdx.x / gridDim.x, v1 = vb + nv * (blockIdx.x + 1) / gridDim.x;
-  constexpr int U = 4;   // vectors in flight per thread
   if (a.dyn) {
     // dynamic chunks of 8 x (blockDim x U) vectors: CTAs that get more switch bandwidth take
     // more chunks (the same scheme as the P2P executor's tiles).  A/B option, off by default:
@@ -224,12 +233,12 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
 #pragma unroll
         for (int u = 0; u < U; u++) {
           const long long v = base + (long long)u * blockDim.x;
-          if (v < c1) x[u] = ld_reduce<BF16>(a.mc + v * 16);
+          if (v < c1) x[u] = ld_reduce<MODE>(a.mc + v * 16);
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
           const long long v = base + (long long)u * blockDim.x;
-          if (v < c1) mc_store<BF16>(a.mc + v * 16, x[u]);
+          if (v < c1) mc_store<MODE>(a.mc + v * 16, x[u]);
         }
       }
     }
@@ -239,19 +248,19 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const long long v = base + (long long)u * blockDim.x;
-      if (v < v1) x[u] = ld_reduce<BF16>(a.mc + v * 16);
+      if (v < v1) x[u] = ld_reduce<MODE>(a.mc + v * 16);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const long long v = base + (long long)u * blockDim.x;
-      if (v < v1) mc_store<BF16>(a.mc + v * 16, x[u]);
+      if (v < v1) mc_store<MODE>(a.mc + v * 16, x[u]);
     }
   }
   if (a.tail_len > 0 && blockIdx.x == 0) {
-    const int step = BF16 ? 2 : 1;
+    const int step = MODE != 0 ? 2 : 1;
     for (long long e = a.tail_off + (long long)threadIdx.x * step; e < a.tail_off + a.tail_len;
          e += (long long)blockDim.x * step)
-      tail_reduce_store<BF16>(a.mc + e * a.esize);
+      tail_reduce_store<MODE>(a.mc + e * a.esize);
   }
   nv_barrier(a, 1, epoch, t0);   // every rank's results have landed in every GPU's buffer
   if (threadIdx.x == 0) {
@@ -277,7 +286,26 @@ struct ar_nvls {
   int nctas = 0;
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
   bool dyn = false;
+  int unroll = 4;              // 16-byte vectors in flight per thread (AR_NVLS_U: 2, 4, 8, 16)
+  bool bf16_acc_bf16 = false;  // AR_NVLS_BF16_ACC=bf16: switch accumulates bf16 (measurement only)
 };
+
+namespace {
+template <int MODE>
+void launch_unroll(int unroll, int nctas, cudaStream_t st, const NvArgs &a) {
+  switch (unroll) {
+    case 2: nvls_kernel<MODE, 2><<<nctas, kNvThreads, 0, st>>>(a); break;
+    case 8: nvls_kernel<MODE, 8><<<nctas, kNvThreads, 0, st>>>(a); break;
+    case 16: nvls_kernel<MODE, 16><<<nctas, kNvThreads, 0, st>>>(a); break;
+    default: nvls_kernel<MODE, 4><<<nctas, kNvThreads, 0, st>>>(a); break;
+  }
+}
+void launch_mode(int mode, int unroll, int nctas, cudaStream_t st, const NvArgs &a) {
+  if (mode == 1) launch_unroll<1>(unroll, nctas, st, a);
+  else if (mode == 2) launch_unroll<2>(unroll, nctas, st, a);
+  else launch_unroll<0>(unroll, nctas, st, a);
+}
+}  // namespace
 
 namespace gtar {
 // Launch the in-switch AllReduce of `count` elements of this rank's NVLS buffer (dptr must be
@@ -311,8 +339,8 @@ void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, vo
   a.esize = es;
   a.timeout_ns = n->timeout_ns;
   a.dyn = n->dyn ? 1 : 0;
-  if (dtype == AR_BF16) nvls_kernel<true><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
-  else nvls_kernel<false><<<n->nctas, kNvThreads, 0, (cudaStream_t)stream>>>(a);
+  const int mode = dtype == AR_BF16 ? (n->bf16_acc_bf16 ? 2 : 1) : 0;
+  launch_mode(mode, n->unroll, n->nctas, (cudaStream_t)stream, a);
   RT_CALL(cudaGetLastError());
 }
 }  // namespace gtar
@@ -377,6 +405,12 @@ int ar_nvls_create(int32_t rank, int32_t world, int32_t cuda_device, uint64_t by
     if (const char *v = std::getenv("AR_NVLS_CTAS")) n->nctas = std::max(1, std::min(kNvCtaCap, std::atoi(v)));
     if (const char *t = std::getenv("AR_FLAG_TIMEOUT_MS")) n->timeout_ns = std::strtoull(t, nullptr, 10) * 1000000ull;
     if (const char *v = std::getenv("AR_NVLS_DYN")) n->dyn = std::string(v) != "0";
+    if (const char *v = std::getenv("AR_NVLS_U")) {
+      const int u = std::atoi(v);
+      if (u != 2 && u != 4 && u != 8 && u != 16) throw InvalidArg("AR_NVLS_U must be 2, 4, 8 or 16");
+      n->unroll = u;
+    }
+    if (const char *v = std::getenv("AR_NVLS_BF16_ACC")) n->bf16_acc_bf16 = std::string(v) == "bf16";
     *out = n;
     return AR_OK;
   })

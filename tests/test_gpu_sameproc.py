@@ -308,3 +308,70 @@ def test_ll128_path(world, dtype):
             check(sp, world, sizes[0], dtype, "ring", expect_kernel="ar_exec_kernel")
     finally:
         sp.destroy()
+
+
+@pytest.mark.parametrize("nproc,R", [(2, 4), (4, 2), (2, 8)])
+def test_multi_level_same_process(nproc, R):
+    """Multi-level execution (SURVEY §8(f) NEXT #3, config C5's "8 ranks per GPU", C1's
+    two-level tree): `nproc` communicators from ar_comm_create_multi, each hosting R
+    consecutive ranks in one buffer, living in this process on cuda:0 — the code path of one
+    process per GPU (system-scope flags, per-process flag-page blocks, peers' rank slots at
+    peer_base + (r mod R)·stride), with same-process peers mapped by raw pointer.  The GenTree
+    plan of the two-level tree (leaf level among a process's ranks, root level across
+    processes) and forced flat kinds that mix hosted and peer ranks inside every step; SUM then
+    AVG; bit-exact against the oracle on every rank."""
+    world = nproc * R
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    old = os.environ.get("AR_FLAG_TIMEOUT_MS")
+    os.environ["AR_FLAG_TIMEOUT_MS"] = "8000"
+    try:
+        comms = [G.Comm.create_multi(p, nproc, R, 0) for p in range(nproc)]
+    finally:
+        if old is None:
+            os.environ.pop("AR_FLAG_TIMEOUT_MS", None)
+        else:
+            os.environ["AR_FLAG_TIMEOUT_MS"] = old
+    try:
+        for c in comms:
+            c.set_ctas(max(1, nsm // world))   # every hosted rank of every process resident at once
+        nvl = {"alpha": 1e-5, "beta": 4.0 / 770e9, "epsilon": 0.0, "w_t": 9}
+        hbm = {"alpha": 3e-6, "beta": 4.0 / 3000e9, "epsilon": 0.0, "w_t": 64}
+        server = {"gamma": 0.0, "delta": 4.0 / 6.5e12}
+        tree = T.two_level_doc([R] * nproc, nvl, hbm, server)
+        flat = T.single_switch_doc(world, nvl, server)
+        streams = [torch.cuda.Stream() for _ in range(nproc)]
+        for dtype in ("f32", "bf16"):
+            es = 4 if dtype == "f32" else 2
+            for count in (world * 1024 + 7, 1 << 18):
+                stride = G.rank_stride_bytes(count, dtype)
+                bufs = [torch.zeros(stride * R, dtype=torch.uint8, device="cuda") for _ in range(nproc)]
+                blobs = [c.export(b) for c, b in zip(comms, bufs)]
+                for c in comms:
+                    c.open_peers(blobs)
+                for doc, force in ((tree, None), (flat, "cps"), (flat, "ring")):
+                    for p in range(nproc):
+                        for i in range(R):
+                            G.fill_synthetic(bufs[p].data_ptr() + i * stride, count, dtype, SEED, p * R + i, 0)
+                    plan = G.Plan.from_topology(doc, count, dtype, None, force)
+                    oplan, _ = GT.gentree(T.parse_topology(doc), count, es, force=force)
+                    assert plan.to_json() == OP.plan_to_json(oplan, dtype)
+                    torch.cuda.synchronize()
+                    for op in ("sum", "avg"):
+                        for p in range(nproc):
+                            G.allreduce_exec(plan, comms[p], bufs[p], count, dtype, stream=streams[p], op=op)
+                    torch.cuda.synchronize()
+                    for c in comms:
+                        c.async_error()
+                        assert c.last_kernel() == "ar_exec_kernel"
+                    xs = GEN.generate_all(SEED, world, count, dtype)
+                    want = SM.simulate(oplan, SM.simulate(oplan, xs, dtype), dtype, op="avg")
+                    for p in range(nproc):
+                        host = bufs[p].cpu().numpy()
+                        for i in range(R):
+                            got = host[i * stride: i * stride + count * es].view(
+                                np.float32 if dtype == "f32" else np.uint16)
+                            assert_bits_equal(got, want[p * R + i], dtype,
+                                              f"{force or 'tree'} {dtype} count={count} rank {p * R + i}")
+    finally:
+        for c in comms:
+            c.destroy()
