@@ -14,8 +14,9 @@ for n in 2 3 4; do
 done
 S="16777216 268435456 1073741824"
 for n in 4 2; do
-  for u in 4 8 16 2; do
-    for c in 16 32 64 8; do
+  if [ $n = 4 ]; then US="4 8 16 2"; CS="16 32 64 8"; else US="4 8 16"; CS="16 32 64"; fi
+  for u in $US; do
+    for c in $CS; do
       step sw_n${n}_u${u}_c${c} timeout 300 bash -c "$(declare -f T); P=$((P+10+n*100+u*5+c)); AR_NVLS_U=$u AR_NVLS_CTAS=$c T --nproc-per-node $n tools/harness.py sweep --dtype f32 --plans nvls --no-nccl --timing graph --sizes $S > $O/sw_n${n}_u${u}_c${c}_f32.jsonl 2> $O/sw_n${n}_u${u}_c${c}.err"
     done
   done
