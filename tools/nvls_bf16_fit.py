@@ -14,6 +14,11 @@ inputs (float64 where provably exact, Fraction otherwise) and from fixed associa
   seq_{order}_f32_{rne,rz}      sequential fp32 sum in a rank order, then to bf16
   seq_{order}_bf16_rne          every partial rounded to bf16 (RNE) (bf16 accumulation)
 
+Then, over the elements whose exact sum is not a bf16 value, the probability that the switch
+rounded AWAY from zero as a function of the sum's position between its two bf16 neighbours
+(frac = distance from the toward-zero neighbour in units of the gap): a round-to-nearest unit
+gives 0 below 1/2 and 1 above; stochastic rounding gives P(away) rising with frac.
+
 Measurement analysis only; nothing on the product path depends on it.
 """
 import json
@@ -151,6 +156,32 @@ def hypotheses(inp):
     return H
 
 
+def away_table(inp, got):
+    """P(rounded away from zero | frac) in eighths, plus the ties (frac = 1/2) separately."""
+    X = bf16_to_f64(inp)
+    ex = exact_sums(X)
+    g = bf16_to_f64(got)
+    fr, aw = [], []
+    for i in range(got.size):
+        q = Fraction(ex[i])
+        z = Fraction(round_to(q, 8, "rz"))
+        if q == z:
+            continue
+        b = int(np.array([float(z)], dtype=np.float32).view(np.uint32)[0] >> 16)
+        nxt = Fraction(float(np.array([(b + 1) << 16], dtype=np.uint32).view(np.float32)[0]))
+        fr.append(float((abs(q) - abs(z)) / (abs(nxt) - abs(z))))
+        aw.append(bool(g[i] != float(z)))
+    fr, aw = np.array(fr), np.array(aw)
+    rows = []
+    for k in range(8):
+        m = (fr >= k / 8) & (fr < (k + 1) / 8)
+        if m.any():
+            rows.append({"frac": [k / 8, (k + 1) / 8], "n": int(m.sum()), "p_away": round(float(aw[m].mean()), 4)})
+    t = fr == 0.5
+    return {"inexact": int(fr.size), "bins": rows,
+            "ties": {"n": int(t.sum()), "p_away": round(float(aw[t].mean()), 4) if t.any() else None}}
+
+
 def main():
     for path in sys.argv[1:]:
         d = np.load(path)
@@ -170,7 +201,8 @@ def main():
                               "best_misses": [{"inputs": [float(x) for x in X[:, i]], "got": int(got[i]),
                                                "best": int(H[bk][i]),
                                                "exact": float(sum(Fraction(float(x)) for x in X[:, i]))}
-                                              for i in bad]}), flush=True)
+                                              for i in bad],
+                              "p_away_by_frac": away_table(inp[:, :60000], got[:60000])}), flush=True)
 
 
 if __name__ == "__main__":
