@@ -119,11 +119,12 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
 /* GenTree with the NVLS plan kind as an extra candidate (reading NV1;
  * the paper's min-GenModel selection): builds gentree_plan's plan, and on a
  * single-switch topology with dtype AR_F32 replaces it by the NVLS plan when the NVLS row
- * predicts less time than the path the executor would run the plan on: the one-shot row
- * (reading OS1, `oneshot_params`) when oneshot_params != NULL, the plan is one-shot eligible
- * and count·esize <= oneshot_max_bytes (the communicator's cut-off); else the LL128 row
- * (`ll128_params`) when given, the plan is eligible, count·esize <= ll128_max_bytes and the
- * blocks are equal and 16-byte aligned; else the executed-plan prediction
+ * predicts less time than the path the executor would run the plan on (the communicator's
+ * cut-offs, ar_comm_get_paths / ar_default_paths): the LL128 row (`ll128_params`) when
+ * given, the plan is one-shot eligible with equal 16-byte-aligned blocks, N <= 8 and
+ * min(ll128_min_bytes, oneshot_max_bytes) < count·esize <= ll128_max_bytes; else the one-shot
+ * row (reading OS1, `oneshot_params`) when given, the plan is one-shot eligible and
+ * count·esize <= oneshot_max_bytes; else the executed-plan prediction
  * (genmodel_choose_nvls).  NULL row params leave that path out.  NVLS plans (also
  * force_kind "nvls" in gentree_plan; fp32 only, single switch) have the CPS data movement
  * and "switch_reduce": true in their JSON; every element ends as the correctly rounded fp32
@@ -132,7 +133,8 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
  * (ar_comm_attach_nvls; dptr = that buffer).  params and nvls_params are required. */
 int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
                       const gm_params *nvls_params, const gm_params *oneshot_params, uint64_t oneshot_max_bytes,
-                      const gm_params *ll128_params, uint64_t ll128_max_bytes, gt_plan **out);
+                      const gm_params *ll128_params, uint64_t ll128_min_bytes, uint64_t ll128_max_bytes,
+                      gt_plan **out);
 
 /* Convenience: single switch with `world` ranks and uniform `params` (required). */
 int gentree_plan_single_switch(int32_t world, uint64_t count, int32_t dtype, const gm_params *params,
@@ -279,9 +281,9 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
  * previous launch left.  Every element of every rank's buffer ends
  * equal to the plan's left-to-right fp32 sum of the ranks' inputs (bit-exact to the CPU
  * oracle).  One rank per GPU, CPS-shaped plans take a flag-free path by size: the one-shot
- * kernel up to the one-shot cut-off, the LL128 two-shot kernel (flags inside 128-byte lines)
- * up to AR_LL128_MAX_KB (16 MiB default) when the blocks are equal and 16-byte aligned, else
- * the step-table kernel — all with the plan's bits (ar_comm_last_kernel tells which).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
+ * LL128 two-shot kernel (flags inside 128-byte lines) when the blocks are equal and 16-byte
+ * aligned and the message lies in its range (ar_comm_get_paths), else the one-shot kernel up
+ * to the one-shot cut-off, else the step-table kernel — all with the plan's bits (ar_comm_last_kernel tells which).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
  * plan's, unregistered or misaligned buffer; AR_ESYS on launch failure. */
 int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
                    void *stream);
@@ -321,9 +323,23 @@ int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
  * or "nvls_kernel" (NVLS plans); "" before the first call.  Static storage. */
 const char *ar_comm_last_kernel(ar_comm *comm);
 
+/* Path cut-offs (bytes per rank) of CPS-shaped plans on a one-rank-per-GPU communicator:
+ * messages with equal 16-byte-aligned blocks (and N <= 8) in (ll128_min, ll128_max] take the
+ * LL128 two-shot kernel; otherwise messages up to oneshot_max take the one-shot kernel;
+ * everything else the step-table kernel.  ar_default_paths gives the defaults for `world`
+ * ranks, measured on 2 and 4 B200s (one-shot to 1.5 MiB/(N−1); LL128 from 768 KiB/(N−1),
+ * at most 384 KiB, to 64 MiB/N); AR_LL_MAX_KB, AR_LL128_MIN_KB and AR_LL128_MAX_KB override
+ * them at communicator creation.  ar_comm_get_paths reports a communicator's effective
+ * values (ll128_min already capped by oneshot_max; zeros where a path is unavailable:
+ * emulated or several-ranks-per-GPU communicators, N > 8 for LL128).  NULL outputs are
+ * skipped.  Errors: AR_EINVAL for world outside [2, AR_MAX_RANKS] / a NULL comm. */
+int ar_default_paths(int32_t world, uint64_t *oneshot_max_bytes, uint64_t *ll128_min_bytes, uint64_t *ll128_max_bytes);
+int ar_comm_get_paths(ar_comm *comm, uint64_t *oneshot_max_bytes, uint64_t *ll128_min_bytes, uint64_t *ll128_max_bytes);
+
 /* Largest message (bytes per rank) run through the one-shot small-message path (default the
  * measured cut-off 1.5 MiB/(N−1); e.g. set it to GenModel's crossover of the "oneshot" row and
- * the executed-plan prediction).  0 disables the path.  AR_EINVAL above the scratch capacity
+ * the executed-plan prediction; messages the LL128 path takes (ar_comm_get_paths) do not reach
+ * it).  0 disables the path.  AR_EINVAL above the scratch capacity
  * allocated at creation or on a communicator without one (emulated / several ranks per GPU). */
 int ar_comm_set_oneshot_max(ar_comm *comm, uint64_t bytes);
 

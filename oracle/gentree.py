@@ -412,26 +412,28 @@ def oneshot_eligible(plan: Plan) -> bool:
 
 def gentree_nvls(topo, count: int, esize: int, params: Params, nvls_params: Params,
                  oneshot_params: Params | None = None, oneshot_max_bytes: int = 0,
-                 ll128_params: Params | None = None, ll128_max_bytes: int = 0):
+                 ll128_params: Params | None = None, ll128_max_bytes: int = 0, ll128_min_bytes: int = 0):
     """GenTree with the NVLS plan kind as one more candidate (reading NV1; the paper's
     minimum-GenModel choice): on a single-switch topology in fp32, the NVLS plan
     replaces GenTree's plan iff the NVLS row's closed form (P:441-444 with its own α, β) is
     strictly below the prediction of the path the executor runs GenTree's plan on — the
-    one-shot row (reading OS1) for one-shot-eligible plans up to oneshot_max_bytes when its
-    parameters are given, else the LL128 row for eligible plans with equal 16-byte-aligned
-    blocks up to ll128_max_bytes when given, else the executed-plan prediction (ties keep the
-    plan)."""
+    LL128 row for one-shot-eligible plans with equal 16-byte-aligned blocks, N <= 8 and a size
+    in (min(ll128_min_bytes, oneshot_max_bytes), ll128_max_bytes] when its parameters are
+    given, else the one-shot row (reading OS1) for one-shot-eligible plans up to
+    oneshot_max_bytes when given, else the executed-plan prediction (ties keep the plan).
+    The cut-offs are the executor's (a measured engineering choice, not the paper's)."""
     from .genmodel import predict_executed
     plan, reps = gentree(topo, count, esize, params)
     single = sum(1 for nd in topo.nodes.values() if nd.kind != "server") == 1
     if esize == 4 and single:
         t_plan = predict_executed(plan, esize, params)["total"]
         n = len(topo.servers)
-        if oneshot_params is not None and count * esize <= oneshot_max_bytes and oneshot_eligible(plan):
-            t_plan = closed_form_f64("oneshot", n, count * esize, oneshot_params)["total"]
-        elif (ll128_params is not None and count * esize <= ll128_max_bytes and oneshot_eligible(plan)
-              and count % n == 0 and (count // n) * esize % 16 == 0):
-            t_plan = closed_form_f64("ll128", n, count * esize, ll128_params)["total"]
+        S = count * esize
+        if (ll128_params is not None and oneshot_eligible(plan) and n <= 8 and count % n == 0
+                and (count // n) * esize % 16 == 0 and min(ll128_min_bytes, oneshot_max_bytes) < S <= ll128_max_bytes):
+            t_plan = closed_form_f64("ll128", n, S, ll128_params)["total"]
+        elif oneshot_params is not None and S <= oneshot_max_bytes and oneshot_eligible(plan):
+            t_plan = closed_form_f64("oneshot", n, S, oneshot_params)["total"]
         t_nvls = closed_form_f64("nvls", len(topo.servers), count * esize, nvls_params)["total"]
         if t_nvls < t_plan:
             return gentree(topo, count, esize, params, "nvls")

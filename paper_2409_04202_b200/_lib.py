@@ -105,7 +105,7 @@ _SIGS = {
     "allreduce_exec_nvls": (I32, [P, U64, I32, P]),
     "ar_comm_attach_nvls": (I32, [P, P]),
     "gentree_plan_nvls": (I32, [ctypes.c_char_p, U64, I32, ctypes.POINTER(GmParams), ctypes.POINTER(GmParams),
-                                ctypes.POINTER(GmParams), U64, ctypes.POINTER(GmParams), U64, ctypes.POINTER(P)]),
+                                ctypes.POINTER(GmParams), U64, ctypes.POINTER(GmParams), U64, U64, ctypes.POINTER(P)]),
     "ar_nvls_get_async_error": (I32, [P]),
     "ar_nvls_destroy": (I32, [P]),
     "ar_comm_set_trace": (I32, [P, I32]),
@@ -117,6 +117,8 @@ _SIGS = {
     "ar_exec_movement_plan": (I32, [P, P, P, U64, I32, P]),
     "ar_comm_last_kernel": (ctypes.c_char_p, [P]),
     "ar_comm_set_oneshot_max": (I32, [P, U64]),
+    "ar_default_paths": (I32, [I32, ctypes.POINTER(U64), ctypes.POINTER(U64), ctypes.POINTER(U64)]),
+    "ar_comm_get_paths": (I32, [P, ctypes.POINTER(U64), ctypes.POINTER(U64), ctypes.POINTER(U64)]),
     "allreduce_exec_host": (I32, [P, P, P, P, U64, I32, P]),
     "ar_fill_synthetic": (I32, [P, U64, I32, U64, I32, I32, U64, P]),
     "ar_local_reduce": (I32, [ctypes.POINTER(P), I32, P, U64, I32, P]),

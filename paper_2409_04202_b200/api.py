@@ -108,16 +108,17 @@ class Plan:
     def from_topology_nvls(cls, topology_json: str, count: int, dtype, params: GmParams,
                            nvls_params: GmParams, oneshot_params: GmParams | None = None,
                            oneshot_max_bytes: int = 0, ll128_params: GmParams | None = None,
-                           ll128_max_bytes: int = 0) -> "Plan":
+                           ll128_max_bytes: int = 0, ll128_min_bytes: int = 0) -> "Plan":
         """GenTree with the NVLS kind as a candidate (gentree_plan_nvls, reading NV1); the plan
-        side is predicted on the row of the path the executor takes (one-shot, LL128, steps)."""
+        side is predicted on the row of the path the executor takes (LL128, one-shot, steps;
+        cut-offs as default_paths() / Comm.paths())."""
         h = ctypes.c_void_p()
         check(lib.gentree_plan_nvls(topology_json.encode(), count, dtype_code(dtype), ctypes.byref(params),
                                     ctypes.byref(nvls_params),
                                     ctypes.byref(oneshot_params) if oneshot_params is not None else None,
                                     int(oneshot_max_bytes),
                                     ctypes.byref(ll128_params) if ll128_params is not None else None,
-                                    int(ll128_max_bytes), ctypes.byref(h)))
+                                    int(ll128_min_bytes), int(ll128_max_bytes), ctypes.byref(h)))
         return cls(h)
 
     @property
@@ -304,6 +305,12 @@ class Comm:
     def async_error(self):
         check(lib.ar_comm_get_async_error(self._h))
 
+    def paths(self) -> dict:
+        """The communicator's path cut-offs (ar_comm_get_paths), bytes per rank."""
+        a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.ar_comm_get_paths(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return {"oneshot_max": a.value, "ll128_min": b.value, "ll128_max": c.value}
+
     def set_oneshot_max(self, nbytes: int):
         """Cut-off of the one-shot small-message path (ar_comm_set_oneshot_max)."""
         check(lib.ar_comm_set_oneshot_max(self._h, int(nbytes)))
@@ -417,6 +424,14 @@ class Executor:
 
 
 OPS = {"sum": 0, "avg": 1}
+
+
+def default_paths(world: int) -> dict:
+    """Default path cut-offs of a one-rank-per-GPU communicator of `world` ranks
+    (ar_default_paths), bytes per rank."""
+    a, b, c = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.ar_default_paths(world, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return {"oneshot_max": a.value, "ll128_min": b.value, "ll128_max": c.value}
 
 
 def allreduce_exec(plan: Plan, comm: Comm, buf, count: int | None = None, dtype=None, stream=None, op: str = "sum"):

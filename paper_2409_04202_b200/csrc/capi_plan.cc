@@ -247,7 +247,8 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
 
 int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, const gm_params *params,
                       const gm_params *nvls_params, const gm_params *oneshot_params, uint64_t oneshot_max_bytes,
-                      const gm_params *ll128_params, uint64_t ll128_max_bytes, gt_plan **out) {
+                      const gm_params *ll128_params, uint64_t ll128_min_bytes, uint64_t ll128_max_bytes,
+                      gt_plan **out) {
   AR_TRY({
     if (!topology_json || !nvls_params || !params || !out) throw InvalidArg("null argument");
     check_params(nvls_params);
@@ -270,14 +271,16 @@ int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, 
       const int64_t S = (int64_t)count * esize_of(dtype);
       const bool eligible = !oneshot_order(g->plan).empty();
       const int n = g->plan.n;
-      if (oneshot_params && (uint64_t)S <= oneshot_max_bytes && eligible) {
-        // the executor runs this plan through its one-shot path: compare that row instead
-        tp = closed_form_f64("oneshot", n, S, to_params(oneshot_params), {}).total;
-        use = tn < tp ? 1 : 0;
-      } else if (ll128_params && (uint64_t)S <= ll128_max_bytes && eligible && count % (uint64_t)n == 0 &&
-                 (count / n) * esize_of(dtype) % 16 == 0) {
-        // ... or through its LL128 two-shot path (equal, 16-byte-aligned blocks)
+      const bool ll128_ok = eligible && n <= 8 && count % (uint64_t)n == 0 && (count / n) * esize_of(dtype) % 16 == 0 &&
+                            (uint64_t)S > std::min(ll128_min_bytes, oneshot_max_bytes) && (uint64_t)S <= ll128_max_bytes;
+      if (ll128_params && ll128_ok) {
+        // the executor runs this plan through its LL128 two-shot path (equal, 16-byte-aligned
+        // blocks, above the LL128 floor): compare that row instead
         tp = closed_form_f64("ll128", n, S, to_params(ll128_params), {}).total;
+        use = tn < tp ? 1 : 0;
+      } else if (oneshot_params && (uint64_t)S <= oneshot_max_bytes && eligible) {
+        // ... or through its one-shot path
+        tp = closed_form_f64("oneshot", n, S, to_params(oneshot_params), {}).total;
         use = tn < tp ? 1 : 0;
       }
       if (use) {

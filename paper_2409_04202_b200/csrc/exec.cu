@@ -1444,9 +1444,10 @@ struct ar_comm {
   bool ll_opened = false;
   int ll_ctas = 32;
   // LL128 two-shot path (ar_ll128_kernel) for CPS-shaped plans with 16-byte-aligned equal
-  // blocks, ll_max_bytes < message <= ll128_max_bytes (AR_LL128_MAX_KB; 0 = off); its scratch
-  // follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
-  long long ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
+  // blocks, min(ll128_min_bytes, ll_max_bytes) < message <= ll128_max_bytes (AR_LL128_MIN_KB,
+  // AR_LL128_MAX_KB; max 0 = off) — it takes such messages before the one-shot path; its
+  // scratch follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
+  long long ll128_min_bytes = 0, ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
   int ll128_per_sm = 1;        // resident ar_ll128_kernel CTAs per SM
   int ll128_ctas = 296;
   std::map<uint64_t, std::vector<int>> ll_shape;   // plan uid -> summation order (empty: not CPS-shaped)
@@ -1482,6 +1483,7 @@ struct Blob {
   int64_t pid;
   int32_t device, pad3;
   uint64_t raw_base, raw_sig, raw_ll;
+  int64_t ll128_min_bytes;
 };
 static_assert(sizeof(Blob) <= AR_BLOB_BYTES, "blob too large");
 
@@ -1870,8 +1872,22 @@ static int resident_ctas(int device) {
   }
 
 constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
-// LL128 two-shot path up to this message size (AR_LL128_MAX_KB; 0 = off)
-constexpr long long kLL128DefaultMaxBytes = 16LL << 20;
+
+// Default path cut-offs of a one-rank-per-GPU communicator of `world` ranks (bytes per rank),
+// measured on 2 and 4 B200s (fp32 and bf16, graph timing; profiles/round2/README.md §12):
+//  * one-shot path (ar_ll_kernel) up to 1.5 MiB/(N−1): it beats the flag protocol there
+//    (~(N−1)·2S of line traffic against two flag round trips);
+//  * the LL128 two-shot path (ar_ll128_kernel) takes eligible messages (equal 16-byte-aligned
+//    blocks) from 768 KiB/(N−1) (at most 384 KiB) up to 64 MiB/N: above the floor it beats the
+//    one-shot path (N = 4, 512 KiB: 9.3 vs 13.6 us; N = 2, 1.5 MiB: 8.4 vs 17.5 us), and up to
+//    the ceiling the step-table kernel (N = 2, 24-32 MiB: 564 vs 492-516 GB/s; N = 4, 32 MiB:
+//    508 vs 554 — the ceiling falls with N).
+static void default_paths(int world, long long *oneshot_max, long long *ll128_min, long long *ll128_max) {
+  const long long w1 = std::max(1, world - 1);
+  *oneshot_max = std::min<long long>(kLLDefaultMaxBytes, (3LL << 19) / w1) / 256 * 256;
+  *ll128_min = std::min<long long>(*oneshot_max, std::min<long long>(384 << 10, (768LL << 10) / w1)) / 256 * 256;
+  *ll128_max = std::max<long long>(1LL << 20, ((64LL << 20) / std::max(1, world)) >> 20 << 20);
+}
 // Off by default: measured slower than the pull protocol on 2 and 4 B200s (4 GPUs, 1 MiB:
 // 27.7 vs 22.0 us; 16 MiB: 66.9 vs 55.4 us — the scatter step's per-block copies serialise
 // load -> store -> completion per tile, and the owner cannot start before every source's
@@ -1933,11 +1949,12 @@ static void init_comm(ar_comm *c) {
     // measured on 4 x B200 (profiles/README.md): the one-shot path costs ~(N-1)·2S of line
     // traffic per GPU; it beats the flag protocol up to ~768 KiB at N = 4 (13.6 vs 21.4 us at
     // 512 KiB, 25.2 vs 21.9 at 1 MiB), so the cut-off scales as 1.5 MiB / (N - 1)
-    c->ll_max_bytes = std::min<long long>(kLLDefaultMaxBytes, (3LL << 19) / (c->world - 1)) / 256 * 256;
+    default_paths(c->world, &c->ll_max_bytes, &c->ll128_min_bytes, &c->ll128_max_bytes);
     if (const char *v = std::getenv("AR_LL_MAX_KB")) c->ll_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
     c->ll_max_bytes = std::max(0LL, c->ll_max_bytes);
     c->push_max_bytes = std::max(0LL, c->push_max_bytes);
-    c->ll128_max_bytes = kLL128DefaultMaxBytes;
+    if (const char *v = std::getenv("AR_LL128_MIN_KB")) c->ll128_min_bytes = std::strtoll(v, nullptr, 10) * 1024;
+    c->ll128_min_bytes = std::max(0LL, c->ll128_min_bytes);
     if (const char *v = std::getenv("AR_LL128_MAX_KB")) c->ll128_max_bytes = std::strtoll(v, nullptr, 10) * 1024;
     c->ll128_max_bytes = std::max(0LL, c->ll128_max_bytes);
     if (c->ll_max_bytes > 0 || c->push_max_bytes > 0 || c->ll128_max_bytes > 0) {
@@ -2086,6 +2103,7 @@ int ar_comm_register(ar_comm *c, void *dptr, size_t bytes, void *blob_out) {
     b.ll_max_bytes = c->ll_max_bytes;
     b.push_max_bytes = c->push_max_bytes;
     b.ll128_max_bytes = c->ll128_max_bytes;
+    b.ll128_min_bytes = c->ll128_min_bytes;
     b.pid = (int64_t)getpid();
     b.device = c->device;
     b.raw_base = (uint64_t)(uintptr_t)base;
@@ -2133,9 +2151,9 @@ int ar_comm_open_peers(ar_comm *c, const void *blobs) {
       if (b->bytes != mine->bytes) throw InvalidArg("ranks registered buffers of different sizes");
       if (b->nctas != c->nctas || b->cta_cap != c->cta_cap || b->rpp != c->rpp || b->ll_cap_lines != c->ll_cap_lines ||
           b->ll_max_bytes != mine->ll_max_bytes || b->push_max_bytes != c->push_max_bytes ||
-          b->ll128_max_bytes != c->ll128_max_bytes)
+          b->ll128_max_bytes != c->ll128_max_bytes || b->ll128_min_bytes != c->ll128_min_bytes)
         throw InvalidArg("ranks disagree on communicator settings (ar_comm_set_ctas, AR_LL_MAX_KB, "
-                         "AR_LL128_MAX_KB, AR_PUSH_MAX_MB or the one-shot cut-off must be identical on every rank)");
+                         "AR_LL128_MIN_KB, AR_LL128_MAX_KB, AR_PUSH_MAX_MB or the one-shot cut-off must be identical on every rank)");
       if (t == c->proc) continue;
       const bool same_proc = b->pid == me_pid;
       if (same_proc && b->device != c->device) {
@@ -2228,6 +2246,31 @@ int ar_comm_attach_nvls(ar_comm *c, ar_nvls *nvls) {
     c->nvls = nvls;
     return AR_OK;
   })
+}
+
+int ar_default_paths(int32_t world, uint64_t *oneshot_max_bytes, uint64_t *ll128_min_bytes, uint64_t *ll128_max_bytes) {
+  if (world < 2 || world > AR_MAX_RANKS) {
+    set_error("world must be in [2, AR_MAX_RANKS]");
+    return AR_EINVAL;
+  }
+  long long a, b, c;
+  default_paths(world, &a, &b, &c);
+  if (oneshot_max_bytes) *oneshot_max_bytes = (uint64_t)a;
+  if (ll128_min_bytes) *ll128_min_bytes = (uint64_t)b;
+  if (ll128_max_bytes) *ll128_max_bytes = (uint64_t)c;
+  return AR_OK;
+}
+
+int ar_comm_get_paths(ar_comm *c, uint64_t *oneshot_max_bytes, uint64_t *ll128_min_bytes, uint64_t *ll128_max_bytes) {
+  if (!c) {
+    set_error("null comm");
+    return AR_EINVAL;
+  }
+  const bool on = c->ll_scratch != nullptr;   // emulated / several ranks per GPU: neither path
+  if (oneshot_max_bytes) *oneshot_max_bytes = on ? (uint64_t)c->ll_max_bytes : 0;
+  if (ll128_min_bytes) *ll128_min_bytes = on ? (uint64_t)std::min(c->ll128_min_bytes, c->ll_max_bytes) : 0;
+  if (ll128_max_bytes) *ll128_max_bytes = on && c->world <= 8 ? (uint64_t)c->ll128_max_bytes : 0;
+  return AR_OK;
 }
 
 int ar_comm_set_oneshot_max(ar_comm *c, uint64_t bytes) {
@@ -2486,36 +2529,8 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     check_local_extent(c, dptr,
                        (stride_override ? stride_override : ar_rank_stride_bytes(count, dtype)) * (c->world - 1) +
                            nbytes_call);
-  if (c->ll_opened && (long long)nbytes_call <= c->ll_max_bytes) {
-    // low-latency one-shot path for CPS-shaped plans (see ar_ll_kernel)
-    auto lit = c->ll_shape.find(plan->uid);
-    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
-    if (!lit->second.empty()) {
-      LLArgs la{};
-      la.buf = (char *)dptr;
-      for (int t = 0; t < c->world; t++) la.peer_scratch[t] = c->ll_peer[t];
-      la.my_scratch = c->ll_scratch;
-      for (int k = 0; k < c->world; k++) la.order[k] = lit->second[k];
-      la.bytes = (long long)nbytes_call;
-      la.cap_lines = c->ll_cap_lines;
-      la.me = c->rank;
-      la.world = c->world;
-      la.esize = plan->esize;
-      la.avg_n = avg_n;
-      la.epoch_dev = c->err + 3;
-      la.done_ctr = (unsigned int *)(c->err + 4);
-      la.err = c->err;
-      la.timeout_ns = c->timeout_ns;
-      const long long lines = (la.bytes + 7) / 8;
-      const int ctas = (int)std::max(1LL, std::min<long long>(c->ll_ctas, (lines + kThreads - 1) / kThreads));
-      ar_ll_kernel<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
-      CUDA_OK(cudaGetLastError());
-      c->last_launches = 1;
-      c->last_kernel = "ar_ll_kernel";
-      return AR_OK;
-    }
-  }
-  if (c->ll_opened && c->ll128_max_bytes > 0 && c->world <= 8 && (long long)nbytes_call > c->ll_max_bytes &&
+  if (c->ll_opened && c->ll128_max_bytes > 0 && c->world <= 8 &&
+      (long long)nbytes_call > std::min(c->ll128_min_bytes, c->ll_max_bytes) &&
       (long long)nbytes_call <= c->ll128_max_bytes && count % (uint64_t)c->world == 0 &&
       (count / c->world) * plan->esize % 16 == 0) {
     // LL128 two-shot path for CPS-shaped plans with equal 16-byte-aligned blocks (ar_ll128_kernel)
@@ -2549,6 +2564,35 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
       c->last_kernel = "ar_ll128_kernel";
+      return AR_OK;
+    }
+  }
+  if (c->ll_opened && (long long)nbytes_call <= c->ll_max_bytes) {
+    // low-latency one-shot path for CPS-shaped plans (see ar_ll_kernel)
+    auto lit = c->ll_shape.find(plan->uid);
+    if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
+    if (!lit->second.empty()) {
+      LLArgs la{};
+      la.buf = (char *)dptr;
+      for (int t = 0; t < c->world; t++) la.peer_scratch[t] = c->ll_peer[t];
+      la.my_scratch = c->ll_scratch;
+      for (int k = 0; k < c->world; k++) la.order[k] = lit->second[k];
+      la.bytes = (long long)nbytes_call;
+      la.cap_lines = c->ll_cap_lines;
+      la.me = c->rank;
+      la.world = c->world;
+      la.esize = plan->esize;
+      la.avg_n = avg_n;
+      la.epoch_dev = c->err + 3;
+      la.done_ctr = (unsigned int *)(c->err + 4);
+      la.err = c->err;
+      la.timeout_ns = c->timeout_ns;
+      const long long lines = (la.bytes + 7) / 8;
+      const int ctas = (int)std::max(1LL, std::min<long long>(c->ll_ctas, (lines + kThreads - 1) / kThreads));
+      ar_ll_kernel<<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      CUDA_OK(cudaGetLastError());
+      c->last_launches = 1;
+      c->last_kernel = "ar_ll_kernel";
       return AR_OK;
     }
   }

@@ -157,7 +157,8 @@ def main():
             failures += 1
         dist.barrier()
     # the one-shot cut-off is settable (ar_comm_set_oneshot_max): off, then raised to 2x
-    default_cut = min(1536 * 1024, (3 << 19) // (world - 1)) // 256 * 256
+    default_cut = G.default_paths(world)["oneshot_max"]
+    assert comm.paths()["oneshot_max"] == default_cut
     for cut, count in ((0, 3001), (2 * default_cut, (2 * default_cut) // 4 - 100)):
         comm.set_oneshot_max(cut)
         buf = torch.zeros(count * 4 + 16, dtype=torch.uint8, device="cuda")

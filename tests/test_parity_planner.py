@@ -297,6 +297,18 @@ def test_predict_executed_parity(shared):
     assert checked > 500
 
 
+def test_default_paths():
+    """The executor's default path cut-offs (ar_default_paths; measured): one-shot
+    to 1.5 MiB/(N-1) (at most 1.5 MiB), LL128 from 768 KiB/(N-1) (at most 384 KiB, never above
+    the one-shot cut-off) to 64 MiB/N, 256-byte / 1 MiB granularity."""
+    want = {2: (1536 << 10, 384 << 10, 32 << 20), 3: (768 << 10, 384 << 10, 21 << 20),
+            4: (512 << 10, 256 << 10, 16 << 20), 8: (224512, 112128, 8 << 20)}
+    for n, (om, lmin, lmax) in want.items():
+        assert G.default_paths(n) == {"oneshot_max": om, "ll128_min": lmin, "ll128_max": lmax}
+    with pytest.raises(G.ArInvalid):
+        G.default_paths(1)
+
+
 def test_nvls_plan_kind_parity():
     """NVLS as a GenTree plan kind (NEXT #1, readings NV1/NV2): force "nvls" and the
     min-GenModel choice gentree_plan_nvls give byte-identical plan JSON (CPS movement +
@@ -319,7 +331,8 @@ def test_nvls_plan_kind_parity():
             back = G.Plan.from_json(lp.to_json())
             assert back.to_json() == lp.to_json() and back.is_allreduce
             osp = OG.Params(4.61e-6, 2.963e-12, 0.0, 0.0, 0.0, 1)     # one-shot row (reading OS1)
-            cut = min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256
+            paths = G.default_paths(n)
+            cut = paths["oneshot_max"]
             for nvp in (nv_cheap, nv_dear):
                 lg = G.Plan.from_topology_nvls(doc, count, "f32", lib_params(pp), lib_params(nvp))
                 og, _ = GT.gentree_nvls(t, count, 4, pp, nvp)
@@ -328,11 +341,13 @@ def test_nvls_plan_kind_parity():
                 oo, _ = GT.gentree_nvls(t, count, 4, pp, nvp, osp, cut)
                 assert lo.to_json() == OP.plan_to_json(oo, "f32")
                 llp = OG.Params(5.1e-6, 1.74e-12, 0.0, 0.0, 0.0, 1)   # LL128 row
-                for c2 in (count, n * 4 * 4096):                      # ragged / aligned blocks
-                    l2 = G.Plan.from_topology_nvls(doc, c2, "f32", lib_params(pp), lib_params(nvp), lib_params(osp),
-                                                   cut, lib_params(llp), 16 << 20)
-                    o2, _ = GT.gentree_nvls(t, c2, 4, pp, nvp, osp, cut, llp, 16 << 20)
-                    assert l2.to_json() == OP.plan_to_json(o2, "f32")
+                # ragged / aligned blocks; below, between and above the LL128 floor and ceiling
+                for c2 in (count, n * 4 * 4096, n * 4 * 256, n * 4 * 16384, n * 4 * (1 << 20)):
+                    for lmin, lmax in ((0, 16 << 20), (paths["ll128_min"], paths["ll128_max"])):
+                        l2 = G.Plan.from_topology_nvls(doc, c2, "f32", lib_params(pp), lib_params(nvp),
+                                                       lib_params(osp), cut, lib_params(llp), lmax, lmin)
+                        o2, _ = GT.gentree_nvls(t, c2, 4, pp, nvp, osp, cut, llp, lmax, lmin)
+                        assert l2.to_json() == OP.plan_to_json(o2, "f32")
                 lb = G.Plan.from_topology_nvls(doc, count, "bf16", lib_params(pp), lib_params(nvp))
                 assert not lb.switch_reduce        # bf16 never takes NVLS
         # large messages: the cheap NVLS row ((N+1)/N·0.9 < 2(N-1)/N·1.465 per byte) wins at

@@ -17,6 +17,9 @@ import paper_2409_04202_b200 as G  # noqa: E402
 
 
 def cutoff(n):
+    """The one-shot cut-off in effect when the committed round-2 C2 data were measured (then the
+    one-shot path took every message up to it; since round 2's cut-off sweep the LL128 path
+    takes eligible messages from ar_default_paths' lower floor)."""
     return min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256
 
 

@@ -224,13 +224,14 @@ def multi(args):
                 fp, fn = fitted("genmodel_params.json"), fitted("genmodel_params_nvls.json")
                 fo = fitted("genmodel_fit_oneshot_graph.json")
                 fl = fitted("genmodel_fit_ll128_graph.json")
-                cut = min(1536 * 1024, (3 << 19) // (world - 1)) // 256 * 256   # the comm's default cut-off
+                paths = comm.paths()   # the path the executor takes decides the plan-side row
                 plan = G.Plan.from_topology_nvls(doc(world), count, args.dtype,
                                                  G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"],
                                                           fp["epsilon"], int(fp["w_t"])),
                                                  G.params(alpha=fn["alpha"], beta=fn["beta"]),
-                                                 G.params(alpha=fo["alpha"], beta=fo["beta"]), cut,
-                                                 G.params(alpha=fl["alpha"], beta=fl["beta"]), fl["max_bytes"])
+                                                 G.params(alpha=fo["alpha"], beta=fo["beta"]), paths["oneshot_max"],
+                                                 G.params(alpha=fl["alpha"], beta=fl["beta"]), paths["ll128_max"],
+                                                 paths["ll128_min"])
                 target, fill_fn = view, refill
                 if plan.switch_reduce:
                     if nvls_buf[0] is None:

@@ -38,7 +38,7 @@ def main():
     lj = json.load(open(os.path.join(P, "genmodel_fit_ll128_graph.json")))
     gp = G.params(pj["alpha"], pj["beta"], pj["gamma"], pj["delta"], pj["epsilon"], pj["w_t"])
     npar = G.params(alpha=nj["alpha"], beta=nj["beta"])
-    ll_max = min(1536 * 1024, (3 << 19) // (n - 1)) // 256 * 256   # executor default (exec.cu, init_comm)
+    paths = G.default_paths(n)   # the executor's default path cut-offs (ar_default_paths)
     rows = []
     for k in range(16, 31):
         nbytes = 1 << k
@@ -47,12 +47,13 @@ def main():
         kind = plan.report()[-1]["chosen"]
         op = G.params(alpha=oj["alpha"], beta=oj["beta"])
         lp = G.params(alpha=lj["alpha"], beta=lj["beta"])
-        if nbytes <= ll_max:
-            t_plan = G.genmodel_closed_form("oneshot", n, nbytes, op)["total"]
-            path = "one-shot"
-        elif nbytes <= lj["max_bytes"] and count % n == 0 and (count // n) * 4 % 16 == 0:
+        if (paths["ll128_min"] < nbytes <= paths["ll128_max"] and count % n == 0
+                and (count // n) * 4 % 16 == 0):
             t_plan = G.genmodel_closed_form("ll128", n, nbytes, lp)["total"]
             path = "LL128 two-shot"
+        elif nbytes <= paths["oneshot_max"]:
+            t_plan = G.genmodel_closed_form("oneshot", n, nbytes, op)["total"]
+            path = "one-shot"
         else:
             t_plan = plan.predict_executed(gp)["total"]
             path = f"{kind} (executed steps)"
@@ -61,7 +62,8 @@ def main():
             {"id": f"s{i}", "kind": "server", "parent": "sw",
              "uplink": {"alpha": 0, "beta": 1, "epsilon": 0, "w_t": 1}, "compute": {"gamma": 0, "delta": 0}}
             for i in range(n)]})
-        pick = G.Plan.from_topology_nvls(doc, count, "f32", gp, npar, op, ll_max, lp, lj["max_bytes"])
+        pick = G.Plan.from_topology_nvls(doc, count, "f32", gp, npar, op, paths["oneshot_max"], lp,
+                                         paths["ll128_max"], paths["ll128_min"])
         t_pick = c["t_nvls"] if pick.switch_reduce else t_plan
         rows.append({"bytes": nbytes, "gentree_plan": kind, "path": path, "t_pred_s": t_plan,
                      "busbw_pred": round(busbw(nbytes, n, t_plan), 1), "t_nvls_pred_s": c["t_nvls"],
