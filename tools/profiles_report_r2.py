@@ -26,9 +26,10 @@ def jload(path):
 
 
 def size(b):
-    if b >= 1 << 30:
-        return f"{b >> 30} GiB"
-    return f"{b >> 20} MiB" if b >= 1 << 20 else f"{b >> 10} KiB"
+    for shift, unit in ((30, "GiB"), (20, "MiB"), (10, "KiB")):
+        if b >= 1 << shift:
+            return f"{b / (1 << shift):g} {unit}"
+    return f"{b} B"
 
 
 def bench_section(out):
@@ -365,6 +366,32 @@ def split_section(out):
                "where the fitted row predicts it above 720 (profiles/README.md §11).\n")
 
 
+def cut_section(out):
+    d = os.path.join(P, "cut")
+    if not os.path.isdir(d):
+        return
+    out.append("## 12. Path cut-offs with the LL128 path in place (GenTree = CPS plan, graph timing; µs per call)\n")
+    out.append("`cut/def_*`: the cut-offs of the round-2 build (one-shot to 1.5 MiB/(N−1), LL128 above it to 16 MiB); "
+               "`cut/ll128all_*`: `AR_LL_MAX_KB=0 AR_LL128_MAX_KB=65536` (LL128 for every eligible size).  Sizes are "
+               "LL128-eligible (equal 16-byte-aligned blocks).  ★ = the faster by more than 2 %; the new defaults "
+               "(ar_default_paths: LL128 from 768 KiB/(N−1), at most 384 KiB, to 64 MiB/N) follow the ★s.\n")
+    for n in (4, 2):
+        for dt in ("f32", "bf16"):
+            a = {r["bytes"]: r for r in jl(os.path.join(d, f"def_n{n}_{dt}.jsonl"))}
+            b = {r["bytes"]: r for r in jl(os.path.join(d, f"ll128all_n{n}_{dt}.jsonl"))}
+            if not a or not b:
+                continue
+            out.append(f"**N = {n}, {dt}**\n")
+            out.append("| size | round-2 paths µs (busbw) | LL128 µs (busbw) |")
+            out.append("|---|---|---|")
+            for k in sorted(a):
+                ta, tb = a[k]["t_med"] * 1e6, b[k]["t_med"] * 1e6
+                sa = " ★" if ta * 1.02 < tb else ""
+                sb = " ★" if tb * 1.02 < ta else ""
+                out.append(f"| {size(k)} | {ta:.1f} ({a[k]['busbw_med']:.0f}){sa} | {tb:.1f} ({b[k]['busbw_med']:.0f}){sb} |")
+            out.append("")
+
+
 def main():
     out = ["# profiles/round2 — measured evidence (round 2)\n",
            "Generated by `tools/profiles_report_r2.py` from the files in this directory.  Commands:",
@@ -385,6 +412,7 @@ def main():
     nvls_sweep_section(out)
     nvls_bf16_section(out)
     split_section(out)
+    cut_section(out)
     print("\n".join(out))
 
 
