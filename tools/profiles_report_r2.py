@@ -77,13 +77,22 @@ def nccl_algo_section(out):
     out.append("")
 
 
+def final_c2(n, dt):
+    """The latest C2 run of the final executor: `r3_c2_*` (re-tuned path cut-offs, session 3),
+    else `final_c2_*`."""
+    return (jl(os.path.join(P, "c2", f"r3_c2_n{n}_{dt}.jsonl")) or
+            jl(os.path.join(P, "c2", f"final_c2_n{n}_{dt}.jsonl")))
+
+
 def c2_section(out):
     out.append("## 2. C2: fp32 busbw vs size — GenTree, GenTree incl. NVLS (path-aware min-GenModel pick), NCCL default / Ring / NVLS-off\n")
-    out.append("Our columns and NCCL default: the final executor (`final_c2_*`: one-shot ≤ 1.5 MiB/(N−1), LL128 two-shot to"
-               " 16 MiB, step-table kernel above); NCCL Ring / NVLS-off: separate processes with the variable set"
-               " (`c2_*_ncclring`, `c2_*_ncclnvlsoff`).  The first C2 run, before the LL128 path, is `c2_n*_f32.jsonl`.\n")
+    out.append("Our columns and NCCL default: the final executor (`r3_c2_*`: LL128 two-shot for equal 16-byte-aligned"
+               " blocks from 768 KiB/(N−1) (≤ 384 KiB) to 64 MiB/N, one-shot otherwise up to 1.5 MiB/(N−1), step-table"
+               " kernel above — §12); NCCL Ring / NVLS-off: separate processes with the variable set"
+               " (`c2_*_ncclring`, `c2_*_ncclnvlsoff`).  Earlier runs: `final_c2_*` (LL128 only above the one-shot"
+               " cut-off, to 16 MiB), `c2_n*_f32.jsonl` (before the LL128 path).\n")
     for n in (4, 2):
-        ours = jl(os.path.join(P, "c2", f"final_c2_n{n}_f32.jsonl")) or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
+        ours = final_c2(n, "f32") or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
         if not ours:
             continue
         ring = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclring.jsonl"))
@@ -114,7 +123,7 @@ def c2_section(out):
 
 
 def bf16_section(out):
-    rows4 = jl(os.path.join(P, "c2", "final_c2_n4_bf16.jsonl"))
+    rows4 = final_c2(4, "bf16")
     if not rows4:
         return
     out.append("**bf16, graph timing, final executor: GenTree plan vs NCCL default (busbw GB/s)**\n")
@@ -122,7 +131,7 @@ def bf16_section(out):
     out.append("|---|---|---|---|---|---|---|")
     d = {}
     for n in (4, 2):
-        rows = jl(os.path.join(P, "c2", f"final_c2_n{n}_bf16.jsonl"))
+        rows = final_c2(n, "bf16")
         d[n] = ({r["bytes"]: r["busbw_med"] for r in rows if r["impl"] == "ours"},
                 {r["bytes"]: r["busbw_med"] for r in rows if r["impl"] == "nccl"})
     for b in sorted(d[4][0]):
@@ -139,7 +148,7 @@ def pick_section(out):
     predicted on the row of the path the executor takes (gentree_plan_nvls with the OS1 and
     LL128 rows)."""
     for n in (4, 2):
-        final = jl(os.path.join(P, "c2", f"final_c2_n{n}_f32.jsonl"))
+        final = final_c2(n, "f32")
         pk = [r for r in final if r.get("plan") == "gentree+nvls"] or jl(os.path.join(P, "c2", f"c2pick_n{n}_f32.jsonl"))
         base = final or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
         ring = jl(os.path.join(P, "c2", f"c2_n{n}_f32_ncclring.jsonl"))
