@@ -401,6 +401,37 @@ def cut_section(out):
             out.append("")
 
 
+def llsplit_section(out):
+    import glob
+    files = sorted(glob.glob(os.path.join(P, "llsplit", "b_n*.jsonl")))
+    if not files:
+        return
+    out.append("## 13. One CPS message split between the LL128 and the step-table kernel (fp32, `tools/ll128_exec_split.py`)\n")
+    out.append("The first x·S bytes through the LL128 kernel (AR_LL128_MAX_KB=262144), the rest (one element short of "
+               "equal blocks) through the step-table kernel with 100 CTAs (`SPLIT_EXEC_CTAS=100`; LL128 then gets ≤ 300), "
+               "concurrently on two streams; x = 0 and 1 are the LL128 kernel alone.  With the step-table kernel at "
+               "148 CTAs both kernels cannot be resident together and the run deadlocks into the flag timeout (a "
+               "resident LL128 CTA waits for a peer's unscheduled one) — the same residency rule the LL128 path "
+               "already enforces.  busbw GB/s:\n")
+    shares = (0, 0.1, 0.2, 0.3, 0.4, 0.5, 1)
+    out.append("| N | size | " + " | ".join(f"x = {x:g}" for x in shares) + " | C2 (r3, default paths) |")
+    out.append("|---|---|" + "---|" * (len(shares) + 1))
+    for f in files:
+        rows = jl(f)
+        n = rows[0]["n"]
+        c2 = {r["bytes"]: r["busbw_med"] for r in final_c2(n, "f32")
+              if r.get("timing") == "graph" and r["impl"] == "ours" and r["plan"] == "gentree"}
+        for b in sorted({r["bytes"] for r in rows}):
+            d = {r["ll128_share"]: r["busbw_med"] for r in rows if r["bytes"] == b}
+            out.append(f"| {n} | {size(b)} | " + " | ".join(f"{d[x]:.0f}" if x in d else "-" for x in shares) +
+                       f" | {c2.get(b, float('nan')):.0f} |")
+    out.append("")
+    out.append("No split beats the default path (the step-table kernel at 148 CTAs above the LL128 ceiling): the "
+               "LL128 kernel alone falls to ≈ 390–520 GB/s from 64 MiB (its 128-byte lines pass through the "
+               "owner's HBM scratch), and the step-table kernel's fixed per-call cost is already small against "
+               "these sizes.  Not adopted.\n")
+
+
 def main():
     out = ["# profiles/round2 — measured evidence (round 2)\n",
            "Generated by `tools/profiles_report_r2.py` from the files in this directory.  Commands:",
@@ -422,6 +453,7 @@ def main():
     nvls_bf16_section(out)
     split_section(out)
     cut_section(out)
+    llsplit_section(out)
     print("\n".join(out))
 
 
