@@ -28,12 +28,21 @@ def main():
     ap.add_argument("files", nargs="+")
     ap.add_argument("--timing", default="graph")
     ap.add_argument("--max-bytes", type=int, default=16 << 20)
+    ap.add_argument("--paths", choices=["round2", "current"], default="round2",
+                    help="which LL128 range the data were measured with: round2 = (one-shot cut-off, "
+                         "--max-bytes]; current = ar_default_paths' (ll128_min, ll128_max]")
     a = ap.parse_args()
     rows = []
     for f in a.files:
         rows += [json.loads(l) for l in open(f) if l.startswith("{")]
+    def in_range(n, b):
+        if a.paths == "current":
+            d = G.default_paths(n)
+            return d["ll128_min"] < b <= d["ll128_max"]
+        return oneshot_cutoff(n) < b <= a.max_bytes
+
     sel = [r for r in rows if r.get("timing") == a.timing and r["plan"] == "gentree" and r.get("impl", "ours") == "ours"
-           and oneshot_cutoff(r["n"]) < r["bytes"] <= a.max_bytes and r["bytes"] % (r["n"] * 16) == 0]
+           and in_range(r["n"], r["bytes"]) and r["bytes"] % (r["n"] * 16) == 0]
     fit_rows = [(r["n"], r["bytes"], r["t_mean"]) for r in sel]
     p, sse = G.genmodel_fit_row("ll128", fit_rows)
     errs = []
@@ -56,7 +65,7 @@ def main():
             cross[f"fit_n{fit_n}"] = {"alpha": pf.alpha, "beta": pf.beta, "heldout_rows": len(ev),
                                       "heldout_err_median": sorted(ev)[len(ev) // 2], "heldout_err_max": max(ev)}
     out = {"timing": a.timing, "rows": len(errs), "alpha": p.alpha, "beta": p.beta, "cross_n": cross,
-           "line_gbs": 1 / p.beta / 1e9 if p.beta > 0 else None, "sse": sse, "max_bytes": a.max_bytes,
+           "line_gbs": 1 / p.beta / 1e9 if p.beta > 0 else None, "sse": sse, "max_bytes": a.max_bytes, "paths": a.paths,
            "pred_err_median": e[len(e) // 2], "pred_err_max": e[-1], "points": errs, "sources": a.files}
     json.dump(out, open(os.path.join(ROOT, "profiles", f"genmodel_fit_ll128_{a.timing}.json"), "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k not in ("points", "sources")}, indent=1))
