@@ -533,6 +533,12 @@ def main():
                      "model": ("GenModel of the executed steps, all ranks sharing one HBM (reading A6e)" if n == 1
                                else "GenModel of the executed (fused, full-duplex) steps (reading A6x)"),
                      "validation_held_out": fp.get("validation")},
+        # busbw (nccl-tests) is a per-rank figure: the bus bandwidth every rank sustains, which a
+        # bandwidth-optimal AllReduce keeps flat in the rank count — so `value` is not expected
+        # to grow with N.  The job-wide figure is the sum over the ranks.
+        "value_semantics": "busbw per rank (nccl-tests: S/t x 2(R-1)/R); not additive over GPUs",
+        "aggregate_busbw": {"value": round(value * world, 2), "unit": "GB/s",
+                            "note": f"sum over the {world} ranks ({'all on one GPU' if n == 1 else 'one per GPU'})"},
         "busbw_per_step_min_median_max": [round(busbw(nbytes, world, max(per_step)), 2),
                                           round(busbw(nbytes, world, statistics.median(per_step)), 2),
                                           round(busbw(nbytes, world, min(per_step)), 2)],

@@ -375,3 +375,26 @@ def test_multi_level_same_process(nproc, R):
     finally:
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_path_choice_follows_the_cutoffs(world):
+    """The executor's path for CPS-shaped plans follows the communicator's cut-offs
+    (ar_comm_get_paths = ar_default_paths by default): LL128 for equal 16-byte-aligned blocks in
+    (ll128_min, ll128_max] — ahead of the one-shot path — one-shot up to oneshot_max otherwise,
+    the step-table kernel above; every path with the plan's bits."""
+    paths = G.default_paths(world)
+    sp = SameProcess(world, paths["ll128_max"] + (1 << 20))
+    try:
+        assert sp.comms[0].paths() == paths
+        unit = world * 4                                   # fp32: blocks of whole 16-byte vectors
+        lo, hi = paths["ll128_min"] // 4 // unit * unit, paths["ll128_max"] // 4 // unit * unit
+        cases = [(lo, "ar_ll_kernel"),                     # at the floor: one-shot
+                 (lo + unit, "ar_ll128_kernel"),           # just above: LL128
+                 (lo + unit + 1, "ar_ll_kernel"),          # ragged blocks: one-shot
+                 (hi, "ar_ll128_kernel"),                  # the ceiling
+                 (hi + unit, "ar_exec_kernel")]            # above it
+        for count, kern in cases:
+            check(sp, world, count, "f32", None, expect_kernel=kern)
+    finally:
+        sp.destroy()
