@@ -50,7 +50,7 @@ def main():
     failures = 0
     for dtype in ("f32", "bf16"):
         es = 4 if dtype == "f32" else 2
-        for count in (1, world * 4096 + 5, 1 << 20, 3_000_001):
+        for count in (1, world * 4096 + 5, world * 4 * 40000, 1 << 20, 3_000_001):
             buf = torch.zeros(max(16, count * es), dtype=torch.uint8, device="cuda")
             keep.append(buf)
             comm.register(buf)

@@ -38,9 +38,12 @@ def test_nvls_in_switch_reduction(world):
 
 
 @pytest.mark.parametrize("jitter", [0, 20000])
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_multi_process_bit_exact(world, jitter):
-    """jitter > 0: random delays (ns) before every flag post on every GPU."""
+    """jitter > 0: random delays (ns) before every flag post on every GPU.
+    world = 3: a rank count that is not a power of two (no RHD; LL128 blocks of N·4 elements)."""
+    if world == 3 and jitter:
+        pytest.skip("N = 3 runs without jitter only (time)")
     if ngpus() < world:
         pytest.skip(f"needs {world} GPUs")
     env = dict(os.environ, AR_FLAG_TIMEOUT_MS="20000", PYTHONPATH=ROOT, AR_JITTER_NS=str(jitter))
