@@ -7,6 +7,7 @@ reports, ncu summaries)."""
 import glob
 import json
 import os
+import sys
 import statistics
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -432,6 +433,40 @@ def llsplit_section(out):
                "these sizes.  Not adopted.\n")
 
 
+def simu_baselines_section(out):
+    """Desk analysis of tab:gentreesimu: each baseline is one fixed plan, so its
+    time is affine in S; the intercept is its latency term."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from tools.gentreesimu import PAPER
+    a = 6.58e-3
+    out.append("## 14. What tab:gentreesimu's rows fix (desk analysis of the printed table, P:1144-1190)\n")
+    out.append("Every baseline is one fixed plan, so its time is affine in S: T = A + K·S.  Fitted through the "
+               "1e7 and 1e8 points, each baseline predicts its printed 3.2e7 point to ±0.1 %, and A is an exact "
+               "multiple of the printed α = 6.58e-3 s (CDC384: of α_cross = 3e-2 plus 4α):\n")
+    out.append("| topology | plan | A (s) | A / α | K (s per float) | 3.2e7: affine vs printed |")
+    out.append("|---|---|---|---|---|---|")
+    for topo, rows in PAPER.items():
+        for alg, (t1, t2, t3) in rows.items():
+            k = (t3 - t1) / 9e7
+            aa = t1 - k * 1e7
+            out.append(f"| {topo} | {alg} | {aa:.4f} | {aa / a:.2f} | {k:.4e} | {(aa + k * 3.2e7) / t2 - 1:+.2%} |")
+    out.append("")
+    out.append("Readings: (i) on one switch every step costs 3α (CPS 2 steps → 6α, RHD(32) 10 steps → 30α) — "
+               "reading Q16's α_eff = 3α — but Ring costs 2N steps (144α at N = 24, 192α at 32), two more than "
+               "2(N−1): the 4 % by which the flow simulator's Ring rows sit low (§7 of ../README.md) is exactly "
+               "2 × 3α; (ii) on the two-level trees a step costs 5α (CPS 10α; Ring 400α = 80 × 5α on SYM384 and "
+               "ASY384, 480α = 96 × 5α on SYM512, i.e. (2·24 + 2·16) and (2·32 + 2·16) steps of a per-switch "
+               "ring) and on CDC384 α_cross + 4α = 0.0563 s (CPS 2 steps, Ring 80 steps): the paper charges "
+               "every step the α summed along the tree's longest server-to-server path, whatever the step's "
+               "own path; (iii) GenTree's rows are not affine (its plan changes with S).  The slopes K are not "
+               "reproduced by the readings checked (the flow simulator's flat and per-switch baselines, and by "
+               "hand for flat CPS on SYM384: incast counted per flow, per source or per receiver, max-min or "
+               "summed over hops): e.g. flat CPS on SYM384 is 2.2e-7 s/float printed against ≈ 1.05e-7 for "
+               "incast-bound max-min on the server links — the "
+               "unreleased simulator's bandwidth model for multi-level trees stays unknown, so the hierarchical "
+               "rows remain reported, not pinned.\n")
+
+
 def main():
     out = ["# profiles/round2 — measured evidence (round 2)\n",
            "Generated by `tools/profiles_report_r2.py` from the files in this directory.  Commands:",
@@ -454,6 +489,7 @@ def main():
     split_section(out)
     cut_section(out)
     llsplit_section(out)
+    simu_baselines_section(out)
     print("\n".join(out))
 
 
