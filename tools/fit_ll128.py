@@ -28,6 +28,9 @@ def main():
     ap.add_argument("files", nargs="+")
     ap.add_argument("--timing", default="graph")
     ap.add_argument("--max-bytes", type=int, default=16 << 20)
+    ap.add_argument("--stat", choices=["t_mean", "t_med"], default="t_mean",
+                    help="timing statistic fitted and compared (the paper reports means, P:227; the "
+                         "median is robust to a disturbed graph replay)")
     ap.add_argument("--paths", choices=["round2", "current"], default="round2",
                     help="which LL128 range the data were measured with: round2 = (one-shot cut-off, "
                          "--max-bytes]; current = ar_default_paths' (ll128_min, ll128_max]")
@@ -43,29 +46,41 @@ def main():
 
     sel = [r for r in rows if r.get("timing") == a.timing and r["plan"] == "gentree" and r.get("impl", "ours") == "ours"
            and in_range(r["n"], r["bytes"]) and r["bytes"] % (r["n"] * 16) == 0]
-    fit_rows = [(r["n"], r["bytes"], r["t_mean"]) for r in sel]
+    fit_rows = [(r["n"], r["bytes"], r[a.stat]) for r in sel]
     p, sse = G.genmodel_fit_row("ll128", fit_rows)
     errs = []
     for r in sel:
         pred = G.genmodel_closed_form("ll128", r["n"], r["bytes"], p)["total"]
-        errs.append({"n": r["n"], "bytes": r["bytes"], "measured_s": r["t_mean"], "predicted_s": pred,
-                     "rel_err": abs(pred - r["t_mean"]) / r["t_mean"]})
+        errs.append({"n": r["n"], "bytes": r["bytes"], "measured_s": r[a.stat], "predicted_s": pred,
+                     "rel_err": abs(pred - r[a.stat]) / r[a.stat]})
     e = sorted(x["rel_err"] for x in errs)
     # held out across the rank count: fit on one N, predict the other
     cross = {}
     ns = sorted({r["n"] for r in sel})
     for fit_n in ns:
-        rows_f = [(r["n"], r["bytes"], r["t_mean"]) for r in sel if r["n"] == fit_n]
+        rows_f = [(r["n"], r["bytes"], r[a.stat]) for r in sel if r["n"] == fit_n]
         if len({b for _, b, _ in rows_f}) < 2:
             continue
         pf, _ = G.genmodel_fit_row("ll128", rows_f)
-        ev = [abs(G.genmodel_closed_form("ll128", r["n"], r["bytes"], pf)["total"] - r["t_mean"]) / r["t_mean"]
+        ev = [abs(G.genmodel_closed_form("ll128", r["n"], r["bytes"], pf)["total"] - r[a.stat]) / r[a.stat]
               for r in sel if r["n"] != fit_n]
         if ev:
             cross[f"fit_n{fit_n}"] = {"alpha": pf.alpha, "beta": pf.beta, "heldout_rows": len(ev),
                                       "heldout_err_median": sorted(ev)[len(ev) // 2], "heldout_err_max": max(ev)}
-    out = {"timing": a.timing, "rows": len(errs), "alpha": p.alpha, "beta": p.beta, "cross_n": cross,
-           "line_gbs": 1 / p.beta / 1e9 if p.beta > 0 else None, "sse": sse, "max_bytes": a.max_bytes, "paths": a.paths,
+    # per rank count: the protocol's fixed cost grows with N (a rank waits for the lines of N − 1
+    # peers), which one (α, β) pair over all N cannot express; consumers take the row of their N
+    # when it was measured (tools/harness.py, tools/predict8.py fall back to the pooled row)
+    per_n = {}
+    for fn in ns:
+        rows_f = [(r["n"], r["bytes"], r[a.stat]) for r in sel if r["n"] == fn]
+        if len({b for _, b, _ in rows_f}) < 2:
+            continue
+        pf, _ = G.genmodel_fit_row("ll128", rows_f)
+        ev = sorted(abs(G.genmodel_closed_form("ll128", n_, b_, pf)["total"] - t_) / t_ for n_, b_, t_ in rows_f)
+        per_n[str(fn)] = {"alpha": pf.alpha, "beta": pf.beta, "rows": len(rows_f),
+                          "err_median": ev[len(ev) // 2], "err_max": ev[-1]}
+    out = {"timing": a.timing, "rows": len(errs), "alpha": p.alpha, "beta": p.beta, "per_n": per_n, "cross_n": cross,
+           "line_gbs": 1 / p.beta / 1e9 if p.beta > 0 else None, "sse": sse, "max_bytes": a.max_bytes, "paths": a.paths, "stat": a.stat,
            "pred_err_median": e[len(e) // 2], "pred_err_max": e[-1], "points": errs, "sources": a.files}
     json.dump(out, open(os.path.join(ROOT, "profiles", f"genmodel_fit_ll128_{a.timing}.json"), "w"), indent=1)
     print(json.dumps({k: v for k, v in out.items() if k not in ("points", "sources")}, indent=1))

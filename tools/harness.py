@@ -224,6 +224,7 @@ def multi(args):
                 fp, fn = fitted("genmodel_params.json"), fitted("genmodel_params_nvls.json")
                 fo = fitted("genmodel_fit_oneshot_graph.json")
                 fl = fitted("genmodel_fit_ll128_graph.json")
+                fl = fl.get("per_n", {}).get(str(world), fl)   # the row fitted at this rank count
                 paths = comm.paths()   # the path the executor takes decides the plan-side row
                 plan = G.Plan.from_topology_nvls(doc(world), count, args.dtype,
                                                  G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"],

@@ -36,6 +36,9 @@ def main():
     nj = json.load(open(os.path.join(P, "genmodel_params_nvls.json")))
     oj = json.load(open(os.path.join(P, "genmodel_fit_oneshot_graph.json")))
     lj = json.load(open(os.path.join(P, "genmodel_fit_ll128_graph.json")))
+    per_n = lj.get("per_n", {})
+    if per_n:   # the row fitted at n ranks, else at the largest measured rank count
+        lj = dict(lj, **per_n.get(str(n), per_n[max(per_n, key=int)]))
     gp = G.params(pj["alpha"], pj["beta"], pj["gamma"], pj["delta"], pj["epsilon"], pj["w_t"])
     npar = G.params(alpha=nj["alpha"], beta=nj["beta"])
     paths = G.default_paths(n)   # the executor's default path cut-offs (ar_default_paths)
@@ -72,8 +75,8 @@ def main():
                      "pick_busbw_pred": round(busbw(nbytes, n, t_pick), 1)})
     out = {"tool": "predict8", "world": n, "dtype": "f32", "kind": "GenModel prediction, not a measurement",
            "params": pj["source"], "nvls_params": nj["source"], "oneshot_params": "genmodel_fit_oneshot_graph.json",
-           "ll128_params": "genmodel_fit_ll128_graph.json",
-           "oneshot_max_bytes": ll_max,
+           "ll128_params": "genmodel_fit_ll128_graph.json (the row of the largest measured rank count)",
+           "paths": paths,
            "fit_range": "parameters fitted on CPS rows at N = 2..4 (w_t >= 4, eps = 0: no incast seen up to the 4-GPU lease)",
            "context": "NCCL 8-rank all-reduce busbw 725 GB/s at 1 GiB on B200 (B200_PROFILING.md)",
            "rows": rows}
