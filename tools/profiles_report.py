@@ -369,8 +369,10 @@ def predict8_section(out):
         return
     d = json.load(open(path))
     out.append(f"## 11. GenModel prediction for C2 at {d['world']} x B200 (not measured: no 8-GPU lease here)\n")
+    pth = d.get("paths") or {"oneshot_max": d.get("oneshot_max_bytes", 0), "ll128_min": 0, "ll128_max": 0}
     out.append(f"`tools/predict8.py`: GenTree's plan and the fitted executed-plan model ({d['params']}; one-shot row\n"
-               f"below {d['oneshot_max_bytes'] >> 10} KiB), and the fitted NVLS row ({d['nvls_params']}).  "
+               f"up to {pth['oneshot_max'] >> 10} KiB, LL128 row for {pth['ll128_min'] >> 10} KiB < S <= "
+               f"{pth['ll128_max'] >> 20} MiB), and the fitted NVLS row ({d['nvls_params']}).  "
                f"{d['fit_range']}.\n")
     out.append("| size | GenTree plan | path | predicted busbw GB/s | NVLS row predicted busbw GB/s |")
     out.append("|---|---|---|---|---|")
