@@ -2830,7 +2830,11 @@ int allreduce_exec_host(const gt_plan *plan, ar_comm *c, void *dptr, void *host,
     const size_t bytes = c->rpp > 1 ? ar_rank_stride_bytes(count, dtype) * c->rpp
                                     : count * (size_t)(dtype == AR_BF16 ? 2 : 4);
     cudaStream_t s = (cudaStream_t)stream;
-    int chunks = 8;
+    // chunks of >= 4 MiB per rank, at most 32: the copies of the first and last chunk cannot
+    // overlap anything, so more chunks shorten that fill/drain (bench N = 1, 8 x 256 MiB:
+    // 8 / 16 / 32 / 64 chunks -> 9.89 / 10.29 / 10.42 / 10.32 GB/s busbw end to end)
+    const uint64_t per_rank = count * (uint64_t)plan->esize;
+    int chunks = (int)std::min<uint64_t>(32, std::max<uint64_t>(2, per_rank / (4u << 20)));
     if (const char *v = std::getenv("AR_E2E_CHUNKS")) chunks = std::max(1, std::atoi(v));
     if (chunks > 1 && count * (uint64_t)plan->esize >= (8u << 20) && (uint64_t)plan->plan.count == count &&
         plan->dtype == dtype && ascending_cps(plan->plan)) {
