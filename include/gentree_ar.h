@@ -121,7 +121,7 @@ int gentree_plan(const char *topology_json, uint64_t count, int32_t dtype, const
  * single-switch topology with dtype AR_F32 replaces it by the NVLS plan when the NVLS row
  * predicts less time than the path the executor would run the plan on (the communicator's
  * cut-offs, ar_comm_get_paths / ar_default_paths): the LL128 row (`ll128_params`) when
- * given, the plan is one-shot eligible with equal 16-byte-aligned blocks, N <= 8 and
+ * given, the plan is one-shot eligible, N <= 8, count·esize >= 8N and
  * min(ll128_min_bytes, oneshot_max_bytes) < count·esize <= ll128_max_bytes; else the one-shot
  * row (reading OS1, `oneshot_params`) when given, the plan is one-shot eligible and
  * count·esize <= oneshot_max_bytes; else the executed-plan prediction
@@ -281,8 +281,9 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
  * previous launch left.  Every element of every rank's buffer ends
  * equal to the plan's left-to-right fp32 sum of the ranks' inputs (bit-exact to the CPU
  * oracle).  One rank per GPU, CPS-shaped plans take a flag-free path by size: the one-shot
- * LL128 two-shot kernel (flags inside 128-byte lines) when the blocks are equal and 16-byte
- * aligned and the message lies in its range (ar_comm_get_paths), else the one-shot kernel up
+ * LL128 two-shot kernel (flags inside 128-byte lines, its own block partition: any count,
+ * 8-byte-aligned buffer) when the message lies in its range (ar_comm_get_paths), else the
+ * one-shot kernel up
  * to the one-shot cut-off, else the step-table kernel — all with the plan's bits (ar_comm_last_kernel tells which).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
  * plan's, unregistered or misaligned buffer; AR_ESYS on launch failure. */
 int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
@@ -324,8 +325,8 @@ int ar_comm_last_launch_count(ar_comm *comm, int32_t *kernels);
 const char *ar_comm_last_kernel(ar_comm *comm);
 
 /* Path cut-offs (bytes per rank) of CPS-shaped plans on a one-rank-per-GPU communicator:
- * messages with equal 16-byte-aligned blocks (and N <= 8) in (ll128_min, ll128_max] take the
- * LL128 two-shot kernel; otherwise messages up to oneshot_max take the one-shot kernel;
+ * messages in (ll128_min, ll128_max] take the LL128 two-shot kernel (N <= 8, 8-byte-aligned
+ * buffer); otherwise messages up to oneshot_max take the one-shot kernel;
  * everything else the step-table kernel.  ar_default_paths gives the defaults for `world`
  * ranks, measured on 2 and 4 B200s (one-shot to 1.5 MiB/(N−1); LL128 from 768 KiB/(N−1),
  * at most 384 KiB, to 64 MiB/N); AR_LL_MAX_KB, AR_LL128_MIN_KB and AR_LL128_MAX_KB override

@@ -417,8 +417,8 @@ def gentree_nvls(topo, count: int, esize: int, params: Params, nvls_params: Para
     minimum-GenModel choice): on a single-switch topology in fp32, the NVLS plan
     replaces GenTree's plan iff the NVLS row's closed form (P:441-444 with its own α, β) is
     strictly below the prediction of the path the executor runs GenTree's plan on — the
-    LL128 row for one-shot-eligible plans with equal 16-byte-aligned blocks, N <= 8 and a size
-    in (min(ll128_min_bytes, oneshot_max_bytes), ll128_max_bytes] when its parameters are
+    LL128 row for one-shot-eligible plans with N <= 8, at least 8 bytes per rank and block, and
+    a size in (min(ll128_min_bytes, oneshot_max_bytes), ll128_max_bytes] when its parameters are
     given, else the one-shot row (reading OS1) for one-shot-eligible plans up to
     oneshot_max_bytes when given, else the executed-plan prediction (ties keep the plan).
     The cut-offs are the executor's (a measured engineering choice, not the paper's)."""
@@ -429,8 +429,8 @@ def gentree_nvls(topo, count: int, esize: int, params: Params, nvls_params: Para
         t_plan = predict_executed(plan, esize, params)["total"]
         n = len(topo.servers)
         S = count * esize
-        if (ll128_params is not None and oneshot_eligible(plan) and n <= 8 and count % n == 0
-                and (count // n) * esize % 16 == 0 and min(ll128_min_bytes, oneshot_max_bytes) < S <= ll128_max_bytes):
+        if (ll128_params is not None and oneshot_eligible(plan) and n <= 8 and S >= 8 * n
+                and min(ll128_min_bytes, oneshot_max_bytes) < S <= ll128_max_bytes):
             t_plan = closed_form_f64("ll128", n, S, ll128_params)["total"]
         elif oneshot_params is not None and S <= oneshot_max_bytes and oneshot_eligible(plan):
             t_plan = closed_form_f64("oneshot", n, S, oneshot_params)["total"]

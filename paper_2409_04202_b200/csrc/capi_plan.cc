@@ -271,11 +271,11 @@ int gentree_plan_nvls(const char *topology_json, uint64_t count, int32_t dtype, 
       const int64_t S = (int64_t)count * esize_of(dtype);
       const bool eligible = !oneshot_order(g->plan).empty();
       const int n = g->plan.n;
-      const bool ll128_ok = eligible && n <= 8 && count % (uint64_t)n == 0 && (count / n) * esize_of(dtype) % 16 == 0 &&
+      const bool ll128_ok = eligible && n <= 8 && (uint64_t)S >= 8ull * n &&
                             (uint64_t)S > std::min(ll128_min_bytes, oneshot_max_bytes) && (uint64_t)S <= ll128_max_bytes;
       if (ll128_params && ll128_ok) {
-        // the executor runs this plan through its LL128 two-shot path (equal, 16-byte-aligned
-        // blocks, above the LL128 floor): compare that row instead
+        // the executor runs this plan through its LL128 two-shot path (above the LL128 floor):
+        // compare that row instead
         tp = closed_form_f64("ll128", n, S, to_params(ll128_params), {}).total;
         use = tn < tp ? 1 : 0;
       } else if (oneshot_params && (uint64_t)S <= oneshot_max_bytes && eligible) {

@@ -1142,8 +1142,11 @@ struct LL128Args {
   char *peer_scr[AR_MAX_RANKS];           // rank -> its LL128 region as seen here
   char *my_scr;
   int order[AR_MAX_RANKS];                // the plan's summation order
-  long long blk_bytes;                    // bytes per block (all blocks equal, multiple of 16)
-  long long lines;                        // 128-byte lines per block
+  // the LL128 partition (not the plan's: a CPS-shaped plan's bits do not depend on which rank
+  // sums an element): blocks 0..N-2 of blk_bytes (a multiple of 8), block N-1 the rest
+  long long blk_bytes;                    // bytes of blocks 0..N-2
+  long long lines;                        // 128-byte lines of blocks 0..N-2
+  long long last_bytes, last_lines;       // block N-1 (blk_bytes <= last_bytes < blk_bytes + 8N)
   long long lines_cap;                    // lines per (parity, area, source) slot
   int me, world, esize, avg_n;
   unsigned long long *epoch_dev;          // last completed LL128 call (device-resident)
@@ -1163,19 +1166,38 @@ __device__ __forceinline__ void ld_vol_v2u64(const void *p, unsigned long long &
 __device__ __forceinline__ char *ll128_line(char *base, const LL128Args &a, int par, int area, int src, long long i) {
   return base + ((((long long)par * 2 + area) * a.world + src) * a.lines_cap + i) * kLineBytes;
 }
+// An 8-byte payload word at p with `rem` bytes of the block left from p: whole words directly,
+// the block's last partial word (2, 4 or 6 bytes: elements are 2 or 4 bytes) element-pairwise
+// out of line (at most one word per block), bytes past the block's end as 0 (never stored back)
+__device__ __forceinline__ unsigned long long ll128_ld_partial(const char *p, int rem) {
+  unsigned long long w = 0ull;
+  for (int k = 0; k < rem; k += 2) w |= (unsigned long long)*(const unsigned short *)(p + k) << (8 * k);
+  return w;
+}
+__device__ __forceinline__ void ll128_st_partial(char *p, int rem, unsigned long long w) {
+  for (int k = 0; k < rem; k += 2) *(unsigned short *)(p + k) = (unsigned short)(w >> (8 * k));
+}
+__device__ __forceinline__ unsigned long long ll128_ld_word(const char *p, long long rem) {
+  if (rem >= 8) return *(const unsigned long long *)p;
+  return rem > 0 ? ll128_ld_partial(p, (int)rem) : 0ull;
+}
+__device__ __forceinline__ void ll128_st_word(char *p, long long rem, unsigned long long w) {
+  if (rem >= 8) *(unsigned long long *)p = w;
+  else if (rem > 0) ll128_st_partial(p, (int)rem, w);
+}
 // this lane's payload words of line i of a block that starts at `blk` (part j < 7: bytes
-// 16j..16j+15, part 7: bytes 112..119); words past the block's end read as 0
+// 16j..16j+15, part 7: bytes 112..119)
 __device__ __forceinline__ void ll128_payload(const char *blk, long long blk_bytes, long long i, int j,
                                               unsigned long long &w0, unsigned long long &w1) {
   const long long o = i * kLinePayload + 16LL * j;
-  w0 = o + 8 <= blk_bytes ? *(const unsigned long long *)(blk + o) : 0ull;
-  w1 = (j < 7 && o + 16 <= blk_bytes) ? *(const unsigned long long *)(blk + o + 8) : 0ull;
+  w0 = ll128_ld_word(blk + o, blk_bytes - o);
+  w1 = j < 7 ? ll128_ld_word(blk + o + 8, blk_bytes - o - 8) : 0ull;
 }
 __device__ __forceinline__ void ll128_store_payload(char *blk, long long blk_bytes, long long i, int j,
                                                     unsigned long long w0, unsigned long long w1) {
   const long long o = i * kLinePayload + 16LL * j;
-  if (o + 8 <= blk_bytes) *(unsigned long long *)(blk + o) = w0;
-  if (j < 7 && o + 16 <= blk_bytes) *(unsigned long long *)(blk + o + 8) = w1;
+  ll128_st_word(blk + o, blk_bytes - o, w0);
+  if (j < 7) ll128_st_word(blk + o + 8, blk_bytes - o - 8, w1);
 }
 // Load line i from a scratch slot until its flag (lane 7 of the 8-lane group, second word)
 // equals `flag`.  Every lane of the warp runs the loop (__any_sync); lanes without a line
@@ -1221,7 +1243,7 @@ __device__ __forceinline__ void ll128_pack(const float (&acc)[8], unsigned long 
 }
 
 template <bool BF16>
-__global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constant__ LL128Args a) {
+__global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_constant__ LL128Args a) {
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
   __syncthreads();
@@ -1230,25 +1252,30 @@ __global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constan
   const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3;
   const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const long long L = a.lines;
-  const long long iters = (L + nwarps * 4 - 1) / (nwarps * 4);   // same trip count in every lane
   const unsigned long long start = globaltimer();
+  // block b's bytes and lines in the LL128 partition; loop trip counts depend only on b, so
+  // every lane of a warp runs the same number of iterations (the loads' warp votes)
+  auto bbytes = [&](int b) { return b == a.world - 1 ? a.last_bytes : a.blk_bytes; };
+  auto blines = [&](int b) { return b == a.world - 1 ? a.last_lines : a.lines; };
+  auto trips = [&](long long L) { return (L + nwarps * 4 - 1) / (nwarps * 4); };
   // 1. scatter my slices of the other blocks to their owners
   for (int b = 0; b < a.world; b++) {
     if (b == a.me) continue;
     const char *blk = a.buf + (long long)b * a.blk_bytes;
+    const long long L = blines(b), nb = bbytes(b), iters = trips(L);
     char *dst = ll128_line(a.peer_scr[b], a, par, 0, a.me, 0);
     for (long long it = 0; it < iters; it++) {
       const long long i = (it * nwarps + gwarp) * 4 + sub;
       if (i >= L) continue;
       unsigned long long w0, w1;
-      ll128_payload(blk, a.blk_bytes, i, j, w0, w1);
+      ll128_payload(blk, nb, i, j, w0, w1);
       st_vol_v2u64(dst + i * kLineBytes + 16 * j, w0, j == 7 ? epoch : w1);
     }
   }
   // 2. reduce my block in the plan's order; result to my buffer and every peer's AG area
   {
     char *blk = a.buf + (long long)a.me * a.blk_bytes;
+    const long long L = blines(a.me), nb = bbytes(a.me), iters = trips(L);
     for (long long it = 0; it < iters; it++) {
       const long long i = (it * nwarps + gwarp) * 4 + sub;
       const bool live = i < L;
@@ -1257,7 +1284,7 @@ __global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constan
         const int q = a.order[k];
         unsigned long long w0 = 0, w1 = 0;
         if (q == a.me) {
-          if (live) ll128_payload(blk, a.blk_bytes, i, j, w0, w1);
+          if (live) ll128_payload(blk, nb, i, j, w0, w1);
         } else {
           ll128_load(ll128_line(a.my_scr, a, par, 0, q, live ? i : 0), j, live, epoch, w0, w1, a, start);
           if (j == 7) w1 = 0ull;   // the flag word carries no payload
@@ -1269,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constan
         for (int k = 0; k < 8; k++) acc[k] = __fdiv_rn(acc[k], (float)a.avg_n);
       unsigned long long r0, r1;
       ll128_pack<BF16>(acc, r0, r1);
-      ll128_store_payload(blk, a.blk_bytes, i, j, r0, r1);
+      ll128_store_payload(blk, nb, i, j, r0, r1);
       for (int d = 0; d < a.world; d++) {
         if (d == a.me) continue;
         st_vol_v2u64(ll128_line(a.peer_scr[d], a, par, 1, a.me, i) + 16 * j, r0, j == 7 ? epoch : r1);
@@ -1280,12 +1307,13 @@ __global__ void __launch_bounds__(kThreads) ar_ll128_kernel(const __grid_constan
   for (int o = 0; o < a.world; o++) {
     if (o == a.me) continue;
     char *blk = a.buf + (long long)o * a.blk_bytes;
+    const long long L = blines(o), nb = bbytes(o), iters = trips(L);
     for (long long it = 0; it < iters; it++) {
       const long long i = (it * nwarps + gwarp) * 4 + sub;
       const bool live = i < L;
       unsigned long long w0 = 0, w1 = 0;
       ll128_load(ll128_line(a.my_scr, a, par, 1, o, live ? i : 0), j, live, epoch, w0, w1, a, start);
-      if (live) ll128_store_payload(blk, a.blk_bytes, i, j, w0, w1);
+      if (live) ll128_store_payload(blk, nb, i, j, w0, w1);
     }
   }
   __syncthreads();
@@ -1443,8 +1471,8 @@ struct ar_comm {
   std::vector<char *> ll_peer;                 // rank -> scratch as seen here
   bool ll_opened = false;
   int ll_ctas = 32;
-  // LL128 two-shot path (ar_ll128_kernel) for CPS-shaped plans with 16-byte-aligned equal
-  // blocks, min(ll128_min_bytes, ll_max_bytes) < message <= ll128_max_bytes (AR_LL128_MIN_KB,
+  // LL128 two-shot path (ar_ll128_kernel) for CPS-shaped plans (any count; its own block
+  // partition), min(ll128_min_bytes, ll_max_bytes) < message <= ll128_max_bytes (AR_LL128_MIN_KB,
   // AR_LL128_MAX_KB; max 0 = off) — it takes such messages before the one-shot path; its
   // scratch follows the push planes: [parity][area][source][ll128_cap_lines] 128-byte lines
   long long ll128_min_bytes = 0, ll128_max_bytes = 0, ll128_cap_lines = 0, ll128_off = 0;
@@ -1877,9 +1905,8 @@ constexpr long long kLLDefaultMaxBytes = 1536 * 1024;
 // measured on 2 and 4 B200s (fp32 and bf16, graph timing; profiles/round2/README.md §12):
 //  * one-shot path (ar_ll_kernel) up to 1.5 MiB/(N−1): it beats the flag protocol there
 //    (~(N−1)·2S of line traffic against two flag round trips);
-//  * the LL128 two-shot path (ar_ll128_kernel) takes eligible messages (equal 16-byte-aligned
-//    blocks) from 768 KiB/(N−1) (at most 384 KiB) up to 64 MiB/N: above the floor it beats the
-//    one-shot path (N = 4, 512 KiB: 9.3 vs 13.6 us; N = 2, 1.5 MiB: 8.4 vs 17.5 us), and up to
+//  * the LL128 two-shot path (ar_ll128_kernel) takes CPS-shaped messages from 768 KiB/(N−1)
+//    (at most 384 KiB) up to 64 MiB/N: above the floor it beats the one-shot path (N = 4, 512 KiB: 9.3 vs 13.6 us; N = 2, 1.5 MiB: 8.4 vs 17.5 us), and up to
 //    the ceiling the step-table kernel (N = 2, 24-32 MiB: 564 vs 492-516 GB/s; N = 4, 32 MiB:
 //    508 vs 554 — the ceiling falls with N).
 static void default_paths(int world, long long *oneshot_max, long long *ll128_min, long long *ll128_max) {
@@ -1964,7 +1991,8 @@ static void init_comm(ar_comm *c) {
       c->push_slot = ((c->push_max_bytes + c->world - 1) / c->world + 16 + 255) / 256 * 256;
       c->push_plane = c->push_slot * c->world;
       c->ll128_off = c->ll_region + (c->push_max_bytes > 0 ? 2 * c->push_plane : 0);
-      c->ll128_cap_lines = (c->ll128_max_bytes / c->world + kLinePayload - 1) / kLinePayload;
+      // + 1: the last block of the LL128 partition carries up to 8N bytes more than max/N
+      c->ll128_cap_lines = (c->ll128_max_bytes / c->world + kLinePayload - 1) / kLinePayload + 1;
       const size_t sz = (size_t)c->ll128_off + (size_t)4 * c->world * c->ll128_cap_lines * kLineBytes;
       CUDA_OK(cudaMalloc(&c->ll_scratch, sz));
       CUDA_OK(cudaMemset(c->ll_scratch, 0, sz));
@@ -2531,9 +2559,10 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
                            nbytes_call);
   if (c->ll_opened && c->ll128_max_bytes > 0 && c->world <= 8 &&
       (long long)nbytes_call > std::min(c->ll128_min_bytes, c->ll_max_bytes) &&
-      (long long)nbytes_call <= c->ll128_max_bytes && count % (uint64_t)c->world == 0 &&
-      (count / c->world) * plan->esize % 16 == 0) {
-    // LL128 two-shot path for CPS-shaped plans with equal 16-byte-aligned blocks (ar_ll128_kernel)
+      (long long)nbytes_call <= c->ll128_max_bytes && nbytes_call >= 8ull * c->world && (uintptr_t)dptr % 8 == 0) {
+    // LL128 two-shot path for CPS-shaped plans (ar_ll128_kernel), any count: blocks of its own
+    // partition (8-byte multiples, the remainder on the last block; the plan's bits do not depend
+    // on the partition because every block sums its elements in the same order)
     auto lit = c->ll_shape.find(plan->uid);
     if (lit == c->ll_shape.end()) lit = c->ll_shape.emplace(plan->uid, oneshot_order(plan->plan)).first;
     if (!lit->second.empty()) {
@@ -2542,9 +2571,14 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       for (int t = 0; t < c->world; t++) la.peer_scr[t] = c->ll_peer[t] + c->ll128_off;
       la.my_scr = c->ll_scratch + c->ll128_off;
       for (int k = 0; k < c->world; k++) la.order[k] = lit->second[k];
-      la.blk_bytes = (long long)(count / c->world) * plan->esize;
+      const long long unit = 8 / plan->esize;   // elements per 8-byte word
+      const long long blk = (long long)(count / c->world) / unit * unit;
+      la.blk_bytes = blk * plan->esize;
       la.lines = (la.blk_bytes + kLinePayload - 1) / kLinePayload;
+      la.last_bytes = ((long long)count - (long long)(c->world - 1) * blk) * plan->esize;
+      la.last_lines = (la.last_bytes + kLinePayload - 1) / kLinePayload;
       la.lines_cap = c->ll128_cap_lines;
+      if (la.last_lines > la.lines_cap) throw SysError("LL128 scratch too small (internal error)");
       la.me = c->rank;
       la.world = c->world;
       la.esize = plan->esize;
@@ -2553,7 +2587,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       la.done_ctr = (unsigned int *)(c->err + 6);
       la.err = c->err;
       la.timeout_ns = c->timeout_ns;
-      const long long warps_needed = (la.lines + 3) / 4;
+      const long long warps_needed = (la.last_lines + 3) / 4;
       // every CTA of every rank must be resident at once (a resident CTA may wait for lines a
       // not-yet-scheduled CTA of a peer would write): at most the kernel's occupancy per SM times
       // the caller's share of the GPU (ar_comm_set_ctas; several ranks' comms on one GPU)

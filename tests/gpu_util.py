@@ -53,3 +53,16 @@ def assert_bits_equal(got: np.ndarray, want: np.ndarray, dtype: str, what: str =
         i = int(np.nonzero(~ok)[0][0])
         raise AssertionError(f"{what}: first mismatch at element {i}: got {int(g[i]):#x} want {int(w[i]):#x} "
                              f"({int((~ok).sum())} mismatches)")
+
+
+def cps_path_kernel(paths: dict, count: int, es: int, world: int) -> str:
+    """The kernel the executor picks for a CPS-shaped plan on a one-rank-per-GPU communicator
+    with these cut-offs (ar_comm_get_paths; 8-byte-aligned buffer): the LL128 kernel in
+    (ll128_min, ll128_max] for N <= 8, else the one-shot kernel up to oneshot_max, else the
+    step-table kernel."""
+    nbytes = count * es
+    if world <= 8 and paths["ll128_max"] and paths["ll128_min"] < nbytes <= paths["ll128_max"] and nbytes >= 8 * world:
+        return "ar_ll128_kernel"
+    if nbytes <= paths["oneshot_max"]:
+        return "ar_ll_kernel"
+    return "ar_exec_kernel"

@@ -17,7 +17,7 @@ from oracle import plans as OP  # noqa: E402
 from oracle import simulate as SM  # noqa: E402
 from oracle import topology as T  # noqa: E402
 from synth import generator as GEN  # noqa: E402
-from tests.gpu_util import assert_bits_equal  # noqa: E402
+from tests.gpu_util import assert_bits_equal, cps_path_kernel  # noqa: E402
 
 
 def main():
@@ -172,7 +172,7 @@ def main():
         G.allreduce_exec(plan, comm, buf)
         torch.cuda.synchronize()
         comm.async_error()
-        expect = "ar_ll_kernel" if cut else "ar_exec_kernel"
+        expect = cps_path_kernel(comm.paths(), count, 4, world)   # LL128 precedes the one-shot path
         want = SM.simulate(oplan, GEN.generate_all(seed + 4, world, count, "f32"), "f32")[rank]
         got = buf.cpu().numpy()[: count * 4].view(np.float32)
         try:

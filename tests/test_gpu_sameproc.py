@@ -122,9 +122,10 @@ def check(sp, world, count, dtype, force, mode="gradient", op="sum", calls=1, ex
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_flag_path_all_kinds(world, dtype):
-    """ar_exec_kernel with .sys flags: every plan kind, ragged count (> one-shot cut-off)."""
+    """ar_exec_kernel with .sys flags: every plan kind, ragged count (> one-shot cut-off; the
+    LL128 path, which would take the CPS-shaped ones, switched off)."""
     count = 1_000_003 if dtype == "f32" else 2_000_003
-    sp = SameProcess(world, count * 4)
+    sp = SameProcess(world, count * 4, env={"AR_LL128_MAX_KB": "0"})
     try:
         kinds = [None, "cps", "ring", "rb"] + (["rhd", "hcps:2,2"] if world == 4 else ["rhd"])
         for force in kinds:
@@ -153,18 +154,21 @@ def test_modes_every_path(mode, dtype):
     """±0, subnormals, ±max (overflow), ±inf, NaN and integer-valued inputs through the
     one-shot path, the dynamic-tile CPS step and the multi-step kinds."""
     world = 4
-    sp = SameProcess(world, 4 << 20)
-    try:
-        check(sp, world, 30011, dtype, None, mode=mode, expect_kernel="ar_ll_kernel")
-        big = 900_007 if dtype == "f32" else 1_800_007
-        for force in (None, "ring", "rhd", "hcps:2,2", "rb"):
-            got = check(sp, world, big, dtype, force, mode=mode, expect_kernel="ar_exec_kernel")
-            if mode == "integer":
-                xs = GEN.generate_all(SEED, world, big, dtype, "integer")
-                ref = sum(GEN.as_f64(x, dtype).astype(np.int64) for x in xs)
-                assert np.array_equal(GEN.as_f64(got[1], dtype).astype(np.int64), ref)
-    finally:
-        sp.destroy()
+    big = 900_007 if dtype == "f32" else 1_800_007
+    for env, cases in (({}, [(30011, None, "ar_ll_kernel"), (big, None, "ar_ll128_kernel"),
+                             (big, "ring", "ar_exec_kernel"), (big, "rhd", "ar_exec_kernel"),
+                             (big, "hcps:2,2", "ar_exec_kernel"), (big, "rb", "ar_exec_kernel")]),
+                       ({"AR_LL128_MAX_KB": "0"}, [(big, None, "ar_exec_kernel")])):
+        sp = SameProcess(world, 4 << 20, env=env)
+        try:
+            for count, force, kern in cases:
+                got = check(sp, world, count, dtype, force, mode=mode, expect_kernel=kern)
+                if mode == "integer":
+                    xs = GEN.generate_all(SEED, world, count, dtype, "integer")
+                    ref = sum(GEN.as_f64(x, dtype).astype(np.int64) for x in xs)
+                    assert np.array_equal(GEN.as_f64(got[1], dtype).astype(np.int64), ref)
+        finally:
+            sp.destroy()
 
 
 def test_avg_and_back_to_back():
@@ -174,7 +178,7 @@ def test_avg_and_back_to_back():
     sp = SameProcess(world, 8 << 20)
     try:
         check(sp, world, 50001, "bf16", None, op="avg", expect_kernel="ar_ll_kernel")
-        check(sp, world, 1_500_001, "f32", None, op="avg", expect_kernel="ar_exec_kernel")
+        check(sp, world, 1_500_001, "f32", None, op="avg", expect_kernel="ar_ll128_kernel")
         check(sp, world, 1_500_001, "f32", "ring", op="avg")
         for count in (40001, 1_200_001, 40001):
             check(sp, world, count, "f32", None, calls=3)
@@ -185,13 +189,13 @@ def test_avg_and_back_to_back():
 def test_push_protocol_and_jitter():
     """The push protocol (AR_PUSH_MAX_MB) and randomly delayed flag posts (AR_JITTER_NS)."""
     world = 4
-    sp = SameProcess(world, 8 << 20, env={"AR_PUSH_MAX_MB": "16"})
+    sp = SameProcess(world, 8 << 20, env={"AR_PUSH_MAX_MB": "16", "AR_LL128_MAX_KB": "0"})
     try:
         check(sp, world, 1_000_003, "f32", None, calls=2, expect_kernel="ar_exec_kernel")
         check(sp, world, 2_000_001, "bf16", None)
     finally:
         sp.destroy()
-    sp = SameProcess(world, 8 << 20, env={"AR_JITTER_NS": "20000", "AR_LL_MAX_KB": "0"})
+    sp = SameProcess(world, 8 << 20, env={"AR_JITTER_NS": "20000", "AR_LL_MAX_KB": "0", "AR_LL128_MAX_KB": "0"})
     try:
         for force in (None, "ring", "rhd", "hcps:2,2"):
             check(sp, world, 600_001, "f32", force, calls=2, expect_kernel="ar_exec_kernel")
@@ -284,27 +288,37 @@ def test_unverified_plan_is_refused():
         comm.destroy()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_ll128_path(world, dtype):
-    """ar_ll128_kernel (mid-size CPS-shaped plans with equal 16-byte-aligned blocks): the CPS
-    plan's RS and AG steps with the flag inside every 128-byte line — bit-identical to the
-    plan; partial last lines; SUM and AVG; back-to-back calls alternating with the one-shot
-    and the flag paths on the same communicators (epoch parity of both scratch areas)."""
+    """ar_ll128_kernel (CPS-shaped plans between the LL128 floor and ceiling): the CPS plan's RS
+    and AG steps with the flag inside every 128-byte line, over the kernel's own block
+    partition (8-byte-multiple blocks, the remainder on the last one — down to a 2- or 4-byte
+    partial word) — bit-identical to the plan's Q3 partition; partial last lines; SUM and AVG;
+    back-to-back calls alternating with the one-shot and the flag paths on the same
+    communicators (epoch parity of both scratch areas); N = 3 (no count is a multiple of N·16
+    bytes there at powers of two)."""
     es = 4 if dtype == "f32" else 2
+    paths = G.default_paths(world)
     sp = SameProcess(world, 16 << 20)
-    unit = world * 16 // es                        # blocks start on 16-byte boundaries
+    unit = world * 16 // es                        # equal blocks starting on 16-byte boundaries
     try:
-        sizes = [(2 << 20) // es // unit * unit, 2_000_000 // unit * unit, (16 << 20) // es - unit]
-        for count in sizes:
+        top = min(16 << 20, paths["ll128_max"]) // es
+        sizes = [(2 << 20) // es // unit * unit, 2_000_000 // unit * unit, top - unit]
+        ragged = [(1 << 20) // es + 1, 1_000_003 if dtype == "f32" else 2_000_003, top - 1,
+                  paths["ll128_min"] // es + 3]
+        for count in sizes + ragged:
             check(sp, world, count, dtype, None, expect_kernel="ar_ll128_kernel")
         check(sp, world, sizes[1], dtype, None, op="avg", expect_kernel="ar_ll128_kernel")
-        for count, kern in ((sizes[0], "ar_ll128_kernel"), (4093, "ar_ll_kernel"), (sizes[0] + 1, "ar_exec_kernel"),
-                            (sizes[1], "ar_ll128_kernel"), (sizes[1], "ar_ll128_kernel")):
+        check(sp, world, ragged[1], dtype, None, op="avg", expect_kernel="ar_ll128_kernel")
+        for count, kern in ((sizes[0], "ar_ll128_kernel"), (4093, "ar_ll_kernel"), (sizes[0] + 1, "ar_ll128_kernel"),
+                            (top + unit, "ar_exec_kernel"), (sizes[1], "ar_ll128_kernel"),
+                            (sizes[1], "ar_ll128_kernel")):
             check(sp, world, count, dtype, None, calls=2, expect_kernel=kern)
         for mode in ("integer", "specials"):
             check(sp, world, sizes[1], dtype, None, mode=mode, expect_kernel="ar_ll128_kernel")
-        if world == 4:   # multi-step plans never take it
+            check(sp, world, ragged[1], dtype, None, mode=mode, expect_kernel="ar_ll128_kernel")
+        if world > 2:   # multi-step plans never take it
             check(sp, world, sizes[0], dtype, "ring", expect_kernel="ar_exec_kernel")
     finally:
         sp.destroy()
@@ -377,11 +391,11 @@ def test_multi_level_same_process(nproc, R):
             c.destroy()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_path_choice_follows_the_cutoffs(world):
     """The executor's path for CPS-shaped plans follows the communicator's cut-offs
-    (ar_comm_get_paths = ar_default_paths by default): LL128 for equal 16-byte-aligned blocks in
-    (ll128_min, ll128_max] — ahead of the one-shot path — one-shot up to oneshot_max otherwise,
+    (ar_comm_get_paths = ar_default_paths by default): LL128 in (ll128_min, ll128_max] — any
+    count, ahead of the one-shot path — one-shot up to oneshot_max otherwise,
     the step-table kernel above; every path with the plan's bits."""
     paths = G.default_paths(world)
     sp = SameProcess(world, paths["ll128_max"] + (1 << 20))
@@ -391,7 +405,8 @@ def test_path_choice_follows_the_cutoffs(world):
         lo, hi = paths["ll128_min"] // 4 // unit * unit, paths["ll128_max"] // 4 // unit * unit
         cases = [(lo, "ar_ll_kernel"),                     # at the floor: one-shot
                  (lo + unit, "ar_ll128_kernel"),           # just above: LL128
-                 (lo + unit + 1, "ar_ll_kernel"),          # ragged blocks: one-shot
+                 (lo + unit + 1, "ar_ll128_kernel"),       # ragged blocks: LL128 (its own partition)
+                 (lo - 3, "ar_ll_kernel"),                 # ragged below the floor: one-shot
                  (hi, "ar_ll128_kernel"),                  # the ceiling
                  (hi + unit, "ar_exec_kernel")]            # above it
         for count, kern in cases:

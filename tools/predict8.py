@@ -50,8 +50,7 @@ def main():
         kind = plan.report()[-1]["chosen"]
         op = G.params(alpha=oj["alpha"], beta=oj["beta"])
         lp = G.params(alpha=lj["alpha"], beta=lj["beta"])
-        if (paths["ll128_min"] < nbytes <= paths["ll128_max"] and count % n == 0
-                and (count // n) * 4 % 16 == 0):
+        if paths["ll128_min"] < nbytes <= paths["ll128_max"]:
             t_plan = G.genmodel_closed_form("ll128", n, nbytes, lp)["total"]
             path = "LL128 two-shot"
         elif nbytes <= paths["oneshot_max"]:

@@ -87,8 +87,8 @@ def final_c2(n, dt):
 
 def c2_section(out):
     out.append("## 2. C2: fp32 busbw vs size — GenTree, GenTree incl. NVLS (path-aware min-GenModel pick), NCCL default / Ring / NVLS-off\n")
-    out.append("Our columns and NCCL default: the final executor (`r3_c2_*`: LL128 two-shot for equal 16-byte-aligned"
-               " blocks from 768 KiB/(N−1) (≤ 384 KiB) to 64 MiB/N, one-shot otherwise up to 1.5 MiB/(N−1), step-table"
+    out.append("Our columns and NCCL default: the final executor (`r3_c2_*`: LL128 two-shot (CPS-shaped plans; equal"
+               " 16-byte-aligned blocks when measured, any count since) from 768 KiB/(N−1) (≤ 384 KiB) to 64 MiB/N, one-shot otherwise up to 1.5 MiB/(N−1), step-table"
                " kernel above — §12); NCCL Ring / NVLS-off: separate processes with the variable set"
                " (`c2_*_ncclring`, `c2_*_ncclnvlsoff`).  Earlier runs: `final_c2_*` (LL128 only above the one-shot"
                " cut-off, to 16 MiB), `c2_n*_f32.jsonl` (before the LL128 path).\n")
@@ -503,7 +503,7 @@ def c2_genmodel_section(out):
             for r in sorted(rows, key=lambda r: r["bytes"]):
                 b = r["bytes"]
                 c = b // es
-                if paths["ll128_min"] < b <= paths["ll128_max"] and c % n == 0 and (c // n) * es % 16 == 0:
+                if paths["ll128_min"] < b <= paths["ll128_max"]:
                     t, tag = G.genmodel_closed_form("ll128", n, b, lp)["total"], "l"
                 elif b <= paths["oneshot_max"]:
                     t, tag = G.genmodel_closed_form("oneshot", n, b, op)["total"], "o"
