@@ -2515,13 +2515,18 @@ static void launch_exec(ar_comm *c, dim3 grid, void **args, cudaStream_t stream)
 // stride_override: bytes between consecutive hosted ranks' buffers when dptr points into the
 // middle of larger rank buffers (the chunked end-to-end path); 0 = derived from count.
 static void check_local_extent(ar_comm *c, void *dptr, size_t need) {
-  // emulated comm: dptr is the base of world rank buffers; the whole extent must be one allocation
+  // emulated comm: dptr is the base of world rank buffers; the whole extent must be one
+  // allocation.  One rank per GPU: the flag-free paths (one-shot, LL128) write only this
+  // rank's buffer and the communicator's scratch, so they need no registration, but the
+  // buffer must hold count elements (cached: the last checked pointer and extent)
   if ((char *)dptr == c->checked_base && need <= c->checked_need) return;
   char *base;
   size_t size;
   base_of(dptr, &base, &size);
   if ((char *)dptr + need > base + size)
-    throw InvalidArg("buffer too small: an emulated communicator needs world rank buffers at ar_rank_stride_bytes");
+    throw InvalidArg(c->local ? "buffer too small: an emulated communicator needs world rank buffers at "
+                                "ar_rank_stride_bytes"
+                              : "buffer too small: it must hold count elements of dtype");
   c->checked_base = (char *)dptr;
   c->checked_need = need;
 }
@@ -2557,6 +2562,7 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
     check_local_extent(c, dptr,
                        (stride_override ? stride_override : ar_rank_stride_bytes(count, dtype)) * (c->world - 1) +
                            nbytes_call);
+  if (!c->local && c->ll_opened) check_local_extent(c, dptr, nbytes_call);   // flag-free paths below
   if (c->ll_opened && c->ll128_max_bytes > 0 && c->world <= 8 &&
       (long long)nbytes_call > std::min(c->ll128_min_bytes, c->ll_max_bytes) &&
       (long long)nbytes_call <= c->ll128_max_bytes && nbytes_call >= 8ull * c->world && (uintptr_t)dptr % 8 == 0) {

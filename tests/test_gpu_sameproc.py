@@ -157,7 +157,8 @@ def test_modes_every_path(mode, dtype):
     big = 900_007 if dtype == "f32" else 1_800_007
     for env, cases in (({}, [(30011, None, "ar_ll_kernel"), (big, None, "ar_ll128_kernel"),
                              (big, "ring", "ar_exec_kernel"), (big, "rhd", "ar_exec_kernel"),
-                             (big, "hcps:2,2", "ar_exec_kernel"), (big, "rb", "ar_exec_kernel")]),
+                             (big, "hcps:2,2", "ar_exec_kernel"),
+                             (big, "rb", "ar_ll128_kernel")]),     # RB's blocks share one order
                        ({"AR_LL128_MAX_KB": "0"}, [(big, None, "ar_exec_kernel")])):
         sp = SameProcess(world, 4 << 20, env=env)
         try:
@@ -229,9 +230,11 @@ def test_settings_are_checked():
 
 def test_open_peers_selects_the_right_registration():
     """Two registrations of the same size: open_peers binds the one whose blob it is given.
-    (Above the one-shot cut-off: the one-shot path reads only the local buffer and the
-    communicator's own scratch, so it needs no registration.)"""
-    world, count = 2, 600_001
+    (Above the LL128 ceiling: the flag-free paths read only the local buffer and the
+    communicator's own scratch, so they need no registration — only a buffer that holds count
+    elements.)"""
+    world = 2
+    count = G.default_paths(world)["ll128_max"] // 4 + 1001
     comms = [G.Comm.create(r, world, 0) for r in range(world)]
     a = [torch.zeros(count * 4, dtype=torch.uint8, device="cuda") for _ in range(world)]
     b = [torch.zeros(count * 4, dtype=torch.uint8, device="cuda") for _ in range(world)]
@@ -258,6 +261,11 @@ def test_open_peers_selects_the_right_registration():
             assert_bits_equal(a[r].cpu().numpy().view(np.float32), want[r], "f32", f"rank {r}")
         with pytest.raises(Exception, match="not registered"):   # b was never opened
             G.allreduce_exec(plan, comms[0], b[0], stream=streams[0])
+        # a flag-free path's size (LL128) on a buffer (a 2 MiB pool segment) too small for it
+        small = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+        with pytest.raises(Exception, match="too small"):
+            G.allreduce_exec(G.Plan.from_topology(single_switch(world), 1_000_001, "f32"), comms[0],
+                             small[256:], 1_000_001, "f32", stream=streams[0])
         del blobs_b
     finally:
         for c in comms:
@@ -312,7 +320,7 @@ def test_ll128_path(world, dtype):
         check(sp, world, sizes[1], dtype, None, op="avg", expect_kernel="ar_ll128_kernel")
         check(sp, world, ragged[1], dtype, None, op="avg", expect_kernel="ar_ll128_kernel")
         for count, kern in ((sizes[0], "ar_ll128_kernel"), (4093, "ar_ll_kernel"), (sizes[0] + 1, "ar_ll128_kernel"),
-                            (top + unit, "ar_exec_kernel"), (sizes[1], "ar_ll128_kernel"),
+                            (ragged[0], "ar_ll128_kernel"), (sizes[1], "ar_ll128_kernel"),
                             (sizes[1], "ar_ll128_kernel")):
             check(sp, world, count, dtype, None, calls=2, expect_kernel=kern)
         for mode in ("integer", "specials"):
