@@ -1186,18 +1186,31 @@ __device__ __forceinline__ void ll128_st_word(char *p, long long rem, unsigned l
   else if (rem > 0) ll128_st_partial(p, (int)rem, w);
 }
 // this lane's payload words of line i of a block that starts at `blk` (part j < 7: bytes
-// 16j..16j+15, part 7: bytes 112..119)
+// 16j..16j+15, part 7: bytes 112..119).  RAGGED = false: blk_bytes is a multiple of 8 (equal
+// 16-byte-aligned blocks), whole words only
+template <bool RAGGED>
 __device__ __forceinline__ void ll128_payload(const char *blk, long long blk_bytes, long long i, int j,
                                               unsigned long long &w0, unsigned long long &w1) {
   const long long o = i * kLinePayload + 16LL * j;
-  w0 = ll128_ld_word(blk + o, blk_bytes - o);
-  w1 = j < 7 ? ll128_ld_word(blk + o + 8, blk_bytes - o - 8) : 0ull;
+  if (RAGGED) {
+    w0 = ll128_ld_word(blk + o, blk_bytes - o);
+    w1 = j < 7 ? ll128_ld_word(blk + o + 8, blk_bytes - o - 8) : 0ull;
+  } else {
+    w0 = o + 8 <= blk_bytes ? *(const unsigned long long *)(blk + o) : 0ull;
+    w1 = (j < 7 && o + 16 <= blk_bytes) ? *(const unsigned long long *)(blk + o + 8) : 0ull;
+  }
 }
+template <bool RAGGED>
 __device__ __forceinline__ void ll128_store_payload(char *blk, long long blk_bytes, long long i, int j,
                                                     unsigned long long w0, unsigned long long w1) {
   const long long o = i * kLinePayload + 16LL * j;
-  ll128_st_word(blk + o, blk_bytes - o, w0);
-  if (j < 7) ll128_st_word(blk + o + 8, blk_bytes - o - 8, w1);
+  if (RAGGED) {
+    ll128_st_word(blk + o, blk_bytes - o, w0);
+    if (j < 7) ll128_st_word(blk + o + 8, blk_bytes - o - 8, w1);
+  } else {
+    if (o + 8 <= blk_bytes) *(unsigned long long *)(blk + o) = w0;
+    if (j < 7 && o + 16 <= blk_bytes) *(unsigned long long *)(blk + o + 8) = w1;
+  }
 }
 // Load line i from a scratch slot until its flag (lane 7 of the 8-lane group, second word)
 // equals `flag`.  Every lane of the warp runs the loop (__any_sync); lanes without a line
@@ -1242,7 +1255,9 @@ __device__ __forceinline__ void ll128_pack(const float (&acc)[8], unsigned long 
   w1 = (unsigned long long)u[2] | ((unsigned long long)u[3] << 32);
 }
 
-template <bool BF16>
+// RAGGED = false: all N blocks equal (last_bytes == blk_bytes), the measured fast path;
+// RAGGED = true: any count (the last block longer, possibly ending in a partial word)
+template <bool BF16, bool RAGGED>
 __global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_constant__ LL128Args a) {
   __shared__ unsigned long long s_epoch;
   if (threadIdx.x == 0) s_epoch = *(volatile unsigned long long *)a.epoch_dev + 1;
@@ -1255,8 +1270,8 @@ __global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_cons
   const unsigned long long start = globaltimer();
   // block b's bytes and lines in the LL128 partition; loop trip counts depend only on b, so
   // every lane of a warp runs the same number of iterations (the loads' warp votes)
-  auto bbytes = [&](int b) { return b == a.world - 1 ? a.last_bytes : a.blk_bytes; };
-  auto blines = [&](int b) { return b == a.world - 1 ? a.last_lines : a.lines; };
+  auto bbytes = [&](int b) { return RAGGED && b == a.world - 1 ? a.last_bytes : a.blk_bytes; };
+  auto blines = [&](int b) { return RAGGED && b == a.world - 1 ? a.last_lines : a.lines; };
   auto trips = [&](long long L) { return (L + nwarps * 4 - 1) / (nwarps * 4); };
   // 1. scatter my slices of the other blocks to their owners
   for (int b = 0; b < a.world; b++) {
@@ -1268,7 +1283,7 @@ __global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_cons
       const long long i = (it * nwarps + gwarp) * 4 + sub;
       if (i >= L) continue;
       unsigned long long w0, w1;
-      ll128_payload(blk, nb, i, j, w0, w1);
+      ll128_payload<RAGGED>(blk, nb, i, j, w0, w1);
       st_vol_v2u64(dst + i * kLineBytes + 16 * j, w0, j == 7 ? epoch : w1);
     }
   }
@@ -1284,7 +1299,7 @@ __global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_cons
         const int q = a.order[k];
         unsigned long long w0 = 0, w1 = 0;
         if (q == a.me) {
-          if (live) ll128_payload(blk, nb, i, j, w0, w1);
+          if (live) ll128_payload<RAGGED>(blk, nb, i, j, w0, w1);
         } else {
           ll128_load(ll128_line(a.my_scr, a, par, 0, q, live ? i : 0), j, live, epoch, w0, w1, a, start);
           if (j == 7) w1 = 0ull;   // the flag word carries no payload
@@ -1296,7 +1311,7 @@ __global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_cons
         for (int k = 0; k < 8; k++) acc[k] = __fdiv_rn(acc[k], (float)a.avg_n);
       unsigned long long r0, r1;
       ll128_pack<BF16>(acc, r0, r1);
-      ll128_store_payload(blk, nb, i, j, r0, r1);
+      ll128_store_payload<RAGGED>(blk, nb, i, j, r0, r1);
       for (int d = 0; d < a.world; d++) {
         if (d == a.me) continue;
         st_vol_v2u64(ll128_line(a.peer_scr[d], a, par, 1, a.me, i) + 16 * j, r0, j == 7 ? epoch : r1);
@@ -1313,7 +1328,7 @@ __global__ void __launch_bounds__(kThreads, 3) ar_ll128_kernel(const __grid_cons
       const bool live = i < L;
       unsigned long long w0 = 0, w1 = 0;
       ll128_load(ll128_line(a.my_scr, a, par, 1, o, live ? i : 0), j, live, epoch, w0, w1, a, start);
-      if (live) ll128_store_payload(blk, nb, i, j, w0, w1);
+      if (live) ll128_store_payload<RAGGED>(blk, nb, i, j, w0, w1);
     }
   }
   __syncthreads();
@@ -2006,9 +2021,12 @@ static void init_comm(ar_comm *c) {
   // measured 0-6 % slower: not kept)
   {
     int per = 0, per2 = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_ll128_kernel<false>, kThreads, 0));
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, ar_ll128_kernel<true>, kThreads, 0));
-    c->ll128_per_sm = std::max(1, std::min(per, per2));
+    int per3 = 0, per4 = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_ll128_kernel<false, false>, kThreads, 0));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, ar_ll128_kernel<true, false>, kThreads, 0));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per3, ar_ll128_kernel<false, true>, kThreads, 0));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per4, ar_ll128_kernel<true, true>, kThreads, 0));
+    c->ll128_per_sm = std::max(1, std::min(std::min(per, per2), std::min(per3, per4)));
   }
   c->ll128_ctas = c->ll128_per_sm * nsm;   // 3 per SM: equal to 2 up to 8 MiB, +1-11 % at 16-32 MiB
   if (const char *v = std::getenv("AR_LL128_CTAS")) c->ll128_ctas = std::max(1, std::atoi(v));
@@ -2599,8 +2617,14 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       // the caller's share of the GPU (ar_comm_set_ctas; several ranks' comms on one GPU)
       const long long cap = std::min<long long>(c->ll128_ctas, (long long)c->ll128_per_sm * c->nctas);
       const int ctas = (int)std::max(1LL, std::min<long long>(cap, (warps_needed + 15) / 16));
-      if (plan->esize == 2) ar_ll128_kernel<true><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
-      else ar_ll128_kernel<false><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      const bool ragged = la.last_bytes != la.blk_bytes;
+      if (plan->esize == 2) {
+        if (ragged) ar_ll128_kernel<true, true><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+        else ar_ll128_kernel<true, false><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      } else {
+        if (ragged) ar_ll128_kernel<false, true><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+        else ar_ll128_kernel<false, false><<<ctas, kThreads, 0, (cudaStream_t)stream>>>(la);
+      }
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
       c->last_kernel = "ar_ll128_kernel";
