@@ -293,7 +293,8 @@ int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t coun
  * reading AV1): the last ReduceScatter op writing each block divides its fp32 sum by the
  * world size N with one correctly rounded IEEE fp32 division, before the store's rounding
  * (bf16: RNE of the fp32 quotient); the AllGather then copies that value, so every rank ends
- * with the same bits. */
+ * with the same bits.  On an NVLS plan (fp32): the switch's correctly rounded sum divided by N
+ * with one correctly rounded division before the multicast store. */
 #define AR_OP_SUM 0
 #define AR_OP_AVG 1
 

@@ -58,11 +58,14 @@ def simulate(plan: Plan, inputs: list, dtype: str, op: str = "sum") -> list:
         raise ValueError(op)
     if plan.switch_reduce:
         # NVLS plan (reading NV2): every element is the correctly rounded fp32 sum of the
-        # ranks' inputs, on every rank (the switch reduces each element once)
-        if dtype != "f32" or op != "sum":
-            raise ValueError("NVLS plans: fp32 SUM only (reading NV2)")
+        # ranks' inputs, on every rank (the switch reduces each element once); AVG (reading
+        # AV1 on this kind): that sum divided by N, one IEEE binary32 division (RNE)
+        if dtype != "f32":
+            raise ValueError("NVLS plans: fp32 only (reading NV2)")
         from .exactsum import correctly_rounded_sum_f32
         out = correctly_rounded_sum_f32(inputs)
+        if op == "avg":
+            out = (out / np.float32(n)).astype(np.float32)
         return [out.copy() for _ in range(n)]
     last = last_rs_step(plan)
     bufs = [np.array(x, copy=True) for x in inputs]

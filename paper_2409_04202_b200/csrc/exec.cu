@@ -2557,11 +2557,11 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
                      "ar_exec_movement_plan");
   if (plan->plan.switch_reduce) {
     // NVLS plan kind: the fan-in-N reduce and the broadcast happen in the NVSwitch
-    if (op != AR_OP_SUM) throw InvalidArg("NVLS plans support AR_OP_SUM only");
+    if (op != AR_OP_SUM && op != AR_OP_AVG) throw InvalidArg("unknown reduction op");
     if (!c->nvls) throw InvalidArg("NVLS plan: attach the NVLS buffer first (ar_comm_attach_nvls)");
     if (plan->plan.n != c->world) throw InvalidArg("plan and communicator have different world sizes");
     if ((uint64_t)plan->plan.count != count || plan->dtype != dtype) throw InvalidArg("count/dtype differ from the plan's");
-    nvls_launch(c->nvls, dptr, count, dtype, stream);
+    nvls_launch(c->nvls, dptr, count, dtype, stream, op == AR_OP_AVG ? plan->plan.n : 0);
     c->last_launches = 1;
     c->last_kernel = "nvls_kernel";
     return AR_OK;

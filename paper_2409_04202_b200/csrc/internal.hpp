@@ -26,7 +26,7 @@ struct ar_nvls;
 namespace gtar {
 void set_error(const std::string &msg);
 // nvls.cu: in-switch AllReduce of `count` elements of the rank's NVLS buffer (throws)
-void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, void *stream);
+void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, void *stream, int avg_n = 0);
 uint64_t next_plan_uid();
 inline int esize_of(int dtype) { return dtype == 0 ? 4 : 2; }
 inline const char *dtype_name(int dtype) { return dtype == 0 ? "f32" : "bf16"; }

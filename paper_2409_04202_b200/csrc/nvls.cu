@@ -117,6 +117,7 @@ struct NvArgs {
   int world, esize;
   unsigned long long timeout_ns;
   int dyn;                        // 1 = chunks handed out by atomicAdd on epoch_dev[3] (AR_NVLS_DYN)
+  int avg_n;                      // AVG (fp32): divide the switch's sum by N (0 = SUM)
 };
 
 __device__ __forceinline__ unsigned long long nv_ld_acquire(const unsigned long long *p) {
@@ -186,9 +187,20 @@ __device__ __forceinline__ void mc_store(void *mc, const uint4 &v) {
                  : "memory");
 }
 
+// AVG (fp32 only, reading NV3): the switch's correctly rounded sum divided by N with one
+// correctly rounded IEEE division per element, before the multicast store
+__device__ __forceinline__ uint4 avg4(uint4 v, int n) {
+  const float d = (float)n;
+  v.x = __float_as_uint(__fdiv_rn(__uint_as_float(v.x), d));
+  v.y = __float_as_uint(__fdiv_rn(__uint_as_float(v.y), d));
+  v.z = __float_as_uint(__fdiv_rn(__uint_as_float(v.z), d));
+  v.w = __float_as_uint(__fdiv_rn(__uint_as_float(v.w), d));
+  return v;
+}
+
 // Scalar tail (count not a multiple of 16 bytes): fp32 one element, bf16 an element pair.
 template <int MODE>
-__device__ __forceinline__ void tail_reduce_store(char *mc) {
+__device__ __forceinline__ void tail_reduce_store(char *mc, int avg_n) {
   uint32_t v;
   if (MODE == 1)
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.bf16x2 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
@@ -198,6 +210,7 @@ __device__ __forceinline__ void tail_reduce_store(char *mc) {
     asm volatile("multimem.st.relaxed.sys.global.bf16x2 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
   } else {
     asm volatile("multimem.ld_reduce.relaxed.sys.global.add.f32 %0, [%1];" : "=r"(v) : "l"(mc) : "memory");
+    if (avg_n) v = __float_as_uint(__fdiv_rn(__uint_as_float(v), (float)avg_n));
     asm volatile("multimem.st.relaxed.sys.global.f32 [%0], %1;" ::"l"(mc), "r"(v) : "memory");
   }
 }
@@ -238,7 +251,7 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
 #pragma unroll
         for (int u = 0; u < U; u++) {
           const long long v = base + (long long)u * blockDim.x;
-          if (v < c1) mc_store<MODE>(a.mc + v * 16, x[u]);
+          if (v < c1) mc_store<MODE>(a.mc + v * 16, (MODE == 0 && a.avg_n) ? avg4(x[u], a.avg_n) : x[u]);
         }
       }
     }
@@ -253,14 +266,14 @@ __global__ void __launch_bounds__(kNvThreads) nvls_kernel(const __grid_constant_
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const long long v = base + (long long)u * blockDim.x;
-      if (v < v1) mc_store<MODE>(a.mc + v * 16, x[u]);
+      if (v < v1) mc_store<MODE>(a.mc + v * 16, (MODE == 0 && a.avg_n) ? avg4(x[u], a.avg_n) : x[u]);
     }
   }
   if (a.tail_len > 0 && blockIdx.x == 0) {
     const int step = MODE != 0 ? 2 : 1;
     for (long long e = a.tail_off + (long long)threadIdx.x * step; e < a.tail_off + a.tail_len;
          e += (long long)blockDim.x * step)
-      tail_reduce_store<MODE>(a.mc + e * a.esize);
+      tail_reduce_store<MODE>(a.mc + e * a.esize, a.avg_n);
   }
   nv_barrier(a, 1, epoch, t0);   // every rank's results have landed in every GPU's buffer
   if (threadIdx.x == 0) {
@@ -312,13 +325,14 @@ namespace gtar {
 // its unicast base).  Whole 16-byte vectors are split evenly over the ranks (the result does
 // not depend on the split: the switch reduces every element once); the trailing elements past
 // the last whole vector go to the last rank (fp32: any count; bf16: even counts).
-void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, void *stream) {
+void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, void *stream, int avg_n) {
   if (!n || !n->bound) throw InvalidArg("nvls buffer not bound");
   if (dtype != AR_F32 && dtype != AR_BF16) throw InvalidArg("unknown dtype");
   if ((CUdeviceptr)dptr != n->uc) throw InvalidArg("the buffer is not this communicator's NVLS buffer");
   const int es = dtype == AR_BF16 ? 2 : 4;
   if (count < 1 || count * es > n->data_bytes) throw InvalidArg("count exceeds the nvls buffer");
   if (dtype == AR_BF16 && count % 2) throw InvalidArg("nvls bf16 needs an even count");
+  if (avg_n && dtype != AR_F32) throw InvalidArg("NVLS AVG is fp32 only");
   int cur = -1;
   RT_CALL(cudaGetDevice(&cur));
   if (cur != n->device) RT_CALL(cudaSetDevice(n->device));
@@ -339,6 +353,7 @@ void nvls_launch(ar_nvls *n, const void *dptr, uint64_t count, int32_t dtype, vo
   a.esize = es;
   a.timeout_ns = n->timeout_ns;
   a.dyn = n->dyn ? 1 : 0;
+  a.avg_n = avg_n;
   const int mode = dtype == AR_BF16 ? (n->bf16_acc_bf16 ? 2 : 1) : 0;
   launch_mode(mode, n->unroll, n->nctas, (cudaStream_t)stream, a);
   RT_CALL(cudaGetLastError());
@@ -476,7 +491,7 @@ int ar_nvls_bind(ar_nvls *n, void **uc_ptr_out) {
 int allreduce_exec_nvls(ar_nvls *n, uint64_t count, int32_t dtype, void *stream) {
   NV_TRY({
     if (!n || !n->bound) throw InvalidArg("nvls buffer not bound");
-    gtar::nvls_launch(n, (const void *)n->uc, count, dtype, stream);
+    gtar::nvls_launch(n, (const void *)n->uc, count, dtype, stream, 0);
     return AR_OK;
   })
 }

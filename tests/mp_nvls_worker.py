@@ -104,6 +104,20 @@ def main():
         if not (ok and all(a == allv[0] for a in allv)):
             print(f"rank {rank} FAIL nvls plan count={count}", flush=True)
             failures += 1
+        if count in (world * 4 + 1, 1000003):   # AVG: the rounded sum / N, one RNE division
+            G.fill_synthetic(nv.ptr, count, "f32", seed, rank, 0)
+            torch.cuda.synchronize()
+            dist.barrier()
+            G.allreduce_exec(plan, comm, nv.ptr, op="avg")
+            torch.cuda.synchronize()
+            comm.async_error()
+            got = nv.tensor[: count * 4].cpu().numpy().view(np.uint32)
+            xs = GEN.generate_all(seed, world, count, "f32")
+            want = SM.simulate(type(oplan)(world, count, oplan.steps[:0], True), xs, "f32", op="avg")[rank]
+            if not np.array_equal(got, want.view(np.uint32)):
+                print(f"rank {rank} FAIL nvls AVG count={count}: {int(np.sum(got != want.view(np.uint32)))} differ",
+                      flush=True)
+                failures += 1
     comm.destroy()
     dist.barrier()
     nv.destroy()

@@ -98,3 +98,30 @@ def test_round_fraction_overflow_and_subnormal():
 def test_rejects_non_finite():
     with pytest.raises(ValueError):
         correctly_rounded_sum_f32([np.array([np.inf], np.float32), np.array([1.0], np.float32)])
+
+
+def test_nvls_avg_is_the_rounded_quotient_of_the_rounded_sum():
+    """NVLS AVG (fp32; readings NV2 + AV1): oracle.simulate of a switch_reduce plan with op
+    "avg" gives every element as round(round(Σx)/N) — checked element by element against the
+    quotient of exact rationals rounded with round_fraction_to_f32 (N = 3, 5: non-powers of two,
+    where the division rounds), against Σ × 1/N exactly for N = 4 (a power of two, normal range),
+    and N equal inputs average to the input."""
+    from oracle import plans as OP
+    from oracle import simulate as SM
+    rng = np.random.default_rng(7)
+    for n in (3, 4, 5):
+        count = 3000
+        x = wide_random(rng, n, count, 20)
+        plan = OP.Plan(n, count, [], True)
+        got = SM.simulate(plan, list(x), "f32", op="avg")[0]
+        s = correctly_rounded_sum_f32(list(x))
+        for i in range(0, count, 7):
+            want = round_fraction_to_f32(Fraction(float(s[i])) / n)
+            assert struct.pack("<f", got[i]) == struct.pack("<f", want) or (got[i] == 0 and want == 0), (n, i)
+        if n == 4:
+            normal = np.abs(s) >= np.float32(2.0 ** -124)
+            assert np.array_equal(got[normal], (s[normal] * np.float32(0.25)).astype(np.float32))
+    same = np.full(64, np.float32(1.375), dtype=np.float32)
+    for n in (3, 6):
+        got = SM.simulate(OP.Plan(n, 64, [], True), [same] * n, "f32", op="avg")
+        assert all(np.array_equal(g, same) for g in got)
