@@ -79,8 +79,9 @@ def nccl_algo_section(out):
 
 
 def final_c2(n, dt):
-    """The latest C2 run of the final executor: `r3_c2_*` (re-tuned path cut-offs, session 3),
-    else `final_c2_*`."""
+    """The latest C2 run of the final executor: `r3_c2_*` (session 3's final build: re-tuned path
+    cut-offs, LL128 for any count; `r3a_c2_*` is the same sweep on the build before the ragged
+    LL128 change, which the LL128 row was fitted on), else `final_c2_*`."""
     return (jl(os.path.join(P, "c2", f"r3_c2_n{n}_{dt}.jsonl")) or
             jl(os.path.join(P, "c2", f"final_c2_n{n}_{dt}.jsonl")))
 
@@ -485,8 +486,8 @@ def c2_genmodel_section(out):
     op = G.params(alpha=oj["alpha"], beta=oj["beta"])
     out.append("## 15. GenModel prediction error of the GenTree plan along the C2 sweep (`r3_c2_*`, graph timing)\n")
     out.append("Each size is predicted on the row of the path the executor takes (ar_default_paths): the LL128 row "
-               f"(`genmodel_fit_ll128_graph.json`, per rank count, fitted on the fp32 medians — fit rows for fp32, "
-               "held out for bf16), the one-shot row OS1 (round-2 fit, held out here) or the executed-plan model "
+               f"(`genmodel_fit_ll128_graph.json`, per rank count, fitted on the fp32 medians of the previous run "
+               "`r3a_c2_*` — held out here), the one-shot row OS1 (round-2 fit, held out) or the executed-plan model "
                "A6x (CPS fit, `genmodel_params.json`, held out).  Error = (predicted − measured median) / measured; "
                "path: o = one-shot, l = LL128, a = A6x.\n")
     for n in (4, 2):
@@ -516,10 +517,10 @@ def c2_genmodel_section(out):
             out.append(f"* N = {n}, {dt}: median {e[len(e) // 2]:.1%}, max {e[-1]:.1%} — " + "; ".join(cells))
     out.append("")
     out.append("Every A6x row (≥ 32 MiB) is within 2.3 %.  The largest errors are the LL128 row's: its affine "
-               "α + B·β bends around the measured curve — under at its floor (512 KiB: −12 … −18 %, where the "
-               "fixed cost dominates) and over at 4–8 MiB on 2 GPUs (+6 … +8 %: without entry or exit barriers, "
+               "α + B·β bends around the measured curve — under at its floor (512 KiB: −16 … −20 %, 1 MiB −7 … −13 %, "
+               "where the fixed cost dominates) and over at 4–8 MiB on 2 GPUs (+3 … +9 %: without entry or exit barriers, "
                "back-to-back calls overlap across ranks in the graph replay, so per-call times there imply "
-               "per-byte rates above the link's) — and the one-shot row at 256 KiB on 4 GPUs (+9 … +11 %).\n")
+               "per-byte rates above the link's) — and the one-shot row at 256 KiB on 4 GPUs (+8 … +10 %).\n")
 
 
 def ragged_section(out):
