@@ -2540,7 +2540,15 @@ static void check_local_extent(ar_comm *c, void *dptr, size_t need) {
   if ((char *)dptr == c->checked_base && need <= c->checked_need) return;
   char *base;
   size_t size;
-  base_of(dptr, &base, &size);
+  if (c->local) {
+    base_of(dptr, &base, &size);
+  } else {
+    try {
+      base_of(dptr, &base, &size);
+    } catch (const std::exception &) {
+      return;   // not a driver allocation it can size (e.g. a virtual-memory mapping): unchecked
+    }
+  }
   if ((char *)dptr + need > base + size)
     throw InvalidArg(c->local ? "buffer too small: an emulated communicator needs world rank buffers at "
                                 "ar_rank_stride_bytes"
