@@ -382,7 +382,10 @@ def main():
     kern_t = statistics.mean(per_step)
     if n == 1:
         hbm_peak, hbm_src = load_peaks()
-        alg_bytes = 2 * world * nbytes          # every rank buffer read once + written once
+        # the plan's HBM bytes, all ranks sharing one HBM (reading A6e's D: every op's k reads and
+        # one write per destination): 2·R·S for CPS (every rank buffer read once, written once),
+        # (5R − 6)·S for Ring, …
+        alg_bytes = int(plan.predict_executed_shared(G.params(0.0, 1e-30, 0.0, 1.0, 0.0, 9))["memory"])
         achieved = alg_bytes / kern_t / 1e9
         roof = {"kernel": comm.last_kernel(), "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak,
                 "unit": "GB/s",
