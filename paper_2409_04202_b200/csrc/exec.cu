@@ -999,6 +999,119 @@ __global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_const
   bulk_store_drain();
 }
 
+// ------------------------------------------------------------------ multi-step plans on emulated ranks
+// All ranks in one HBM (emulated comm), a multi-step plan (Ring, RHD, HCPS, rearrangement):
+// every executed step's ops are independent of each other (O3; the fusion rule keeps it so), so
+// the ops of ALL ranks in a step are concatenated and split evenly over every SM, as in
+// ar_flat_kernel, and a grid-wide barrier separates consecutive steps in place of the
+// step-table kernel's per-rank flags.  Same bodies, summation order and rounding: the plan's
+// bits.  One cooperative launch (every CTA resident for the barrier).
+struct FlatStepsArgs {
+  char *base;
+  long long stride;
+  const DevOp *ops;                  // the ops of global step s: [gbegin[s], gbegin[s + 1])
+  const int *ranks;                  // src / dst rank lists of the ops
+  const int *gbegin;
+  int nsteps, esize, avg_n, stages, stage_bytes;
+  unsigned int *bar;                 // [0] barrier arrivals, [1] finished CTAs (reset by the last)
+  unsigned long long *err;
+  unsigned long long timeout_ns;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) ar_flatsteps_kernel(const __grid_constant__ FlatStepsArgs a) {
+  __shared__ OpShared sh;
+  __shared__ Pipe pp;
+  extern __shared__ __align__(128) uint8_t dyn_smem[];
+  const bool bf16 = a.esize == 2;
+  const long long E = 16 / a.esize;
+  const unsigned long long t0 = globaltimer();
+  if (threadIdx.x == 0) {
+    pp.stages = a.stages;
+    pp.stage_bytes = a.stage_bytes;
+    for (int st = 0; st < a.stages; st++) {
+      mbar_init(&pp.full[st], 1);
+      mbar_init(&pp.empty[st], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t g = 0;
+  for (int s = 0; s < a.nsteps; s++) {
+    if (s > 0) {
+      // grid barrier: the previous step's bulk stores are complete (bulk_store_drain) and
+      // released at gpu scope before this CTA's arrival; the acquire below orders this
+      // step's reads (the bulk producer also fences the async proxy)
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.bar) : "memory");
+        const unsigned int target = (unsigned int)s * gridDim.x;
+        unsigned int spins = 0;
+        for (;;) {
+          unsigned int v;
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+          if (v >= target) break;
+          if ((++spins & 1023u) == 0 && globaltimer() - t0 > a.timeout_ns) {
+            atomicExch(a.err, 1ull);
+            break;
+          }
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      __syncthreads();
+    }
+    const int o0 = a.gbegin[s], o1 = a.gbegin[s + 1];
+    long long total = 0;
+    for (int oi = o0; oi < o1; oi++) {
+      const DevOp &op = a.ops[oi];
+      const long long vb = (op.off * a.esize + 15) / 16, ve = (op.off + op.len) * a.esize / 16;
+      if (ve > vb) total += ve - vb;
+    }
+    const long long my0 = total * blockIdx.x / gridDim.x, my1 = total * (blockIdx.x + 1) / gridDim.x;
+    long long acc = 0;
+    for (int oi = o0; oi < o1; oi++) {
+      const DevOp op = a.ops[oi];
+      const long long vb = (op.off * a.esize + 15) / 16, ve = (op.off + op.len) * a.esize / 16;
+      const long long nv = ve > vb ? ve - vb : 0;
+      const long long lo = max(my0, acc), hi = min(my1, acc + nv);
+      const bool mine_vec = lo < hi;
+      const bool mine_scalar = blockIdx.x == 0 && op.len > 0 &&
+                               (nv == 0 || vb * 16 > op.off * a.esize || ve * 16 < (op.off + op.len) * a.esize);
+      if (mine_vec || mine_scalar) {
+        __syncthreads();
+        if (threadIdx.x < op.nsrc) sh.src[threadIdx.x] = (const uint4 *)(a.base + a.stride * a.ranks[op.src_begin + threadIdx.x]);
+        if (threadIdx.x < op.ndst) sh.dst[threadIdx.x] = (uint4 *)(a.base + a.stride * a.ranks[op.dst_begin + threadIdx.x]);
+        if (threadIdx.x == 0) {
+          sh.nsrc = op.nsrc;
+          sh.ndst = op.ndst;
+          sh.div = op.fin ? a.avg_n : 0;
+        }
+        __syncthreads();
+        if (mine_vec) {
+          const size_t v0 = (size_t)(vb + lo - acc), v1 = (size_t)(vb + hi - acc);
+          if (bf16) body_dispatch_bulk_st<true>(sh, v0, v1, g, dyn_smem, pp);
+          else body_dispatch_bulk_st<false>(sh, v0, v1, g, dyn_smem, pp);
+        }
+        if (mine_scalar) {
+          if (nv == 0) {
+            scalar_elems(sh, op.off, op.off + op.len, bf16);
+          } else {
+            if (vb * 16 > op.off * a.esize) scalar_elems(sh, op.off, vb * E, bf16);
+            if (ve * 16 < (op.off + op.len) * a.esize) scalar_elems(sh, ve * E, op.off + op.len, bf16);
+          }
+        }
+      }
+      acc += nv;
+    }
+    bulk_store_drain();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(a.bar + 1, 1u) == gridDim.x - 1) {
+    a.bar[0] = 0u;   // every CTA is past its last barrier
+    a.bar[1] = 0u;
+    __threadfence();
+  }
+}
+
 // ------------------------------------------------------------------ low-latency one-shot path
 // Small messages on one rank per GPU, CPS-shaped plans (one fan-in-N reduce per block, every
 // block with the same input order): every rank pushes its whole input to every peer's
@@ -1439,6 +1552,13 @@ struct Lowered {
   unsigned int *dyn_ctr = nullptr;   // per-op tile counters (dynamic scheduling), nullptr = static
   int nops = 0;
 };
+// an emulated comm's multi-step plan for ar_flatsteps_kernel: every rank's ops grouped by step
+struct FlatSteps {
+  DevOp *ops = nullptr;
+  int *ranks = nullptr;
+  int *gbegin = nullptr;
+  int nsteps = 0;
+};
 
 }  // namespace
 
@@ -1456,6 +1576,7 @@ struct ar_comm {
   std::map<std::string, char *> ipc_opened;    // handle bytes -> base (opened once)
   std::vector<Registration> regs;
   std::map<uint64_t, Lowered> lowered;
+  std::map<uint64_t, FlatSteps> flatsteps_cache;   // plan uid -> ar_flatsteps_kernel tables
   unsigned long long *err = nullptr;
   unsigned long long timeout_ns = 10ull * 1000 * 1000 * 1000;
   int last_launches = 0;
@@ -1475,6 +1596,8 @@ struct ar_comm {
   bool flat = true;                            // emulated single-step plans via ar_flat_kernel (AR_FLAT=0: off)
   bool dyn = true;                             // dynamic tile scheduling of CPS-shaped plans (AR_DYN=0: off)
   unsigned int *flat_ctr = nullptr;            // ar_flat_kernel tile counters (local comms)
+  unsigned int *fs_bar = nullptr;              // ar_flatsteps_kernel grid-barrier words (local comms)
+  bool flatsteps = true;                       // emulated multi-step plans via ar_flatsteps_kernel (AR_FLATSTEPS=0: off)
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
@@ -1896,6 +2019,7 @@ static int resident_ctas(int device) {
   CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
   CUDA_OK(cudaFuncSetAttribute(ar_exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   CUDA_OK(cudaFuncSetAttribute(ar_flat_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  CUDA_OK(cudaFuncSetAttribute(ar_flatsteps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ar_exec_kernel, kThreads, kMaxDynSmem));
   return nsm * std::max(per, 1);
 }
@@ -1959,6 +2083,8 @@ static void init_comm(ar_comm *c) {
   if (c->local) {   // ar_flat_kernel's tile counters (dynamic scheduling)
     CUDA_OK(cudaMalloc(&c->flat_ctr, (AR_MAX_RANKS + 1) * sizeof(unsigned int)));
     CUDA_OK(cudaMemset(c->flat_ctr, 0, (AR_MAX_RANKS + 1) * sizeof(unsigned int)));
+    CUDA_OK(cudaMalloc(&c->fs_bar, 2 * sizeof(unsigned int)));
+    CUDA_OK(cudaMemset(c->fs_bar, 0, 2 * sizeof(unsigned int)));
   }
   c->sig.assign(c->world, nullptr);
   for (int i = 0; i < c->rpp; i++) c->sig[c->rank + i] = c->sig_local + (size_t)i * c->page_elems;
@@ -1983,6 +2109,7 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
   if (const char *v = std::getenv("AR_LAUNCH")) c->plain_launch = std::string(v) == "plain";
   if (const char *v = std::getenv("AR_FLAT")) c->flat = std::string(v) != "0";
+  if (const char *v = std::getenv("AR_FLATSTEPS")) c->flatsteps = std::string(v) != "0";
   if (const char *v = std::getenv("AR_DYN")) c->dyn = std::string(v) != "0";
   if (const char *v = std::getenv("AR_ENTRY_FENCE")) c->entry_fence = std::string(v) == "1";
   if (!c->local && c->rpp == 1) {
@@ -2278,6 +2405,12 @@ int ar_comm_destroy(ar_comm *c) {
   cudaFree(c->ll_scratch);
   cudaFree(c->err);
   if (c->flat_ctr) cudaFree(c->flat_ctr);
+  if (c->fs_bar) cudaFree(c->fs_bar);
+  for (auto &kv : c->flatsteps_cache) {
+    cudaFree(kv.second.ops);
+    cudaFree(kv.second.ranks);
+    cudaFree(kv.second.gbegin);
+  }
   cudaFree(c->trace);
   delete c;
   return AR_OK;
@@ -2688,6 +2821,56 @@ static int exec_impl(const gt_plan *plan, ar_comm *c, void *dptr, uint64_t count
       CUDA_OK(cudaGetLastError());
       c->last_launches = 1;
       c->last_kernel = "ar_flat_kernel";
+      return AR_OK;
+    }
+    if (c->flatsteps) {
+      // emulated ranks, multi-step plan: every step's ops over every SM, grid barriers between
+      // steps (ar_flatsteps_kernel)
+      auto fit = c->flatsteps_cache.find(plan->uid);
+      if (fit == c->flatsteps_cache.end()) {
+        std::vector<DevStep> st;
+        std::vector<DevOp> ops;
+        std::vector<DevWait> w;
+        std::vector<int> rk, pb, pl;
+        lower_plan(plan->plan, c->world, st, ops, w, rk, pb, pl);
+        int maxslot = 0;
+        for (const DevStep &x : st) maxslot = std::max(maxslot, x.slot);
+        std::vector<std::vector<int>> by(maxslot + 1);   // slot s + 1 = after plan step s
+        for (const DevStep &x : st)
+          for (int i = 0; i < x.op_count; i++) by[x.slot].push_back(x.op_begin + i);
+        std::vector<DevOp> gops;
+        std::vector<int> gb{0};
+        for (const auto &v : by) {
+          if (v.empty()) continue;
+          for (int i : v) gops.push_back(ops[i]);
+          gb.push_back((int)gops.size());
+        }
+        FlatSteps F;
+        F.nsteps = (int)gb.size() - 1;
+        F.ops = upload(gops);
+        F.ranks = upload(rk);
+        F.gbegin = upload(gb);
+        fit = c->flatsteps_cache.emplace(plan->uid, F).first;
+      }
+      FlatStepsArgs fs{};
+      fs.base = (char *)dptr;
+      fs.stride = (long long)(stride_override ? stride_override : ar_rank_stride_bytes(count, dtype));
+      fs.ops = fit->second.ops;
+      fs.ranks = fit->second.ranks;
+      fs.gbegin = fit->second.gbegin;
+      fs.nsteps = fit->second.nsteps;
+      fs.esize = plan->esize;
+      fs.avg_n = avg_n;
+      fs.stages = c->stages;
+      fs.stage_bytes = c->stage_bytes;
+      fs.bar = c->fs_bar;
+      fs.err = c->err;
+      fs.timeout_ns = c->timeout_ns;
+      void *args[] = {&fs};
+      CUDA_OK(cudaLaunchCooperativeKernel((const void *)ar_flatsteps_kernel, dim3(c->max_ctas), dim3(kThreads), args,
+                                          dyn_smem_bytes(c->stages, c->stage_bytes), (cudaStream_t)stream));
+      c->last_launches = 1;
+      c->last_kernel = "ar_flatsteps_kernel";
       return AR_OK;
     }
   }

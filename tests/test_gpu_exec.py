@@ -60,7 +60,8 @@ def test_device_generator_matches_numpy(dtype, mode):
         assert np.array_equal(got, want)
 
 
-def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1, red="sum"):
+def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=None, ctas=0, calls=1, red="sum",
+                 expect_kernel=None):
     plan = G.Plan.from_topology(doc, count, dtype, params, force)
     comm = G.Comm.local(world, 0)
     if ctas:
@@ -85,6 +86,8 @@ def run_emulated(doc, world, count, dtype, force=None, mode="gradient", params=N
     for r in range(world):
         assert_bits_equal(got[r], want[r], dtype, f"rank {r}")
     assert comm.last_launch_count() == 1
+    if expect_kernel:
+        assert comm.last_kernel() == expect_kernel, comm.last_kernel()
     return got
 
 
@@ -388,3 +391,23 @@ def test_exec_host_end_to_end(force, dtype):
     for r in range(world):
         got = hv[r * stride: r * stride + count * es].view(np.float32 if dtype == "f32" else np.uint16)
         assert_bits_equal(got, want[r], dtype, f"rank {r}")
+
+
+@pytest.mark.parametrize("flatsteps", ["1", "0"])
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_multi_step_kernels(flatsteps, dtype, monkeypatch):
+    """Emulated multi-step plans run on ar_flatsteps_kernel (every step's ops of all ranks over
+    every SM, grid barriers between steps); AR_FLATSTEPS=0 keeps them on the step-table kernel
+    and its per-rank flags — both with the plan's bits: every kind, ragged sizes, SUM and AVG,
+    back-to-back calls (the barrier words must be back at zero), specials."""
+    monkeypatch.setenv("AR_FLATSTEPS", flatsteps)
+    kern = "ar_flatsteps_kernel" if flatsteps == "1" else "ar_exec_kernel"
+    for force in ("ring", "rhd", "hcps:4,2", "hcps:2,2,2"):
+        for count in (8 * 4096 + 7, 1000003):
+            run_emulated(single_switch(8), 8, count, dtype, force=force, calls=2, expect_kernel=kern)
+        run_emulated(single_switch(8), 8, 300001, dtype, force=force, red="avg", expect_kernel=kern)
+    run_emulated(single_switch(8), 8, 300001, dtype, force="ring", mode="specials", expect_kernel=kern)
+    for world in (3, 5):
+        run_emulated(single_switch(world), world, 200003, dtype, force="ring", expect_kernel=kern)
+    c1 = T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    run_emulated(c1, 4, 100003, dtype, expect_kernel=kern)          # C1's two-level GenTree plan
