@@ -1005,7 +1005,9 @@ __global__ void __launch_bounds__(kThreads, 1) ar_flat_kernel(const __grid_const
 // the ops of ALL ranks in a step are concatenated and split evenly over every SM, as in
 // ar_flat_kernel, and a grid-wide barrier separates consecutive steps in place of the
 // step-table kernel's per-rank flags.  Same bodies, summation order and rounding: the plan's
-// bits.  One cooperative launch (every CTA resident for the barrier).
+// bits.  One cooperative launch (every CTA resident for the barrier).  An A/B option
+// (AR_FLATSTEPS=1): the barrier serialises the steps, and the step-table kernel's range waits
+// (dependent steps overlapping CTA by CTA) measured as fast in bf16 and faster in fp32.
 struct FlatStepsArgs {
   char *base;
   long long stride;
@@ -1597,7 +1599,10 @@ struct ar_comm {
   bool dyn = true;                             // dynamic tile scheduling of CPS-shaped plans (AR_DYN=0: off)
   unsigned int *flat_ctr = nullptr;            // ar_flat_kernel tile counters (local comms)
   unsigned int *fs_bar = nullptr;              // ar_flatsteps_kernel grid-barrier words (local comms)
-  bool flatsteps = true;                       // emulated multi-step plans via ar_flatsteps_kernel (AR_FLATSTEPS=0: off)
+  // emulated multi-step plans via ar_flatsteps_kernel (AR_FLATSTEPS=1; off by default: measured
+  // equal in bf16 and 10-14 % slower in fp32 than the step-table kernel, whose range waits let
+  // dependent steps overlap CTA by CTA — profiles/round2/README.md §17)
+  bool flatsteps = false;
   // low-latency one-shot path (ar_ll_kernel): scratch [parity][src][cap_lines] 16-byte lines
   long long ll_max_bytes = 0;                  // largest message sent this way (AR_LL_MAX_KB; 0 = off)
   long long ll_cap_lines = 0;
@@ -2109,7 +2114,7 @@ static void init_comm(ar_comm *c) {
   if (const char *v = std::getenv("AR_JITTER_NS")) c->jitter_ns = (unsigned int)std::strtoul(v, nullptr, 10);
   if (const char *v = std::getenv("AR_LAUNCH")) c->plain_launch = std::string(v) == "plain";
   if (const char *v = std::getenv("AR_FLAT")) c->flat = std::string(v) != "0";
-  if (const char *v = std::getenv("AR_FLATSTEPS")) c->flatsteps = std::string(v) != "0";
+  if (const char *v = std::getenv("AR_FLATSTEPS")) c->flatsteps = std::string(v) == "1";
   if (const char *v = std::getenv("AR_DYN")) c->dyn = std::string(v) != "0";
   if (const char *v = std::getenv("AR_ENTRY_FENCE")) c->entry_fence = std::string(v) == "1";
   if (!c->local && c->rpp == 1) {

@@ -396,10 +396,10 @@ def test_exec_host_end_to_end(force, dtype):
 @pytest.mark.parametrize("flatsteps", ["1", "0"])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_multi_step_kernels(flatsteps, dtype, monkeypatch):
-    """Emulated multi-step plans run on ar_flatsteps_kernel (every step's ops of all ranks over
-    every SM, grid barriers between steps); AR_FLATSTEPS=0 keeps them on the step-table kernel
-    and its per-rank flags — both with the plan's bits: every kind, ragged sizes, SUM and AVG,
-    back-to-back calls (the barrier words must be back at zero), specials."""
+    """Emulated multi-step plans run on the step-table kernel and its per-rank flags; the A/B
+    option AR_FLATSTEPS=1 runs them on ar_flatsteps_kernel (every step's ops of all ranks over
+    every SM, grid barriers between steps) — both with the plan's bits: every kind, ragged
+    sizes, SUM and AVG, back-to-back calls (the barrier words must be back at zero), specials."""
     monkeypatch.setenv("AR_FLATSTEPS", flatsteps)
     kern = "ar_flatsteps_kernel" if flatsteps == "1" else "ar_exec_kernel"
     for force in ("ring", "rhd", "hcps:4,2", "hcps:2,2,2"):
