@@ -142,6 +142,15 @@ __device__ __forceinline__ uint32_t f2bf(float f) {
   if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FC0u | ((u >> 16) & 0x8000u);
   return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
 }
+// Two fp32 values to a bf16 pair (lo in the low half), round-to-nearest-even in one
+// instruction: the same bits as f2bf for every non-NaN input (finite, subnormal, overflow to
+// inf); a NaN becomes the canonical NaN (payload and sign are not part of the contract: Q2,
+// the tests compare NaNs by isnan)
+__device__ __forceinline__ uint32_t f2bf2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 
 // ------------------------------------------------------------------ reduction core
 // Accumulate one 16-byte vector of source s into acc (fp32).  First source initialises.
@@ -171,10 +180,10 @@ template <bool BF16>
 __device__ __forceinline__ uint4 acc_pack(const float (&acc)[8]) {
   uint4 o;
   if (BF16) {
-    o.x = f2bf(acc[0]) | (f2bf(acc[1]) << 16);
-    o.y = f2bf(acc[2]) | (f2bf(acc[3]) << 16);
-    o.z = f2bf(acc[4]) | (f2bf(acc[5]) << 16);
-    o.w = f2bf(acc[6]) | (f2bf(acc[7]) << 16);
+    o.x = f2bf2(acc[0], acc[1]);
+    o.y = f2bf2(acc[2], acc[3]);
+    o.z = f2bf2(acc[4], acc[5]);
+    o.w = f2bf2(acc[6], acc[7]);
   } else {
     o.x = __float_as_uint(acc[0]); o.y = __float_as_uint(acc[1]);
     o.z = __float_as_uint(acc[2]); o.w = __float_as_uint(acc[3]);
@@ -1213,8 +1222,8 @@ __global__ void __launch_bounds__(kThreads) ar_ll_kernel(const __grid_constant__
       for (int j = 0; j < per; j++) acc[j] = __fdiv_rn(acc[j], (float)a.avg_n);
     uint2 o;
     if (bf16) {
-      o.x = f2bf(acc[0]) | (f2bf(acc[1]) << 16);
-      o.y = f2bf(acc[2]) | (f2bf(acc[3]) << 16);
+      o.x = f2bf2(acc[0], acc[1]);
+      o.y = f2bf2(acc[2], acc[3]);
     } else {
       o.x = __float_as_uint(acc[0]);
       o.y = __float_as_uint(acc[1]);
@@ -1361,7 +1370,7 @@ __device__ __forceinline__ void ll128_pack(const float (&acc)[8], unsigned long 
   uint32_t u[4];
   if (BF16) {
 #pragma unroll
-    for (int k = 0; k < 4; k++) u[k] = f2bf(acc[2 * k]) | (f2bf(acc[2 * k + 1]) << 16);
+    for (int k = 0; k < 4; k++) u[k] = f2bf2(acc[2 * k], acc[2 * k + 1]);
   } else {
 #pragma unroll
     for (int k = 0; k < 4; k++) u[k] = __float_as_uint(acc[k]);
