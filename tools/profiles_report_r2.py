@@ -578,10 +578,40 @@ def flatsteps_section(out):
     out.append("")
     out.append("Barriers between steps cost what the step-table kernel's range waits save: dependent steps there "
                "overlap CTA by CTA (fp32 reaches 0.97–0.98 of the copy peak on Ring / RHD), while the grid-wide "
-               "barrier serialises them (0.86–0.88).  In bf16 both sit at 0.83–0.89 — the same bytes run at 0.98 in "
-               "fp32, which does half the element work per byte, so the 2-source bf16 reduce is most likely limited "
-               "by the consumer warps' unpack/add/round work rather than by the schedule (not profiled further).  ar_flatsteps_kernel stays "
+               "barrier serialises them (0.86–0.88).  In bf16 both sat at 0.83–0.89 — the same bytes ran at 0.98 in "
+               "fp32, which does half the element work per byte: the 2-source bf16 reduce was limited by the "
+               "consumer warps' work, and packing the sums with one `cvt.rn.bf16x2.f32` per pair instead of a "
+               "bitwise RNE per element lifted it to 0.94–0.98 (§18).  ar_flatsteps_kernel stays "
                "an A/B option (AR_FLATSTEPS=1), off by default; its bits are tested (`pytest_exec.log`).\n")
+
+
+def bf16pack_section(out):
+    import glob
+    files = sorted(glob.glob(os.path.join(P, "bf16pack", "bench_*_bf16.json")))
+    if not files:
+        return
+    old = {}
+    for f in glob.glob(os.path.join(P, "flatsteps", "bench_*_bf16_fs0.json")):
+        d = jload(f)
+        if d:
+            old[os.path.basename(f)[6:-len("_bf16_fs0.json")]] = d
+    out.append("## 18. bf16 stores packed with `cvt.rn.bf16x2.f32` (bench N = 1, 8 ranks × 256 MiB bf16)\n")
+    out.append("`bf16pack/`: `python bench.py [--force K] --no-cpu-baseline --no-e2e` on the build that packs each "
+               "pair of fp32 sums with one `cvt.rn.bf16x2.f32` (the same RNE bits for every non-NaN value; the GPU "
+               "suite `pytest_gpu_1gpu.log` incl. subnormal/overflow/inf/NaN inputs passes) against the bitwise RNE "
+               "of the previous build (§17's step-table column).  HBM roofline fraction and the held-out "
+               "GenModel error of the A6e prediction.\n")
+    out.append("| plan | before: ms (frac, pred. err) | after: ms (frac, pred. err) |")
+    out.append("|---|---|---|")
+    for f in files:
+        d = jload(f)
+        if not d:
+            continue
+        k = os.path.basename(f)[6:-len("_bf16.json")]
+        o = old.get(k)
+        cell = lambda x: f"{x['ms_per_step']:.3f} ({x['roofline']['frac']:.3f}, {x['genmodel']['pred_err']:.1%})"
+        out.append(f"| {k} | {cell(o) if o else '-'} | {cell(d)} |")
+    out.append("")
 
 
 def main():
@@ -610,6 +640,7 @@ def main():
     c2_genmodel_section(out)
     ragged_section(out)
     flatsteps_section(out)
+    bf16pack_section(out)
     print("\n".join(out))
 
 
