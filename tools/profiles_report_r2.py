@@ -93,7 +93,7 @@ def c2_section(out):
                " kernel above — §12); NCCL Ring / NVLS-off: separate processes with the variable set"
                " (`c2_*_ncclring`, `c2_*_ncclnvlsoff`).  Earlier runs: `final_c2_*` (LL128 only above the one-shot"
                " cut-off, to 16 MiB), `c2_n*_f32.jsonl` (before the LL128 path).\n")
-    for n in (4, 2):
+    for n in (4, 3, 2):
         ours = final_c2(n, "f32") or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
         if not ours:
             continue
@@ -119,26 +119,28 @@ def c2_section(out):
                     return d[b]["busbw_med"] if b in d else float("nan")
                 pick = f"{v(gn):.1f} ({gn[b]['chosen']})" if b in gn else "-"
                 best = max(x for x in (v(nd), v(nr), v(no)) if x == x) if any(b in d for d in (nd, nr, no)) else float("nan")
-                out.append(f"| {size(b)} | {v(g):.1f} | {pick} | {v(nv):.1f} | {v(nd):.1f} | {v(nr):.1f} | {v(no):.1f} | "
-                           f"{v(g) / v(nr):.2f} | {(v(gn) / best) if b in gn else float('nan'):.2f} |")
+                f1 = lambda x: f"{x:.1f}" if x == x else "-"
+                f2 = lambda x: f"{x:.2f}" if x == x else "-"
+                out.append(f"| {size(b)} | {f1(v(g))} | {pick} | {f1(v(nv))} | {f1(v(nd))} | {f1(v(nr))} | {f1(v(no))} | "
+                           f"{f2(v(g) / v(nr))} | {f2((v(gn) / best) if b in gn else float('nan'))} |")
             out.append("")
 
 
 def bf16_section(out):
-    rows4 = final_c2(4, "bf16")
-    if not rows4:
+    ns = [n for n in (4, 3, 2) if final_c2(n, "bf16")]
+    if not ns:
         return
     out.append("**bf16, graph timing, final executor: GenTree plan vs NCCL default (busbw GB/s)**\n")
-    out.append("| size | GenTree N=4 | NCCL N=4 | ratio | GenTree N=2 | NCCL N=2 | ratio |")
-    out.append("|---|---|---|---|---|---|---|")
+    out.append("| size | " + " | ".join(f"GenTree N={n} | NCCL N={n} | ratio" for n in ns) + " |")
+    out.append("|---|" + "---|---|---|" * len(ns))
     d = {}
-    for n in (4, 2):
+    for n in ns:
         rows = final_c2(n, "bf16")
         d[n] = ({r["bytes"]: r["busbw_med"] for r in rows if r["impl"] == "ours"},
                 {r["bytes"]: r["busbw_med"] for r in rows if r["impl"] == "nccl"})
-    for b in sorted(d[4][0]):
+    for b in sorted(d[ns[0]][0]):
         cells = []
-        for n in (4, 2):
+        for n in ns:
             g, c = d[n]
             cells += [f"{g.get(b, float('nan')):.1f}", f"{c.get(b, float('nan')):.1f}", f"{g.get(b, float('nan')) / c.get(b, float('nan')):.2f}"]
         out.append(f"| {size(b)} | " + " | ".join(cells) + " |")
@@ -149,7 +151,7 @@ def pick_section(out):
     """The final build's "GenTree incl. NVLS" column: the min-GenModel pick with the plan side
     predicted on the row of the path the executor takes (gentree_plan_nvls with the OS1 and
     LL128 rows)."""
-    for n in (4, 2):
+    for n in (4, 3, 2):
         final = final_c2(n, "f32")
         pk = [r for r in final if r.get("plan") == "gentree+nvls"] or jl(os.path.join(P, "c2", f"c2pick_n{n}_f32.jsonl"))
         base = final or jl(os.path.join(P, "c2", f"c2_n{n}_f32.jsonl"))
