@@ -119,7 +119,7 @@ def check(sp, world, count, dtype, force, mode="gradient", op="sum", calls=1, ex
     return got
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_flag_path_all_kinds(world, dtype):
     """ar_exec_kernel with .sys flags: every plan kind, ragged count (> one-shot cut-off; the
@@ -127,23 +127,26 @@ def test_flag_path_all_kinds(world, dtype):
     count = 1_000_003 if dtype == "f32" else 2_000_003
     sp = SameProcess(world, count * 4, env={"AR_LL128_MAX_KB": "0"})
     try:
-        kinds = [None, "cps", "ring", "rb"] + (["rhd", "hcps:2,2"] if world == 4 else ["rhd"])
+        kinds = [None, "cps", "ring", "rb"] + {4: ["rhd", "hcps:2,2"], 8: ["rhd", "hcps:4,2"]}.get(world, ["rhd"])
         for force in kinds:
             check(sp, world, count, dtype, force, expect_kernel="ar_exec_kernel")
     finally:
         sp.destroy()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_oneshot_path(world, dtype):
-    """ar_ll_kernel (small messages, CPS-shaped plans): bit-identical to the plan's bits."""
+    """ar_ll_kernel (small messages, CPS-shaped plans, up to the LL128 floor): bit-identical to
+    the plan's bits."""
+    es = 4 if dtype == "f32" else 2
+    top = min(60001, G.default_paths(world)["ll128_min"] // es - 1)
     sp = SameProcess(world, 1 << 20)
     try:
-        for count in (1, 7, 4093, 60001):
+        for count in (1, 7, 4093, top):
             check(sp, world, count, dtype, None, expect_kernel="ar_ll_kernel")
         if world > 2:   # multi-step plans never take the one-shot path (at N = 2 Ring ≡ CPS)
-            check(sp, world, 60001, dtype, "ring", expect_kernel="ar_exec_kernel")
+            check(sp, world, top, dtype, "ring", expect_kernel="ar_exec_kernel")
     finally:
         sp.destroy()
 
@@ -296,7 +299,7 @@ def test_unverified_plan_is_refused():
         comm.destroy()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_ll128_path(world, dtype):
     """ar_ll128_kernel (CPS-shaped plans between the LL128 floor and ceiling): the CPS plan's RS
@@ -399,7 +402,7 @@ def test_multi_level_same_process(nproc, R):
             c.destroy()
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 def test_path_choice_follows_the_cutoffs(world):
     """The executor's path for CPS-shaped plans follows the communicator's cut-offs
     (ar_comm_get_paths = ar_default_paths by default): LL128 in (ll128_min, ll128_max] — any
