@@ -280,12 +280,14 @@ uint64_t ar_rank_stride_bytes(uint64_t count, int32_t dtype);
  * and the tile counters (dynamic tile scheduling of CPS-shaped plans) that the
  * previous launch left.  Every element of every rank's buffer ends
  * equal to the plan's left-to-right fp32 sum of the ranks' inputs (bit-exact to the CPU
- * oracle).  One rank per GPU, CPS-shaped plans take a flag-free path by size: the one-shot
- * LL128 two-shot kernel (flags inside 128-byte lines, its own block partition: any count,
+ * oracle).  One rank per GPU, CPS-shaped plans take a flag-free path by size: the LL128
+ * two-shot kernel (flags inside 128-byte lines, its own block partition: any count,
  * 8-byte-aligned buffer) when the message lies in its range (ar_comm_get_paths), else the
- * one-shot kernel up
- * to the one-shot cut-off, else the step-table kernel — all with the plan's bits (ar_comm_last_kernel tells which).  Errors: AR_EINVAL for plan/comm world mismatch, count/dtype different from the
- * plan's, unregistered or misaligned buffer; AR_ESYS on launch failure. */
+ * one-shot kernel up to the one-shot cut-off, else the step-table kernel — all with the
+ * plan's bits (ar_comm_last_kernel tells which); the flag-free paths need no registration but
+ * a buffer that holds count elements.  Errors: AR_EINVAL for plan/comm world mismatch,
+ * count/dtype different from the plan's, unregistered, too small or misaligned buffer; AR_ESYS
+ * on launch failure. */
 int allreduce_exec(const gt_plan *plan, ar_comm *comm, void *dptr, uint64_t count, int32_t dtype,
                    void *stream);
 
