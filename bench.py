@@ -171,20 +171,31 @@ def busbw(bytes_per_rank, ranks, seconds):
 
 # ----------------------------------------------------------------------------- CPU oracle legs
 
-def oracle_sample_time(world, dtype, count, force, p):
-    """The oracle (as it stands) simulating the same plan kind on a bounded sample."""
+def oracle_sample(world, dtype, count, force, p):
+    """The oracle's plan and seeded inputs for a bounded sample (built once, outside the timing)."""
     from oracle import genmodel as OG
     from oracle import gentree as GT
-    from oracle import simulate as SM
     from oracle import topology as T
     from synth import generator as GEN
     t = T.parse_topology(single_switch_doc(world, p))
     op = OG.Params(p["alpha"], p["beta"], p["gamma"], p["delta"], p["epsilon"], int(p["w_t"]))
     plan, _ = GT.gentree(t, count, 2 if dtype == "bf16" else 4, params=op, force=force)
-    xs = GEN.generate_all(GEN.config_seed(4), world, count, dtype)
+    return plan, GEN.generate_all(GEN.config_seed(4), world, count, dtype)
+
+
+def oracle_step_time(sample, dtype):
+    """One step of the oracle (as it stands): its step-by-step simulation of the plan on the
+    sample (simulate copies its inputs, so the sample can be reused)."""
+    from oracle import simulate as SM
+    plan, xs = sample
     t0 = time.perf_counter()
     SM.simulate(plan, xs, dtype)
     return time.perf_counter() - t0
+
+
+def oracle_sample_time(world, dtype, count, force, p):
+    """The oracle (as it stands) simulating the same plan kind on a bounded sample."""
+    return oracle_step_time(oracle_sample(world, dtype, count, force, p), dtype)
 
 
 def host_info():
@@ -246,7 +257,12 @@ def run_reference(args):
     world = args.ranks if n == 1 else n
     p, p_src = model_params(world, emulated=n == 1)
     es = 2 if args.dtype == "bf16" else 4
-    count = int(args.cpu_sample_mib * MIB) // es
+    # every one of the --warmup W + --steps K steps simulates the whole plan on a bounded sample;
+    # the sample shrinks as K + W grows so the run stays within a few minutes (1.4 s per step at
+    # 64 MiB per rank x 8 ranks on the GPU box's host: K + W <= 16 keeps the full sample)
+    calls = max(1, args.steps) + max(0, args.warmup)
+    sample_mib = args.cpu_sample_mib * min(1.0, 16.0 / calls)
+    count = max(world * 64, int(sample_mib * MIB) // es // 256 * 256)
     from oracle import gentree as GT
     from oracle import topology as T
     from oracle import genmodel as OG
@@ -254,26 +270,27 @@ def run_reference(args):
     _, reps = GT.gentree(T.parse_topology(single_switch_doc(world, p)), args.mib * MIB // es, es, params=op,
                          force=args.force)
     chosen = reps[-1].chosen
+    sample = oracle_sample(world, args.dtype, count, args.force, p)
     def run():
-        for _ in range(min(args.warmup, 1)):
-            oracle_sample_time(world, args.dtype, count, args.force, p)
-        return [oracle_sample_time(world, args.dtype, count, args.force, p) for _ in range(max(1, min(args.steps, 3)))]
+        for _ in range(max(0, args.warmup)):
+            oracle_step_time(sample, args.dtype)
+        return [oracle_step_time(sample, args.dtype) for _ in range(max(1, args.steps))]
     times, core = pinned_one_core(run)
     t = sum(times) / len(times)
     v = busbw(count * es, world, t)
     line = {"impl": "reference", "metric": "allreduce_busbw", "value": round(v, 4), "unit": "GB/s",
-            "n_gpus": n, "steps": len(times), "warmup": min(args.warmup, 1), "ms_per_step": round(t * 1e3, 3),
+            "n_gpus": n, "steps": len(times), "warmup": max(0, args.warmup), "ms_per_step": round(t * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic",
             "config": arm_config(args, n, world, chosen, p_src),
-            "note": (f"the reference arm is the CPU oracle (no reference implementation exists); it runs "
-                     f"{len(times)} timed steps after {min(args.warmup, 1)} warm-up on a bounded sample so the "
-                     f"run ends in minutes — steps/warmup deliberately differ from the GPU arm's"),
+            "note": (f"the reference arm is the CPU oracle (no reference implementation exists); it runs the "
+                     f"same {len(times)} timed steps after {max(0, args.warmup)} warm-up as the GPU arm, each on a "
+                     f"bounded sample ({count * es / MIB:g} MiB per rank) so the run ends in minutes"),
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                              "pinned_core": core, **host_info(),
                              "sample": f"each step: the oracle's step-by-step simulation of the same plan on a "
                                        f"bounded sample, {world} ranks x {count} {args.dtype} elements "
-                                       f"({args.cpu_sample_mib:g} MiB/rank), numpy single-threaded"},
+                                       f"({count * es / MIB:g} MiB/rank), numpy single-threaded"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

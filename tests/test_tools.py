@@ -37,3 +37,19 @@ def test_nvlcounters_summary():
     s = summarize({"gpm_tx": 4000, "gpm_rx": 2000, "xmit_bytes": 0, "rcv_bytes": 0}, 4, 1000)
     assert s["counters"] == "nvml gpm_tx/gpm_rx" and s["tx_bytes_per_step"] == 1000
     assert summarize({"host_window_s": 1.0}, 1, 1)["counters"] == "none answered"
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the CPU oracle as the reference arm) runs exactly the
+    --steps K / --warmup W it is given and prints one JSON line with the contract's keys."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "2",
+                          "--warmup", "1", "--cpu-sample-mib", "1"], capture_output=True, text=True, cwd=ROOT,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 1
+    assert d["metric"] == "allreduce_busbw" and d["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
+    assert d["e2e"] == {"value": d["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
