@@ -331,6 +331,10 @@ def main():
     # prediction below is held out; the fit's validation summary is carried into the line.
     fp = fitted_params(emulated=n == 1) or NOMINAL
     pred_src = ("fitted " + fp["source"]) if "source" in fp else "nominal"
+    if n == 1 and chosen != "cps" and "step_table_row" in fp:
+        # a multi-step plan runs on the step-table kernel, not ar_flat_kernel: that path's row
+        fp = {**fp["step_table_row"], "validation": fp.get("validation")}
+        pred_src += " (step-table kernel row)"
     gp = G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"], fp["epsilon"], int(fp["w_t"]))
     pred = (plan.predict_executed_shared(gp) if n == 1 else plan.predict_executed(gp))["total"]
     seed = 0x240904202 ^ 4

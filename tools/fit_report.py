@@ -108,34 +108,58 @@ def fit_nvlink(a, cps, val):
                     "held_out_bytes": sorted(hold)}, out_rows
 
 
-def fit_shared(a, cps, val):
+def _nnls_shared(rows, stat):
+    """(α, γ, δ) by NNLS on T = A·α + C·γ + D·δ, the shared coefficients of each row's plan."""
     from scipy.optimize import nnls
-    rows = [r for r in cps if r["bytes"] >= a.min_bytes and r["n"] < a.holdout_n]
     X, t = [], []
     for r in rows:
-        plan = plan_for("cps", r["n"], r["bytes"], r["dtype"])
+        plan = plan_for(r["plan"], r["n"], r["bytes"], r["dtype"])
         # the shared coefficients' A, C, D: read back through unit parameters (bit-exact
         # per-step sums of the library's A6e evaluation)
         ua = plan.predict_executed_shared(G.params(1.0, 0, 0, 0, 0, 1))["latency"]
         uc = plan.predict_executed_shared(G.params(0, 0, 1.0, 0, 0, 1))["compute"]
         ud = plan.predict_executed_shared(G.params(0, 0, 0, 1.0, 0, 1))["memory"]
         X.append([ua, uc, ud])
-        t.append(r["t_mean"])
-    x, res = nnls(np.array(X), np.array(t))
+        t.append(r[stat])
+    return nnls(np.array(X), np.array(t))
+
+
+def fit_shared(a, cps, val):
+    rows = [r for r in cps if r["bytes"] >= a.min_bytes and r["n"] < a.holdout_n]
+    x, res = _nnls_shared(rows, a.stat)
     gp = G.params(x[0], 0.0, x[1], x[2], 0.0, 1 << 20)
+    # executor-path rows (as over NVLink, DESIGN §10): CPS-shaped plans run on ar_flat_kernel,
+    # every multi-step plan on the step-table kernel (static slices, flags between steps) —
+    # with --multistep, that kernel gets its own (α, γ, δ), fitted on multi-step rows of rank
+    # counts below --holdout-n (never the validated rank count)
+    gs, xs, ms_rows = None, None, []
+    if a.multistep:
+        ms_rows = [r for r in load(a.multistep, a.timing) if r["plan"] not in ("cps", "gentree")
+                   and r["bytes"] >= a.min_bytes and r["n"] < a.holdout_n]
+        xs, res_s = _nnls_shared(ms_rows, a.stat)
+        gs = G.params(xs[0], 0.0, xs[1], xs[2], 0.0, 1 << 20)
     out_rows = []
     for r in val:
         if r["bytes"] < a.min_bytes:
             continue
         plan = plan_for(r["plan"], r["n"], r["bytes"], r["dtype"])
-        pg = plan.predict_executed_shared(gp)["total"]
-        m = r["t_mean"]
-        out_rows.append({"plan": r["plan"], "executed": plan.report()[-1]["chosen"], "n": r["n"], "bytes": r["bytes"],
+        executed = plan.report()[-1]["chosen"]
+        path = "flat" if executed == "cps" or gs is None else "step_table"
+        pg = plan.predict_executed_shared(gp if path == "flat" else gs)["total"]
+        m = r[a.stat]
+        out_rows.append({"plan": r["plan"], "executed": executed, "path": path, "n": r["n"], "bytes": r["bytes"],
                          "dtype": r["dtype"], "measured_s": m, "genmodel_s": pg, "err_genmodel": abs(pg - m) / m})
     params = {"alpha": x[0], "beta": 0.0, "gamma": x[1], "delta": x[2], "epsilon": 0.0, "w_t": 1 << 20,
               "model": "shared (reading A6e)", "n_fit": sorted({r["n"] for r in rows})}
-    return params, {"fit_rows": len(rows), "params_per_byte": params, "fit_residual": res,
-                    "held_out_n": a.holdout_n}, out_rows
+    info = {"fit_rows": len(rows), "params_per_byte": params, "fit_residual": res, "held_out_n": a.holdout_n,
+            "stat": a.stat}
+    if gs is not None:
+        params["step_table_row"] = {"alpha": xs[0], "beta": 0.0, "gamma": xs[1], "delta": xs[2], "epsilon": 0.0,
+                                    "w_t": 1 << 20, "fit_rows": len(ms_rows),
+                                    "fit_plans": sorted({r["plan"] for r in ms_rows}),
+                                    "n_fit": sorted({r["n"] for r in ms_rows}), "fit_residual": res_s}
+        info["step_table_row"] = params["step_table_row"]
+    return params, info, out_rows
 
 
 def main():
@@ -149,6 +173,10 @@ def main():
     ap.add_argument("--fanin", default=None, help="harness fanin JSONL (C3-i, Eq. 6)")
     ap.add_argument("--shared", action="store_true", help="emulated ranks on one GPU (reading A6e)")
     ap.add_argument("--holdout-n", type=int, default=8, help="--shared: fit on rank counts below this")
+    ap.add_argument("--multistep", nargs="*", default=None,
+                    help="--shared: multi-step rows (e.g. Ring at 3..7 ranks) fitting the step-table kernel's row")
+    ap.add_argument("--stat", choices=["t_mean", "t_med"], default="t_mean",
+                    help="--shared: timing statistic fitted and compared")
     ap.add_argument("--holdout-bytes", type=int, nargs="*", default=None, help="CPS sizes never fitted")
     ap.add_argument("--wt-min", type=int, default=0, help="incast threshold lower bound (x-to-x probe)")
     ap.add_argument("--wt-max", type=int, default=0)
@@ -175,6 +203,7 @@ def main():
     summary = {"tag": a.tag, "timing": a.timing, "model": "shared" if a.shared else "executed", **info,
                "validation_rows": len(held),
                "genmodel_err": summarize(held, "err_genmodel"),
+               "genmodel_err_ge_64MiB": summarize([x for x in held if x["bytes"] >= 64 << 20], "err_genmodel"),
                "eq6_local_fanin": eq6, "rows": out_rows}
     if not a.shared:
         summary["abc_err"] = summarize(held, "err_abc")
@@ -187,7 +216,8 @@ def main():
         params.update({"source": f"genmodel_fit_{a.tag}.json",
                        "validation": {"rows": len(held), "median": summary["genmodel_err"]["median"],
                                       "max": summary["genmodel_err"]["max"],
-                                      "by_plan_max": summary["genmodel_err"]["by_plan_max"]},
+                                      "by_plan_max": summary["genmodel_err"]["by_plan_max"],
+                                      "ge_64MiB": {k: summary["genmodel_err_ge_64MiB"][k] for k in ("median", "max")}},
                        "note": "per byte; fitted on CPS rows only, validated on held-out plans/sizes"})
         with open(os.path.join(ROOT, "profiles", name), "w") as f:
             json.dump(params, f, indent=1)
