@@ -218,7 +218,10 @@ def main():
                                       "max": summary["genmodel_err"]["max"],
                                       "by_plan_max": summary["genmodel_err"]["by_plan_max"],
                                       "ge_64MiB": {k: summary["genmodel_err_ge_64MiB"][k] for k in ("median", "max")}},
-                       "note": "per byte; fitted on CPS rows only, validated on held-out plans/sizes"})
+                       "note": ("per byte; top level = ar_flat_kernel's row fitted on CPS rows, step_table_row = the "
+                                "step-table kernel's row fitted on multi-step rows; both below the validated rank "
+                                "count, validated on held-out plans/sizes/rank count" if "step_table_row" in params
+                                else "per byte; fitted on CPS rows only, validated on held-out plans/sizes")})
         with open(os.path.join(ROOT, "profiles", name), "w") as f:
             json.dump(params, f, indent=1)
     print(json.dumps({k: v for k, v in summary.items() if k != "rows"}, indent=1))
