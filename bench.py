@@ -331,8 +331,8 @@ def main():
     # prediction below is held out; the fit's validation summary is carried into the line.
     fp = fitted_params(emulated=n == 1) or NOMINAL
     pred_src = ("fitted " + fp["source"]) if "source" in fp else "nominal"
-    if n == 1 and chosen != "cps" and "step_table_row" in fp:
-        # a multi-step plan runs on the step-table kernel, not ar_flat_kernel: that path's row
+    if chosen != "cps" and "step_table_row" in fp:
+        # a multi-step plan runs as dependent steps on the step-table kernel: that path's row
         fp = {**fp["step_table_row"], "validation": fp.get("validation")}
         pred_src += " (step-table kernel row)"
     gp = G.params(fp["alpha"], fp["beta"], fp["gamma"], fp["delta"], fp["epsilon"], int(fp["w_t"]))

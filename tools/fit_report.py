@@ -85,27 +85,55 @@ def fit_nvlink(a, cps, val):
     abc = G.params(max(alpha3, 0.0), 0.0, 0.0, 0.0, 0.0, 1 << 20, combined=max(k3, 0.0))
     out_rows = []
     fit_keys = {(n, s) for n, s, _ in rows}
+    # executor-path rows: with --multistep, plans that run as several dependent
+    # steps on the step-table kernel get their own (α, β, δ), fitted by NNLS on the A6x
+    # coefficients of multi-step rows of rank counts below --holdout-n-nvlink (CPS-shaped
+    # plans, e.g. Ring / RHD at N = 2, stay on the CPS row)
+    st, st_info, st_keys = None, None, set()
+    if a.multistep:
+        from scipy.optimize import nnls
+        ms = [r for r in load(a.multistep, a.timing) if r["plan"] not in ("cps", "gentree") and r["bytes"] >= a.min_bytes
+              and r["n"] < a.holdout_n_nvlink
+              and plan_for(r["plan"], r["n"], r["bytes"], r["dtype"]).report()[-1]["chosen"] != "cps"]
+        X, tt = [], []
+        for r in ms:
+            plan = plan_for(r["plan"], r["n"], r["bytes"], r["dtype"])
+            X.append([plan.predict_executed(G.params(*u, 0.0, 1 << 20))["total"]
+                      for u in ((1.0, 0, 0, 0), (0, 1.0, 0, 0), (0, 0, 0, 1.0))])
+            tt.append(r["t_mean"])
+        xs, res_s = nnls(np.array(X), np.array(tt))
+        st = G.params(xs[0], xs[1], 0.0, xs[2], 0.0, 1 << 20)
+        st_keys = {(r["plan"], r["n"], r["bytes"]) for r in ms}
+        st_info = {"alpha": xs[0], "beta": xs[1], "gamma": 0.0, "delta": xs[2], "epsilon": 0.0, "w_t": 1 << 20,
+                   "fit_rows": len(ms), "fit_plans": sorted({r["plan"] for r in ms}),
+                   "n_fit": sorted({r["n"] for r in ms}), "fit_residual": res_s}
     for r in val:
         if r["bytes"] < a.min_bytes:
             continue
         plan = plan_for(r["plan"], r["n"], r["bytes"], r["dtype"])
-        pg = plan.predict_executed(fit)["total"]
+        on_st = st is not None and plan.report()[-1]["chosen"] != "cps"
+        pg = plan.predict_executed(st if on_st else fit)["total"]
         pa = plan.predict_executed(abc)["total"]
         ps = plan.predict(fit)["total"]
         m = r["t_mean"]
         in_fit = r["plan"] in ("cps", "gentree") and (r["n"], r["bytes"]) in fit_keys
         out_rows.append({"plan": r["plan"], "executed": plan.report()[-1]["chosen"], "n": r["n"], "bytes": r["bytes"],
                          "dtype": r["dtype"], "measured_s": m, "genmodel_s": pg, "abc_s": pa,
-                         "genmodel_paper_steps_s": ps, "cps_point_in_fit": in_fit,
+                         "genmodel_paper_steps_s": ps,
+                         "cps_point_in_fit": in_fit or (r["plan"], r["n"], r["bytes"]) in st_keys,
+                         "path": "step_table" if on_st else "cps",
                          "err_genmodel": abs(pg - m) / m, "err_abc": abs(pa - m) / m,
                          "err_genmodel_paper_steps": abs(ps - m) / m})
     p = fit.as_dict()
     params = {"alpha": p["alpha"], "beta": p["combined"] / 2 if p["has_combined"] else p["beta"],
               "gamma": 0.0 if p["has_combined"] else p["gamma"], "delta": p["delta"], "epsilon": p["epsilon"],
               "w_t": p["w_t"], "n_max_fit": nmax}
-    return params, {"fit_rows": len(rows), "params_per_byte": p, "fit_sse": sse,
-                    "abc_params": {"alpha": abc.alpha, "combined": abc.combined},
-                    "held_out_bytes": sorted(hold)}, out_rows
+    info = {"fit_rows": len(rows), "params_per_byte": p, "fit_sse": sse,
+            "abc_params": {"alpha": abc.alpha, "combined": abc.combined}, "held_out_bytes": sorted(hold)}
+    if st_info is not None:
+        params["step_table_row"] = st_info
+        info["step_table_row"] = st_info
+    return params, info, out_rows
 
 
 def _nnls_shared(rows, stat):
@@ -175,6 +203,8 @@ def main():
     ap.add_argument("--holdout-n", type=int, default=8, help="--shared: fit on rank counts below this")
     ap.add_argument("--multistep", nargs="*", default=None,
                     help="--shared: multi-step rows (e.g. Ring at 3..7 ranks) fitting the step-table kernel's row")
+    ap.add_argument("--holdout-n-nvlink", type=int, default=4,
+                    help="--multistep over NVLink: fit the step-table row on rank counts below this")
     ap.add_argument("--stat", choices=["t_mean", "t_med"], default="t_mean",
                     help="--shared: timing statistic fitted and compared")
     ap.add_argument("--holdout-bytes", type=int, nargs="*", default=None, help="CPS sizes never fitted")
@@ -218,9 +248,9 @@ def main():
                                       "max": summary["genmodel_err"]["max"],
                                       "by_plan_max": summary["genmodel_err"]["by_plan_max"],
                                       "ge_64MiB": {k: summary["genmodel_err_ge_64MiB"][k] for k in ("median", "max")}},
-                       "note": ("per byte; top level = ar_flat_kernel's row fitted on CPS rows, step_table_row = the "
-                                "step-table kernel's row fitted on multi-step rows; both below the validated rank "
-                                "count, validated on held-out plans/sizes/rank count" if "step_table_row" in params
+                       "note": ("per byte; top level = the CPS-shaped plans' row fitted on CPS rows, step_table_row = "
+                                "the multi-step plans' (step-table kernel's) row fitted on multi-step rows of rank "
+                                "counts below the validated one; validated on held-out plans/sizes/rank counts" if "step_table_row" in params
                                 else "per byte; fitted on CPS rows only, validated on held-out plans/sizes")})
         with open(os.path.join(ROOT, "profiles", name), "w") as f:
             json.dump(params, f, indent=1)
