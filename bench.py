@@ -292,13 +292,35 @@ def run_reference(args):
                                        f"bounded sample, {world} ranks x {count} {args.dtype} elements "
                                        f"({count * es / MIB:g} MiB/rank), numpy single-threaded"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------------------- GPU arm
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line on stdout (everything else — e.g. NCCL's C-level version banner — was
+    moved to stderr by keep_stdout_for_json)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def keep_stdout_for_json():
+    """Reserve the process's stdout for the JSON line: keep a duplicate of fd 1 for emit() and
+    point fd 1 at stderr, so libraries printing to stdout (NCCL prints its version there) cannot
+    add lines the driver would have to skip."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
 def main():
     args = parse_args()
+    keep_stdout_for_json()
     if args.impl == "reference":
         run_reference(args)
         return
@@ -572,7 +594,7 @@ def main():
         line["vs_nccl"] = {k: round(value / v["busbw"], 3) for k, v in nccl.items() if isinstance(v, dict)}
     if nvls:
         line["nvls"] = nvls
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
