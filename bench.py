@@ -46,6 +46,9 @@ def parse_args():
     ap.add_argument("--ranks", type=int, default=8, help="emulated ranks when --gpus 1")
     ap.add_argument("--force", default=None, help="plan kind instead of GenTree (cps, ring, rhd, rb, hcps:a,b)")
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--cpu-timing-plan", action="store_true",
+                    help="run SURVEY §8(d)'s CPU-oracle timing plan (C1, C2, C4 data simulation; C1/C5 plan "
+                         "generation, oracle and library) pinned to one core, print JSONL, exit")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
@@ -297,6 +300,80 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 
+def cpu_timing_plan(core=0, reps=2):
+    """SURVEY §8(d) / BASELINE.md §6 CPU-oracle timing plan (the cpu_baseline leg, widened): the
+    oracle as it stands, pinned to ONE core, on the BASELINE.json configs — JSONL on stdout.
+
+      C1  4 ranks, 1 MiB fp32 per rank, GenTree plan on the 2-level tree (Table 5 links): plan
+          generation + step-by-step simulation + GenModel prediction
+      C2  8 ranks, fp32, 16 MiB and 256 MiB per rank, GenTree plan (CPS) on one switch
+      C4  8 ranks, bf16, 256 MiB per rank (bench.py's workload), GenTree plan (CPS)
+      plan generation (host µs): the oracle's GenTree and the library's gentree_plan, and the
+          GenModel evaluation of the plan (oracle predict_plan, library genmodel_predict_executed),
+          on C1 and on C5 (64 ranks = 8 x 8, 2-level tree) at 1e7 / 3.2e7 / 1e8 / 3.2e8 floats
+    Input generation is outside every timing."""
+    import platform
+    os.sched_setaffinity(0, {core})          # one core (numpy's elementwise adds are serial)
+    from oracle import gentree as GT
+    from oracle import simulate as SM
+    from oracle import topology as T
+    from synth import generator as GEN
+    import paper_2409_04202_b200 as G
+    host = {**host_info(), "pinned_core": core, "cores": 1, "python": platform.python_version()}
+    nominal = {"alpha": 3e-6, "beta": 4 / 900e9, "epsilon": 0.0, "w_t": 9}
+    comp = {"gamma": 0.0, "delta": 4 / 6.54e12}
+    c1 = T.two_level_doc([2, 2], T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    cases = [("C1", c1, 4, MIB, "f32"),
+             ("C2", T.single_switch_doc(8, nominal, comp), 8, 16 * MIB, "f32"),
+             ("C2", T.single_switch_doc(8, nominal, comp), 8, 256 * MIB, "f32"),
+             ("C4", T.single_switch_doc(8, nominal, comp), 8, 256 * MIB, "bf16")]
+    for cfg, doc, n, nbytes, dtype in cases:
+        es = 4 if dtype == "f32" else 2
+        count = nbytes // es
+        topo = T.parse_topology(doc)
+        t0 = time.perf_counter()
+        plan, _ = GT.gentree(topo, count, es)
+        t_plan = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pred = GT.predict_plan(topo, plan, es)["total"]
+        t_pred = time.perf_counter() - t0
+        xs = GEN.generate_all(GEN.config_seed(4), n, count, dtype)
+        sims = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            SM.simulate(plan, xs, dtype)
+            sims.append(time.perf_counter() - t0)
+        t_sim = min(sims)
+        emit({"config": cfg, "ranks": n, "bytes_per_rank": nbytes, "dtype": dtype, "plan_steps": len(plan.steps),
+              "t_plan_s": t_plan, "t_predict_s": t_pred, "t_simulate_s": t_sim, "t_simulate_all_s": sims,
+              "oracle_busbw_gbs": busbw(nbytes, n, t_sim), "genmodel_pred_s": pred, **host})
+        del xs
+    c5 = T.two_level_doc([8] * 8, T.TABLE5["root_sw"], T.TABLE5["middle_sw"], T.TABLE5["server"])
+    for cfg, doc, n in (("C1", c1, 4), ("C5", c5, 64)):
+        topo = T.parse_topology(doc)
+        for floats in (10 ** 7, 32 * 10 ** 6, 10 ** 8, 32 * 10 ** 7):
+            row = {"config": cfg + "-plan", "ranks": n, "floats": floats}
+            for side in ("oracle", "library"):
+                ts, tp = [], []
+                for _ in range(max(1, reps)):
+                    t0 = time.perf_counter()
+                    if side == "oracle":
+                        plan, rep = GT.gentree(topo, floats, 4)
+                    else:
+                        lp = G.Plan.from_topology(doc, floats, "f32")
+                    ts.append(time.perf_counter() - t0)
+                    t0 = time.perf_counter()
+                    if side == "oracle":
+                        GT.predict_plan(topo, plan, 4)
+                    else:
+                        lp.predict()
+                    tp.append(time.perf_counter() - t0)
+                row[f"{side}_gentree_us"] = min(ts) * 1e6
+                row[f"{side}_predict_us"] = min(tp) * 1e6
+            row["chosen"] = [r["chosen"] for r in lp.report()]
+            emit({**row, **host})
+
+
 _JSON_OUT = None
 
 
@@ -321,6 +398,9 @@ def keep_stdout_for_json():
 def main():
     args = parse_args()
     keep_stdout_for_json()
+    if args.cpu_timing_plan:
+        cpu_timing_plan()
+        return
     if args.impl == "reference":
         run_reference(args)
         return

@@ -2,7 +2,7 @@
 every plan kind on 4 and 8 emulated ranks, fp32 and bf16, ragged sizes, SUM and AVG, through
 the step-table kernel, the flat kernel and local_reduce; results checked against the oracle.
 
-    compute-sanitizer --tool memcheck python tools/sanitize_probe.py
+    compute-sanitizer --tool memcheck python tests/sanitize_probe.py
 
 (compute-sanitizer is closed on the round-1 GPU pool; the probe alone runs every path once
 with bounded waits and oracle checks.)

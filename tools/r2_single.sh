@@ -15,5 +15,5 @@ step ncu_launches timeout 900 bash -c "ncu --metrics gpu__time_duration.sum --cl
 step ncu_full timeout 1200 bash -c "ncu --set full --clock-control none --import-source on -k regex:ar_flat_kernel -s 2 -c 1 -o $O/ncu_flat_emulated8_bf16_256MiB $B > $O/ncu_full.log 2>&1"
 step emu_cps timeout 900 bash -c "python tools/harness.py emu-cps --timing graph > $O/cps_emu.jsonl 2> $O/cps_emu.err"
 step emu_val timeout 1200 bash -c "python tools/harness.py emu-sweep --ranks 8 --timing graph --sizes 1048576 2097152 4194304 8388608 16777216 33554432 67108864 134217728 268435456 536870912 1073741824 > $O/val_emu8.jsonl 2> $O/val_emu8.err"
-step cpu_oracle timeout 1500 bash -c "python tools/cpu_oracle_timing.py > $O/cpu_oracle_timing.jsonl 2> $O/cpu_oracle_timing.err"
+step cpu_oracle timeout 1500 bash -c "python bench.py --cpu-timing-plan > $O/cpu_oracle_timing.jsonl 2> $O/cpu_oracle_timing.err"
 echo done >> $O/steps.txt
