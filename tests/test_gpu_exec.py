@@ -219,13 +219,15 @@ def test_cta_counts(ctas):
     run_emulated(single_switch(8), 8, 123457, "bf16", force="hcps:4,2", ctas=ctas)
 
 
-@pytest.mark.parametrize("mode", ["gradient", "specials"])
-def test_full_size_bench_config_full_buffer(mode):
+@pytest.mark.parametrize("mode,dtype", [("gradient", "bf16"), ("specials", "bf16"), ("gradient", "f32")])
+def test_full_size_bench_config_full_buffer(mode, dtype):
     """bench.py's N=1 workload in the launch configuration bench.py times: 8 emulated ranks,
-    bf16, 256 MiB per rank, GenTree plan (CPS) on ar_flat_kernel with dynamic tiles, bench's
-    seed — EVERY element of EVERY rank compared with the oracle's step-by-step simulation (a
-    single wrong tile anywhere fails), for gradient-shaped and special-value inputs."""
-    world, count, dtype = 8, 128 * 1024 * 1024, "bf16"
+    256 MiB per rank (bf16, and the `--dtype f32` line), GenTree plan (CPS) on ar_flat_kernel
+    with dynamic tiles, bench's seed — EVERY element of EVERY rank compared with the oracle's
+    step-by-step simulation (a single wrong tile anywhere fails), for gradient-shaped and
+    special-value inputs."""
+    es = 2 if dtype == "bf16" else 4
+    world, count = 8, (256 << 20) // es
     seed = 0x240904202 ^ 4
     doc = single_switch(world)
     plan = G.Plan.from_topology(doc, count, dtype)
@@ -238,12 +240,12 @@ def test_full_size_bench_config_full_buffer(mode):
     torch.cuda.synchronize()
     comm.async_error()
     assert comm.last_kernel() == "ar_flat_kernel"
-    oplan, _ = GT.gentree(T.parse_topology(doc), count, 2)
+    oplan, _ = GT.gentree(T.parse_topology(doc), count, es)
     assert OP.plan_to_json(oplan, dtype) == plan.to_json()
     want = SM.simulate(oplan, GEN.generate_all(seed, world, count, dtype, mode), dtype)
     host = buf.cpu().numpy()
     for r in range(world):
-        got = host[r * stride: r * stride + 2 * count].view(np.uint16)
+        got = host[r * stride: r * stride + es * count].view(np.uint16 if dtype == "bf16" else np.float32)
         assert_bits_equal(got, want[r], dtype, f"rank {r}")
     del host, want
 
