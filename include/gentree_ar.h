@@ -109,7 +109,9 @@ typedef struct gt_plan gt_plan; /* opaque, immutable, library-owned, thread-shar
  * depth-first pre-order.  params == NULL uses each link's own parameters from the
  * document; otherwise `params` is used for every link and server.  force_kind == NULL (or
  * "") runs GenTree's selection; otherwise every switch uses that kind ("cps", "ring",
- * "rhd", "hcps:f0,f1,..", or "rb" on a single-switch topology).  The plan is verified
+ * "rhd", "hcps:f0,f1,..", or "rb" on a single-switch topology); "norearrange" runs GenTree's
+ * selection without the data-rearrangement optimisation — tab:gentreesimu's
+ * GenTree*, "the special plan without data rearrangement".  The plan is verified
  * (conservation invariant) before it is returned.  *out must be released with
  * gt_plan_free.  Errors: AR_EINVAL on a malformed/invalid topology, count < 1, unknown
  * dtype or kind, or a forced kind that does not fit a switch. */

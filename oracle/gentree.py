@@ -149,7 +149,12 @@ def gentree(topo, count: int, esize: int, params: Params | None = None,
     """GenTree on `topo` for `count` elements of `esize` bytes.  Returns (Plan, reports).
 
     `force` (e.g. "ring", "hcps:4,2") restricts every switch's candidate set to that kind;
-    "rb" is only accepted on a single-switch topology (natural Reduce-Broadcast)."""
+    "rb" is only accepted on a single-switch topology (natural Reduce-Broadcast);
+    "norearrange" is tab:gentreesimu's GenTree* ("the special plan without data
+    rearrangement"): Algorithm 2 without its data-rearrangement step (P:705-715)."""
+    rearrange = force != "norearrange"
+    if not rearrange:
+        force = None
     N = len(topo.servers)
     if count < 1:
         raise PlanError("count must be >= 1")
@@ -200,7 +205,7 @@ def gentree(topo, count: int, esize: int, params: Params | None = None,
         rep = SwitchReport(nid, "")
         # ---- data rearrangement
         for ch in node.children:
-            if topo.nodes[ch].kind == "server":
+            if not rearrange or topo.nodes[ch].kind == "server":
                 continue
             ch_servers = topo.ranks_under(ch)
             ni = len(ch_servers)

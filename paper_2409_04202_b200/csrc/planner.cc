@@ -972,7 +972,11 @@ static std::vector<Step> build_acps(const std::map<int, std::set<int>> &init,
 }  // namespace
 
 PlanResult gentree(const Topology &t, int64_t count, int esize, const Params *explicit_params,
-                   const std::string &force) {
+                   const std::string &force_in) {
+  // "norearrange": GenTree* of tab:gentreesimu ("the special plan without data
+  // rearrangement") — Algorithm 2 with the data-rearrangement optimisation switched off
+  const bool rearrange = force_in != "norearrange";
+  const std::string force = rearrange ? force_in : std::string();
   const int N = (int)t.servers.size();
   if (count < 1) throw InvalidArg("count must be >= 1");
   const int64_t S = count * esize;
@@ -1088,7 +1092,7 @@ PlanResult gentree(const Topology &t, int64_t count, int esize, const Params *ex
     rep.sw = nd.id;
     // ---- data rearrangement (readings Q15/Q15b)
     for (int ch : nd.children) {
-      if (t.nodes[ch].server) continue;
+      if (!rearrange || t.nodes[ch].server) continue;
       std::vector<int> chs;
       t.servers_under(ch, chs);
       const int ni = (int)chs.size();

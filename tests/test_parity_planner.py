@@ -372,3 +372,30 @@ def test_nvls_plan_kind_parity():
     ring["switch_reduce"] = True
     with pytest.raises(G.ArInvalid):
         G.Plan.from_json(json.dumps(ring))
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 2, 2), (2, 3, 2, 3), (2, 4, 2, 2)])
+def test_gentree_star_without_rearrangement(shape):
+    """tab:gentreesimu's GenTree* ("the special plan without data rearrangement"):
+    force "norearrange" — library and oracle agree bit for bit, no child is rearranged, no
+    rearrangement moves (single-input reduces) appear, while GenTree does rearrange here.
+    (The rearrangement decision is local — transfer-out time of one child with vs without it,
+    P:705-715 — so the whole-plan GenModel can still price GenTree* lower; it does on these
+    small topologies, in both implementations alike.)"""
+    from tests.topologies import cross_dc
+    doc = cross_dc(*shape)
+    star, ostar = check_topology(doc, 10 ** 6, force="norearrange")
+    assert not any(r["rearranged_children"] for r in star.report())
+    assert not any(len(r.inputs) == 1 for st in ostar.steps for r in st.reduces)
+    full, _ = check_topology(doc, 10 ** 6)
+    assert any(r["rearranged_children"] for r in full.report())
+
+
+def test_gentree_star_equals_gentree_without_rearrangement():
+    """Where GenTree rearranges nothing, GenTree* is the same plan (byte-identical JSON)."""
+    for name, doc in _gtplan_topos().items():
+        for S in (10 ** 7, 10 ** 8):
+            a, _ = check_topology(doc, S)
+            if not any(r["rearranged_children"] for r in a.report()):
+                b, _ = check_topology(doc, S, force="norearrange")
+                assert a.to_json() == b.to_json()

@@ -7,7 +7,8 @@ Topologies of P:1100-1105 with Table 5's parameters (tab:gtcoe): se
 Middle-SW links, middle switches off Root-SW links, the two data centres' roots off one
 Cross-DC link; α per step taken as 3× the printed 6.58e-3 s (reading Q16: the only value that
 reproduces the single-switch rows and tab:gtplan's selections).  Sizes in floats (fp32).
-GenTree* (no data rearrangement) is not reproduced: the planner always considers it."""
+GenTree* (CDC384; "the special plan without data rearrangement", P:1147) is GenTree's
+selection with rearrangement switched off (gentree_plan force "norearrange")."""
 import argparse
 import json
 import os
@@ -34,7 +35,8 @@ PAPER = {   # tab:gentreesimu, seconds at 1e7 / 3.2e7 / 1e8 floats
     "SYM512": {"gentree": (0.639, 1.627, 4.638), "rhd": (0.896, 1.853, 4.812), "ring": (3.571, 4.479, 7.285),
                "cps": (3.479, 10.989, 34.200)},
     "ASY384": {"gentree": (0.570, 1.593, 4.670), "ring": (3.043, 3.947, 6.741), "cps": (2.052, 6.421, 19.925)},
-    "CDC384": {"gentree": (2.427, 8.299, 25.388), "ring": (8.513, 17.329, 44.580), "cps": (11.890, 37.799, 117.882)},
+    "CDC384": {"gentree": (2.427, 8.299, 25.388), "gentree*": (4.484, 13.927, 43.116), "ring": (8.513, 17.329, 44.580),
+               "cps": (11.890, 37.799, 117.882)},
 }
 SIZES = (10 ** 7, 32 * 10 ** 6, 10 ** 8)
 
@@ -89,8 +91,8 @@ def main():
             # baselines: "per-switch" = that kind at every switch of the tree (GenTree's
             # candidate set restricted to it); "flat" = one plan over all servers, routed on
             # the tree (the paper does not say which one its baselines are)
-            variants = [("gentree", None)] if alg == "gentree" else [("per-switch", alg)] + (
-                [("flat", alg)] if flat_ok else [])
+            variants = ([("gentree", None)] if alg == "gentree" else [("gentree", "norearrange")] if alg == "gentree*"
+                        else [("per-switch", alg)] + ([("flat", alg)] if flat_ok else []))
             for variant, kind in variants:
                 for S, pv in zip(SIZES, paper):
                     t0 = time.time()
@@ -115,8 +117,9 @@ def main():
     for name in {r["topo"] for r in rows}:
         for S in SIZES:
             g = next(r["sim_s"] for r in rows if r["topo"] == name and r["alg"] == "gentree" and r["floats"] == S)
+            # GenTree* is GenTree's own ablation: reported against GenTree, not a baseline
             base = {r["alg"] + "/" + r["variant"]: r["sim_s"] for r in rows
-                    if r["topo"] == name and r["alg"] != "gentree" and r["floats"] == S}
+                    if r["topo"] == name and r["alg"] not in ("gentree", "gentree*") and r["floats"] == S}
             claims[f"{name}@{S}"] = {"gentree_fastest": all(g <= v * (1 + 1e-12) for v in base.values()),
                                      "max_speedup": max(v / g for v in base.values())}
     json.dump({"rows": rows, "claims": claims, "alpha_per_step": A3}, open(a.out, "w"), indent=1)
