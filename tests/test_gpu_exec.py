@@ -343,6 +343,14 @@ def test_rearrangement_and_acps(shape):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_gentree_star_executes(dtype):
+    """tab:gentreesimu's GenTree* (force "norearrange") runs through the same executor
+    on the topology where GenTree rearranges: emulated ranks, bit-exact vs the oracle."""
+    from tests.topologies import cross_dc
+    run_emulated(cross_dc(2, 3, 2, 3), 12, 123457, dtype, force="norearrange")
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_emulated_cps_flag_protocol(dtype, monkeypatch):
     """Emulated CPS plans normally run flag-free (ar_flat_kernel); AR_FLAT=0 keeps them on the
     step-table kernel and its flag protocol — both must give the plan's bits."""
