@@ -674,6 +674,13 @@ def main():
         line["vs_nccl"] = {k: round(value / v["busbw"], 3) for k, v in nccl.items() if isinstance(v, dict)}
     if nvls:
         line["nvls"] = nvls
+        g = nvls.get("genmodel")
+        if g is not None and "busbw" in nvls and args.dtype == "f32" and not args.force:
+            # GenTree with the NVLS kind as a candidate (reading NV1, fp32 only: bit-exact there):
+            # GenModel's pick and the busbw this run measured for the picked path
+            line["gentree_incl_nvls"] = {"pick": "nvls" if g["use_nvls"] else chosen,
+                                         "busbw": nvls["busbw"] if g["use_nvls"] else round(value, 2),
+                                         "unit": "GB/s"}
     emit(line)
     if dist is not None:
         dist.barrier()
